@@ -1,0 +1,151 @@
+/*
+ * moeplace_cuda.h — C-ABI of the B200 (sm_100a) engine behind the `moeplace` hot path.
+ *
+ * The reference (arXiv 2508.09229, `moeplace` 0.1.0) is a pure-Python package whose hot-path
+ * operations are specified in /root/reference/SPEC.md; it ships no native code and no FFI.
+ * Each entry point below therefore replaces the CPU body of one SPEC operation; the Python
+ * package `paper_2508_09229_b200` (re-exported as `moeplace`) binds them with ctypes
+ * (see INTEGRATION.md).  Cited lines are SPEC.md:N.
+ *
+ * Conventions (all functions):
+ *   - Plain pointers and sizes only.  Device pointers are CUDA global-memory addresses; the
+ *     caller owns every buffer (inputs, outputs, scratch).  The library never allocates,
+ *     frees, or keeps global mutable state, and is safe to call concurrently on different
+ *     streams.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
+ *     function only ENQUEUES work; nothing synchronises the host.
+ *   - Integer outputs are ACCUMULATED (`+=`): the caller zeroes them.  This makes sharded
+ *     (multi-GPU, token-range) calls compose by plain addition.
+ *   - Return value: MP_OK, or an MP_ERR_* code describing a synchronous argument/launch
+ *     failure (the Python layer maps MP_ERR_ARG/MP_ERR_UNSUPPORTED to ConfigError,
+ *     MP_ERR_CUDA to RuntimeError).  Data errors found by a kernel are written to a caller
+ *     owned device `err` block (int64[4] = {code, layer, value, count}; code 0 = clean).
+ *
+ * Trace layout ("layer planes"): uint8 planes[L][plane_stride]; byte t*K+k of plane l is the
+ * k-th expert selected by token t in MoE layer l.  plane_stride and the
+ * base address must be multiples of 16.  Expert IDs are one byte, so E <= 256.
+ */
+#ifndef MOEPLACE_CUDA_H
+#define MOEPLACE_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_ABI_VERSION 1
+
+#define MP_OK 0
+#define MP_ERR_ARG 1          /* invalid argument (shape, range, alignment)        */
+#define MP_ERR_CUDA 2         /* CUDA launch/runtime failure                       */
+#define MP_ERR_UNSUPPORTED 3  /* outside the u8 device format (E > 256, p > 255)    */
+
+/* device err-block codes (err[0]) */
+#define MP_DATA_OK 0
+#define MP_DATA_EXPERT_RANGE 1   /* expert id >= E            err = {1, layer, id, count}          */
+#define MP_DATA_DUPLICATE 2      /* repeated id in one record err = {2, layer, token, count}       */
+#define MP_DATA_UNREACHABLE 3    /* BFS: disconnected graph   err = {3, src, dst, count}           */
+#define MP_DATA_UNPLACED 4       /* assign outside [0, S)     err = {4, layer, expert, count}      */
+#define MP_DATA_HOPS_RANGE 5     /* hop count > 255           err = {5, src, dst, count}           */
+
+/* ---- library identity ------------------------------------------------------------------- */
+int mp_abi_version(void);
+const char* mp_status_string(int status);
+
+/* ---- trace synthesis: generate_trace ------------------------------
+ * Counter-based Zipf(s) sampler: token t, layer l draws K distinct ranks without replacement
+ * with probability proportional to the integer weights cdf[r+1]-cdf[r] (successive sampling),
+ * maps rank -> expert through perm[l][rank].  Randomness is Philox4x32-10 keyed by `seed`
+ * with counter (t_lo, t_hi, l, k/4), so any token range regenerates bit-identically on any
+ * device or shard.  Writes planes[l][(t - tok_begin)*K + k] for t in [tok_begin, tok_end).
+ *   cdf: device uint32[E+1], cdf[0]=0, strictly increasing, cdf[E] < 2^31
+ *   perm: device uint8[L][E] (a permutation of 0..E-1 per layer)                             */
+int mp_gen_trace(uint64_t seed, int64_t tok_begin, int64_t tok_end, int L, int K, int E,
+                 const uint32_t* cdf, const uint8_t* perm, uint8_t* planes, int64_t plane_stride,
+                 void* stream);
+
+/* ---- ingestion check: ActivationTrace invariants ----------------------------
+ * For tokens [tok_begin, tok_end): every id < E and the K ids of each (token, layer) record
+ * are distinct.  First violation (lowest token) lands in err.                                */
+int mp_validate_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
+                   int L, int K, int E, int64_t* err, void* stream);
+
+/* ---- load statistics: estimate_frequencies ------------------------
+ * counts[l*E + e] += #{(t,k) : t in [tok_begin,tok_end), planes[l][t*K+k] == e}.
+ * Ids >= E are not counted; they raise MP_DATA_EXPERT_RANGE in err.                          */
+int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
+               int L, int K, int E, int64_t* counts, int64_t* err, void* stream);
+
+/* ---- placement tables: Placement -> per-expert round-trip hops ---------
+ * tables[((l*256 + e)*W + w)] is a u32 whose byte j is pe_q[l][e] = cost[topo_of[q]][l][assign[q][l][e]]
+ * for placement q = 4*w + j (q < P; unused lanes and e >= E are 0).  W = 1, 2 or 4 (P <= 4W).
+ *   cost: device uint8[T][L][S]; assign: device int32[P][L][E]; topo_of: device int32[P]      */
+int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P,
+                   int L, int E, int S, uint32_t* tables, int W, int64_t* err, void* stream);
+
+/* ---- traffic evaluator: token_hops / evaluate -----------------
+ * For placement q and chunk c:
+ *   hop_sums[q*C + c] += sum_{t in chunk c, t in [tok_begin,tok_end)} sum_l sum_k pe_q[l][planes[l][t*K+k]]
+ * chunk_bounds: device int64[C+1], ascending token indices; chunk c = [bounds[c], bounds[c+1]).
+ * max_p: an upper bound on every table byte (selects the u8-lane widening interval).
+ * hop_sums is int64[4W][C].                                                                  */
+int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
+                int L, int K, const int64_t* chunk_bounds, int C, const uint32_t* tables, int W,
+                int max_p, int64_t* hop_sums, void* stream);
+
+/* ---- fused statistics + traffic pass (one read of the trace) -----------------------------
+ * mp_hist_u8 and mp_score_u8 over the same token range in one kernel (W = 1 only).           */
+int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
+                     int L, int K, int E, const int64_t* chunk_bounds, int C, const uint32_t* tables,
+                     int max_p, int64_t* counts, int64_t* hop_sums, int64_t* err, void* stream);
+
+/* ---- topology: all_pairs_hops -------------------------------------
+ * Unit-weight BFS over the undirected switch/server graph in CSR form (row_ptr[n_nodes+1],
+ * col[nnz]) from every node in src_nodes; dist[i*n_dst + j] = hops(src_nodes[i], dst_nodes[j]).
+ * Unreachable pairs raise MP_DATA_UNREACHABLE; hop counts > 255 raise MP_DATA_HOPS_RANGE.
+ * n_nodes <= 8192.                                                                            */
+int mp_apsp_bfs(const int32_t* row_ptr, const int32_t* col, int n_nodes, const int32_t* src_nodes,
+                int n_src, const int32_t* dst_nodes, int n_dst, uint8_t* dist, int64_t* err, void* stream);
+
+/* device-level expansion: out[a*S + b] = dsrv[server[a]*n_srv + server[b]]   */
+int mp_expand_dist(const uint8_t* dsrv, int n_srv, const int32_t* dev_server, int S, uint8_t* out,
+                   void* stream);
+
+/* ---- cost_matrix: p[l*S + s] = D[d_l][s] + D[s][c_l] ---------------------
+ * D given at server level: D[a][b] = dsrv[server[a]*n_srv + server[b]].                        */
+int mp_cost_matrix(const uint8_t* dsrv, int n_srv, const int32_t* dev_server, int S,
+                   const int32_t* dispatch, const int32_t* collect, int L, uint8_t* p, void* stream);
+
+/* ---- build_instance coefficients ---------------------------
+ * f[l][e] = counts[l*E+e] / denom (float64; counts == NULL means uniform f = 1/E), then
+ *   w[l][e][s] = f[l][e] * p[l][s]              (float64, nullable output)
+ *   w_int[l][e][s] = rint(w[l][e][s] * scale)   (int64 round-half-even, nullable output)
+ * in exactly numpy's operation order, so results are bit-identical to the host formula.      */
+int mp_coeffs(const int64_t* counts, int64_t denom, const uint8_t* p, int L, int E, int S, double scale,
+              double* w, int64_t* w_int, void* stream);
+
+/* ---- communication_map ------------------------------------------------
+ * traffic[a*n_srv + b] += sum over (l,e) of counts[l*E+e] * D(d_l, s) at (server d_l, server s)
+ * and counts[l*E+e] * D(s, c_l) at (server s, server c_l), with s = assign[l*E+e].
+ * (Un-normalised and un-symmetrised; the host divides by N and symmetrises.)                 */
+int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev_server, const uint8_t* dsrv,
+                int n_srv, const int32_t* dispatch, const int32_t* collect, int L, int E, int S,
+                int64_t* traffic, int64_t* err, void* stream);
+
+/* ---- solve_exact: min-cost flow on the class-compressed FlowNetwork ------
+ * HOST function (the ILP solve stays on the host).  Costs w_int[l][e][s] are int64 >= 0 in
+ * host memory.  When p (host uint8[L][S]) is given, w_int must depend on s only through
+ * p[l][s] (true for build_instance output) and the network is class-compressed:
+ * item(l,e) -> class(l, p value) -> slot(l,s) -> server(s) -> sink, which has the same optimum
+ * as the full network.  p == NULL uses the full item(l,e) -> slot(l,s) arc set of SPEC.md:264-268.
+ * Successive shortest paths with potentials.  assign_out: host int32[L][E] (device ids).
+ * Returns MP_OK, MP_ERR_ARG, or 4 (= infeasible: max flow < L*E; *flow_out says how much). */
+#define MP_INFEASIBLE 4
+int mp_solve_mcf(const int64_t* w_int, const uint8_t* p, int L, int E, int S, int c_layer, int c_exp,
+                 int32_t* assign_out, int64_t* objective_out, int64_t* flow_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEPLACE_CUDA_H */

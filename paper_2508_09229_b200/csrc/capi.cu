@@ -1,0 +1,153 @@
+// extern "C" entry points of libmoeplace_cuda.so (declared in include/moeplace_cuda.h).
+// Argument validation happens here, synchronously; kernels only see checked shapes.
+#include "common.cuh"
+
+namespace mp {
+cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1,
+                          int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
+                          int64_t* hop_sums, int64_t* err, cudaStream_t s);
+cudaError_t launch_gen(uint64_t seed, int64_t t0, int64_t t1, int L, int K, int E, const uint32_t* cdf,
+                       const uint8_t* perm, uint8_t* planes, int64_t stride, cudaStream_t s);
+cudaError_t launch_validate(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                            int64_t* err, cudaStream_t s);
+cudaError_t launch_bfs(const int32_t* row_ptr, const int32_t* col, int n, const int32_t* src, int n_src,
+                       const int32_t* dst, int n_dst, uint8_t* dist, int64_t* err, cudaStream_t s);
+cudaError_t launch_expand(const uint8_t* dsrv, int n_srv, const int32_t* server, int S, uint8_t* out, cudaStream_t s);
+cudaError_t launch_cost(const uint8_t* dsrv, int n_srv, const int32_t* server, int S, const int32_t* disp,
+                        const int32_t* coll, int L, uint8_t* p, cudaStream_t s);
+cudaError_t launch_pack(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
+                        int S, uint32_t* tables, int W, int64_t* err, cudaStream_t s);
+cudaError_t launch_coeffs(const int64_t* counts, int64_t denom, const uint8_t* p, int L, int E, int S, double scale,
+                          double* w, int64_t* w_int, cudaStream_t s);
+cudaError_t launch_comm(const int64_t* counts, const int32_t* assign, const int32_t* server, const uint8_t* dsrv,
+                        int n_srv, const int32_t* disp, const int32_t* coll, int L, int E, int S, int64_t* traffic,
+                        int64_t* err, cudaStream_t s);
+}  // namespace mp
+
+namespace {
+inline int status(cudaError_t e) { return e == cudaSuccess ? MP_OK : MP_ERR_CUDA; }
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+// shared trace-shape checks
+inline int check_trace(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K) {
+  if (!planes || L <= 0 || K <= 0 || t0 < 0 || t1 < t0) return MP_ERR_ARG;
+  if (!aligned16(planes) || (stride & 15) != 0 || stride < t1 * (int64_t)K) return MP_ERR_ARG;
+  return MP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int mp_abi_version(void) { return MP_ABI_VERSION; }
+
+const char* mp_status_string(int st) {
+  switch (st) {
+    case MP_OK: return "ok";
+    case MP_ERR_ARG: return "invalid argument";
+    case MP_ERR_CUDA: return "CUDA launch/runtime failure";
+    case MP_ERR_UNSUPPORTED: return "outside the u8 device format (E > 256 or hop cost > 255)";
+    case MP_INFEASIBLE: return "infeasible: max flow < L*E";
+    default: return "unknown status";
+  }
+}
+
+int mp_gen_trace(uint64_t seed, int64_t tok_begin, int64_t tok_end, int L, int K, int E, const uint32_t* cdf,
+                 const uint8_t* perm, uint8_t* planes, int64_t plane_stride, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  if (E <= 0 || K > E || !cdf || !perm || tok_begin < 0) return MP_ERR_ARG;
+  int r = check_trace(planes, plane_stride, 0, tok_end - tok_begin, L, K);
+  if (r) return r;
+  return status(mp::launch_gen(seed, tok_begin, tok_end, L, K, E, cdf, perm, planes, plane_stride, S(stream)));
+}
+
+int mp_validate_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K, int E,
+                   int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  if (E <= 0 || !err) return MP_ERR_ARG;
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  return status(mp::launch_validate(planes, plane_stride, tok_begin, tok_end, L, K, E, err, S(stream)));
+}
+
+int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K, int E,
+               int64_t* counts, int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  if (E <= 0 || !counts) return MP_ERR_ARG;
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (tok_end == tok_begin) return MP_OK;
+  return status(mp::launch_stream(true, 0, 0, planes, plane_stride, tok_begin, tok_end, L, K, E, nullptr, 1, nullptr,
+                                  counts, nullptr, err, S(stream)));
+}
+
+int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
+                   int S_, uint32_t* tables, int W, int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  if (!cost || !assign || !topo_of || !tables || T <= 0 || P <= 0 || L <= 0 || E <= 0 || S_ <= 0) return MP_ERR_ARG;
+  if (!(W == 1 || W == 2 || W == 4) || P > 4 * W) return MP_ERR_ARG;
+  return status(mp::launch_pack(cost, T, assign, topo_of, P, L, E, S_, tables, W, err, S(stream)));
+}
+
+int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int max_p, int64_t* hop_sums,
+                void* stream) {
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (!chunk_bounds || C <= 0 || !tables || !hop_sums || !(W == 1 || W == 2 || W == 4)) return MP_ERR_ARG;
+  if (max_p < 0) return MP_ERR_ARG;
+  if (max_p > 255) return MP_ERR_UNSUPPORTED;
+  if (tok_end == tok_begin) return MP_OK;
+  return status(mp::launch_stream(false, W, max_p, planes, plane_stride, tok_begin, tok_end, L, K, 256, chunk_bounds,
+                                  C, tables, nullptr, hop_sums, nullptr, S(stream)));
+}
+
+int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                     int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int max_p, int64_t* counts,
+                     int64_t* hop_sums, int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (E <= 0 || !counts || !chunk_bounds || C <= 0 || !tables || !hop_sums || max_p < 0) return MP_ERR_ARG;
+  if (max_p > 255) return MP_ERR_UNSUPPORTED;
+  if (tok_end == tok_begin) return MP_OK;
+  return status(mp::launch_stream(true, 1, max_p, planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C,
+                                  tables, counts, hop_sums, err, S(stream)));
+}
+
+int mp_apsp_bfs(const int32_t* row_ptr, const int32_t* col, int n_nodes, const int32_t* src_nodes, int n_src,
+                const int32_t* dst_nodes, int n_dst, uint8_t* dist, int64_t* err, void* stream) {
+  if (!row_ptr || !col || !src_nodes || !dst_nodes || !dist || n_nodes <= 0 || n_src < 0 || n_dst < 0)
+    return MP_ERR_ARG;
+  if (n_nodes > 8192) return MP_ERR_UNSUPPORTED;
+  return status(mp::launch_bfs(row_ptr, col, n_nodes, src_nodes, n_src, dst_nodes, n_dst, dist, err, S(stream)));
+}
+
+int mp_expand_dist(const uint8_t* dsrv, int n_srv, const int32_t* dev_server, int S_, uint8_t* out, void* stream) {
+  if (!dsrv || !dev_server || !out || n_srv <= 0 || S_ < 0) return MP_ERR_ARG;
+  return status(mp::launch_expand(dsrv, n_srv, dev_server, S_, out, S(stream)));
+}
+
+int mp_cost_matrix(const uint8_t* dsrv, int n_srv, const int32_t* dev_server, int S_, const int32_t* dispatch,
+                   const int32_t* collect, int L, uint8_t* p, void* stream) {
+  if (!dsrv || !dev_server || !dispatch || !collect || !p || n_srv <= 0 || S_ <= 0 || L <= 0) return MP_ERR_ARG;
+  return status(mp::launch_cost(dsrv, n_srv, dev_server, S_, dispatch, collect, L, p, S(stream)));
+}
+
+int mp_coeffs(const int64_t* counts, int64_t denom, const uint8_t* p, int L, int E, int S_, double scale, double* w,
+              int64_t* w_int, void* stream) {
+  if (!p || L <= 0 || E <= 0 || S_ <= 0 || (!w && !w_int)) return MP_ERR_ARG;
+  if (counts && denom <= 0) return MP_ERR_ARG;
+  return status(mp::launch_coeffs(counts, denom, p, L, E, S_, scale, w, w_int, S(stream)));
+}
+
+int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev_server, const uint8_t* dsrv, int n_srv,
+                const int32_t* dispatch, const int32_t* collect, int L, int E, int S_, int64_t* traffic, int64_t* err,
+                void* stream) {
+  if (!counts || !assign || !dev_server || !dsrv || !dispatch || !collect || !traffic || n_srv <= 0 || L <= 0 ||
+      E <= 0 || S_ <= 0)
+    return MP_ERR_ARG;
+  return status(mp::launch_comm(counts, assign, dev_server, dsrv, n_srv, dispatch, collect, L, E, S_, traffic, err,
+                                S(stream)));
+}
+
+}  // extern "C"

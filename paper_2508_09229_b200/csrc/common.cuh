@@ -1,0 +1,95 @@
+// Shared device helpers for the moeplace sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/moeplace_cuda.h"
+
+namespace mp {
+
+constexpr int kMaxE = 256;     // one-byte expert ids
+constexpr int kThreads = 512;  // streaming kernels: 16 warps per CTA
+
+// Streaming 128-bit load that does not allocate in L1 (each trace byte is read once).
+__device__ __forceinline__ int4 ldg_stream(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// prmt.b32: builds a word from the bytes of (a, b).  Used to turn an expert byte into a
+// shared-memory row offset in ONE instruction: selector SEL_ROW(b) puts byte b of `a` into
+// result byte 1 (=> e << 8) and byte 0 of `b` (the lane's slot offset) into result byte 0.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+// result = { byte0: b.byte0, byte1: a.byte[k], byte2: b.byte1 (=0), byte3: b.byte1 (=0) }
+__host__ __device__ constexpr uint32_t sel_row(int k) { return 0x5504u | ((uint32_t)k << 4); }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
+}
+
+// shared-memory increment without return (ATOMS)
+__device__ __forceinline__ void atoms_inc(uint32_t a) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a));
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Record a data error: the first writer sets {code, a, b}; every writer bumps the count.
+__device__ __forceinline__ void report_err(int64_t* err, int code, int64_t a, int64_t b, int64_t n = 1) {
+  if (!err) return;
+  unsigned long long* e = reinterpret_cast<unsigned long long*>(err);
+  if (atomicCAS(e, 0ull, (unsigned long long)code) == 0ull) {
+    e[1] = (unsigned long long)a;
+    e[2] = (unsigned long long)b;
+  }
+  atomicAdd(e + 3, (unsigned long long)n);
+}
+
+__device__ __forceinline__ void atomic_add_i64(int64_t* p, int64_t v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+// Work split shared by the streaming kernels: the byte space of all L planes restricted to
+// [b0, b1) is flattened (plane-major) and cut into gridDim.x contiguous ranges; each CTA then
+// walks the per-plane segments of its range.
+struct Flat {
+  int64_t nb;     // bytes per plane in range
+  int64_t b0;     // first byte (within a plane)
+  int64_t g0, g1; // this CTA's flattened range
+  __device__ Flat(int64_t b0_, int64_t b1_, int L) {
+    b0 = b0_;
+    nb = b1_ - b0_;
+    int64_t total = nb * (int64_t)L;
+    int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    per = (per + 15) & ~(int64_t)15;
+    g0 = min(total, (int64_t)blockIdx.x * per);
+    g1 = min(total, g0 + per);
+  }
+};
+
+}  // namespace mp

@@ -1,0 +1,284 @@
+// Streaming kernels over layer-major u8 traces: load statistics (hist), placement traffic
+// (score) and the fused pass.  One kernel template serves all three.
+//
+// Design: the byte space of the L planes is cut into gridDim.x contiguous
+// ranges; a CTA walks its range plane segment by plane segment.  Per segment it stages
+// layer l's state in shared memory as 256 rows of 256 B, one row per expert id e:
+//   * score table: P = 4W placement hop costs (u8 lanes), replicated per lane slot so the
+//     32 lanes of a warp never bank-conflict (slot = lane*4 | lane*8 | (lane&7)*16 for
+//     W = 1 | 2 | 4 -> one LDS.32 | LDS.64 | LDS.128 wavefront per 32 | 16 | 8 lanes);
+//   * histogram: 32 u32 replicas of bin e at bytes 128 + lane*4 (bank = lane), so the
+//     ATOMS of one warp hit 32 distinct banks and no address is shared between lanes.
+// An expert byte b of a loaded word becomes its row offset (e << 8) | slot with a single
+// PRMT, so a lookup costs PRMT + LDS (+ ATOMS for the histogram).
+// The trace is streamed with 128-bit L1-no-allocate loads, UNROLL per thread in flight.
+#include "common.cuh"
+
+namespace mp {
+
+template <int W>
+struct ScoreAcc {
+  static constexpr int P = 4 * W;
+  uint32_t tot[P];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < P; ++q) tot[q] = 0;
+  }
+};
+
+// one table lookup at row offset `a` (shared address), returning W words
+template <int W>
+__device__ __forceinline__ void table_load(uint32_t a, uint32_t (&t)[W]) {
+  if constexpr (W == 1) {
+    t[0] = lds32(a);
+  } else if constexpr (W == 2) {
+    uint2 v = lds64(a);
+    t[0] = v.x; t[1] = v.y;
+  } else {
+    uint4 v = lds128(a);
+    t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+  }
+}
+
+template <bool HIST, int W, int WIDEN, int UNROLL>
+struct Stream {
+  static constexpr int P = 4 * W;
+  uint32_t base;   // shared address of row 0
+  uint32_t slot;   // lane's score slot (byte 0 of the row offset)
+  uint32_t hslot;  // lane's histogram slot
+
+  // single byte (heads/tails of ranges; rare)
+  __device__ __forceinline__ void one(uint32_t e, ScoreAcc<(W > 0 ? W : 1)>& acc) {
+    if constexpr (HIST) atoms_inc(base + ((e << 8) | hslot) + 128);
+    if constexpr (W > 0) {
+      uint32_t t[W];
+      table_load<W>(base + ((e << 8) | slot), t);
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc.tot[4 * w + j] += (t[w] >> (8 * j)) & 0xffu;
+    }
+  }
+
+  // 16 bytes -> lookups; u8-lane sums widened into u16-lane accumulators every WIDEN lookups
+  __device__ __forceinline__ void vec(const int4& x, uint32_t (&acc16)[2 * (W > 0 ? W : 1)]) {
+    const uint32_t wd[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
+    constexpr int WW = W > 0 ? W : 1;
+    uint32_t acc8[WW];
+#pragma unroll
+    for (int w = 0; w < WW; ++w) acc8[w] = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if constexpr (W > 0) {
+          const uint32_t off = prmt(wd[q], slot, sel_row(b));
+          uint32_t t[W];
+          table_load<W>(base + off, t);
+#pragma unroll
+          for (int w = 0; w < W; ++w) acc8[w] += t[w];
+          if constexpr (HIST) {
+            const uint32_t hoff = (W == 1) ? off : prmt(wd[q], hslot, sel_row(b));
+            atoms_inc(base + hoff + 128);
+          }
+          if (((q * 4 + b + 1) % WIDEN) == 0) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+              acc16[2 * w] += acc8[w] & 0x00ff00ffu;
+              acc16[2 * w + 1] += (acc8[w] >> 8) & 0x00ff00ffu;
+              acc8[w] = 0;
+            }
+          }
+        } else {
+          const uint32_t off = prmt(wd[q], hslot, sel_row(b));
+          atoms_inc(base + off + 128);
+        }
+      }
+    }
+  }
+
+  // all bytes [xa, xb) of one plane
+  __device__ __forceinline__ void range(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb,
+                                        ScoreAcc<(W > 0 ? W : 1)>& acc) {
+    constexpr int WW = W > 0 ? W : 1;
+    const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
+    const int64_t tb = max(ha, xb & ~(int64_t)15);
+    for (int64_t x = xa + threadIdx.x; x < ha; x += blockDim.x) one(plane[x], acc);
+    for (int64_t x = tb + threadIdx.x; x < xb; x += blockDim.x) one(plane[x], acc);
+    const int4* pv = reinterpret_cast<const int4*>(plane);
+    const int64_t v1 = tb >> 4;
+    uint32_t acc16[2 * WW];
+#pragma unroll
+    for (int i = 0; i < 2 * WW; ++i) acc16[i] = 0;
+    for (int64_t v = (ha >> 4) + threadIdx.x; v < v1; v += (int64_t)blockDim.x * UNROLL) {
+      int4 x[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t j = v + (int64_t)u * blockDim.x;
+        x[u] = j < v1 ? ldg_stream(pv + j) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        if (v + (int64_t)u * blockDim.x < v1) vec(x[u], acc16);
+      }
+      if constexpr (W > 0) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          acc.tot[4 * w + 0] += acc16[2 * w] & 0xffffu;
+          acc.tot[4 * w + 2] += acc16[2 * w] >> 16;
+          acc.tot[4 * w + 1] += acc16[2 * w + 1] & 0xffffu;
+          acc.tot[4 * w + 3] += acc16[2 * w + 1] >> 16;
+          acc16[2 * w] = 0;
+          acc16[2 * w + 1] = 0;
+        }
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ int chunk_of(const int64_t* __restrict__ bounds, int C, int64_t t) {
+  // largest c in [0, C) with bounds[c] <= t
+  int lo = 0, hi = C;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(bounds + mid) <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+constexpr int64_t kMaxPiece = (int64_t)1 << 30;  // keeps per-thread u32 sums exact
+
+template <bool HIST, int W, int WIDEN, int UNROLL>
+__global__ void __launch_bounds__(kThreads, (W == 4 || W == 2) ? 2 : 3)
+stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+              const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
+              int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
+  extern __shared__ __align__(128) uint8_t sm[];  // 256 rows x 256 B
+  constexpr int WW = W > 0 ? W : 1;
+  constexpr int P = 4 * WW;
+  const int lane = threadIdx.x & 31;
+  Stream<HIST, W, WIDEN, UNROLL> st;
+  st.base = smem_addr(sm);
+  st.slot = W == 4 ? (uint32_t)((lane & 7) << 4) : W == 2 ? (uint32_t)(lane << 3) : (uint32_t)(lane << 2);
+  st.hslot = (uint32_t)(lane << 2);
+  uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
+
+  Flat f(t0 * K, t1 * K, L);
+  for (int64_t g = f.g0; g < f.g1;) {
+    const int l = (int)(g / f.nb);
+    const int64_t off_in = g - (int64_t)l * f.nb;
+    const int64_t seg = min(f.g1 - g, f.nb - off_in);
+    const int64_t x0 = f.b0 + off_in, x1 = x0 + seg;
+    const uint8_t* plane = planes + (int64_t)l * stride;
+
+    __syncthreads();  // previous segment is done with shared memory
+    if constexpr (W > 0) {
+      // row e, word j (< WPR) <- tables[(l*256 + e)*W + j % W]
+      constexpr int WPR = (W == 2) ? 64 : 32;
+      const uint32_t* tl = tables + (int64_t)l * 256 * W;
+      for (int i = threadIdx.x; i < 256 * WPR; i += blockDim.x) {
+        const int e = i / WPR, j = i % WPR;
+        smw[e * 64 + j] = __ldg(tl + e * W + (j % W));
+      }
+    }
+    if constexpr (HIST) {
+      for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) smw[(i >> 5) * 64 + 32 + (i & 31)] = 0;
+    }
+    __syncthreads();
+
+    if constexpr (W > 0) {
+      for (int64_t x = x0; x < x1;) {
+        const int c = chunk_of(bounds, C, x / K);
+        const int64_t xe = min(min(x1, __ldg(bounds + c + 1) * K), x + kMaxPiece);
+        ScoreAcc<WW> acc;
+        acc.zero();
+        st.range(plane, x, xe, acc);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const unsigned long long s = warp_sum_u64(acc.tot[q]);
+          if (lane == 0 && s) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)s);
+        }
+        x = xe;
+      }
+    } else {
+      ScoreAcc<1> dummy;
+      st.range(plane, x0, x1, dummy);
+    }
+
+    if constexpr (HIST) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+        const uint32_t* row = smw + e * 64 + 32;
+        uint32_t s = 0;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) s += row[(r + e) & 31];  // rotate: no bank conflicts
+        if (s) {
+          if (e < E) atomic_add_i64(counts + (int64_t)l * E + e, (int64_t)s);
+          else report_err(err, MP_DATA_EXPERT_RANGE, l, e, s);
+        }
+      }
+    }
+    g += seg;
+  }
+}
+
+constexpr int kSmemBytes = 256 * 256;
+
+template <bool HIST, int W, int WIDEN>
+static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                            const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
+                            int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+  constexpr int UNROLL = 4;
+  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  // grid: persistent, one wave of resident CTAs; small inputs get fewer CTAs
+  const int64_t total = (t1 - t0) * (int64_t)K * L;
+  int64_t grid = (int64_t)nsm * per_sm;
+  const int64_t min_bytes_per_cta = 64 * 1024;
+  grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
+  kern<<<(unsigned)grid, kThreads, kSmemBytes, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
+                                                     hop_sums, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1,
+                          int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
+                          int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+#define MP_ARGS planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s
+  const int widen = max_p <= 15 ? 16 : max_p <= 63 ? 4 : 1;
+  if (W == 0) return launch_t<true, 0, 16>(MP_ARGS);
+  if (hist) {
+    if (W == 1) {
+      if (widen == 16) return launch_t<true, 1, 16>(MP_ARGS);
+      if (widen == 4) return launch_t<true, 1, 4>(MP_ARGS);
+      return launch_t<true, 1, 1>(MP_ARGS);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (W == 1) {
+    if (widen == 16) return launch_t<false, 1, 16>(MP_ARGS);
+    if (widen == 4) return launch_t<false, 1, 4>(MP_ARGS);
+    return launch_t<false, 1, 1>(MP_ARGS);
+  }
+  if (W == 2) {
+    if (widen == 16) return launch_t<false, 2, 16>(MP_ARGS);
+    if (widen == 4) return launch_t<false, 2, 4>(MP_ARGS);
+    return launch_t<false, 2, 1>(MP_ARGS);
+  }
+  if (W == 4) {
+    if (widen == 16) return launch_t<false, 4, 16>(MP_ARGS);
+    if (widen == 4) return launch_t<false, 4, 4>(MP_ARGS);
+    return launch_t<false, 4, 1>(MP_ARGS);
+  }
+#undef MP_ARGS
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mp

@@ -1,0 +1,265 @@
+"""``moeplace.eval`` — the placement traffic evaluator.
+
+``evaluate`` / ``evaluate_many`` score placements on the GPU: the placements' per-expert
+round-trip hop costs pe_q[l, e] = p[l, assign_q[l, e]] are packed into u8 lanes
+(``mp_pack_tables``) and ``mp_score_u8`` streams the trace once per group of up to 16
+placements, gathering pe_q for every (token, layer, pick) and reducing exact int64 hop sums per
+chunk.  The host derives the report floats from those integers with numpy (the oracle runs the
+same float code on its own integers, so reports are bit-identical, not merely within 1e-6).
+"""
+from __future__ import annotations
+
+import json
+from dataclasses import asdict, dataclass, field
+from typing import Any, Optional, Sequence, Union
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, MoeplaceError
+from .model_trace import ActivationTrace, FrequencyTable, ModelSpec, frequencies_from_counts, validate_trace
+from .placement import CostMatrix, Placement
+
+MAX_LANES = 16  # placements scored per pass (W = 4 words of four u8 lanes)
+
+
+@dataclass
+class EvalReport:
+    """SPEC.md:326-329.  ``std_hops`` is the population std (ddof=0) of per-chunk means."""
+
+    mean_hops_per_token: float
+    std_hops: float
+    n_tokens: int
+    n_chunks: int
+    objective_train: Optional[float] = None
+    label: str = ""
+    empty_chunks: int = 0
+    hop_sum: int = 0                      # exact integer total (sum over tokens)
+    chunk_hop_sums: Optional[list] = None  # exact per-chunk integers (id order)
+
+    def to_json(self) -> dict:
+        d = asdict(self)
+        d.pop("chunk_hop_sums")
+        return d
+
+    def write(self, path) -> None:
+        with open(path, "w") as f:
+            json.dump(self.to_json(), f, indent=1, sort_keys=True)
+
+
+@dataclass
+class CommMap:
+    """symmetric server x server hop volume per token, zero diagonal."""
+
+    traffic: np.ndarray  # float64 [n_servers, n_servers]
+    raw: Optional[np.ndarray] = None  # exact int64 directed accumulations (before /N and symmetrisation)
+
+    def to_csv(self, path) -> None:
+        n = self.traffic.shape[0]
+        with open(path, "w") as f:
+            f.write(",".join(str(i) for i in range(n)) + "\n")
+            for r in range(n):
+                f.write(",".join(repr(float(v)) for v in self.traffic[r]) + "\n")
+
+
+def report_from_sums(sums: np.ndarray, tokens: np.ndarray, label: str = "") -> EvalReport:
+    """EvalReport floats from exact integer per-chunk sums.  Empty chunks
+    are excluded and counted."""
+    sums = np.asarray(sums, dtype=np.int64)
+    tokens = np.asarray(tokens, dtype=np.int64)
+    keep = tokens > 0
+    n_tok = int(tokens.sum())
+    if n_tok == 0:
+        raise MoeplaceError("evaluate: empty trace")
+    total = int(sums.sum())
+    means = sums[keep] / tokens[keep]
+    return EvalReport(mean_hops_per_token=total / n_tok, std_hops=float(np.std(means)), n_tokens=n_tok,
+                      n_chunks=int(keep.sum()), label=label, empty_chunks=int((~keep).sum()), hop_sum=total,
+                      chunk_hop_sums=sums.tolist())
+
+
+def _as_costs(costs, n: int) -> list[CostMatrix]:
+    if isinstance(costs, CostMatrix):
+        return [costs] * n
+    costs = list(costs)
+    if len(costs) != n:
+        raise ConfigError(f"got {len(costs)} cost matrices for {n} placements")
+    return costs
+
+
+def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec, W: int):
+    """Pack one group (<= 4W placements) into device tables uint32 [L, 256, W]."""
+    t = _lib.torch()
+    dev = _lib.require_cuda()
+    uniq: list[CostMatrix] = []
+    topo_of = []
+    for c in costs:
+        for i, u in enumerate(uniq):
+            if u is c:
+                topo_of.append(i)
+                break
+        else:
+            uniq.append(c)
+            topo_of.append(len(uniq) - 1)
+    S = uniq[0].S
+    for c in uniq:
+        if c.S != S or c.L != model.L:
+            raise ConfigError(f"cost matrix shape [{c.L}, {c.S}] inconsistent with [{model.L}, {S}]")
+    cost = t.stack([c.p for c in uniq]).contiguous()
+    assign = np.stack([p.assign for p in placements])
+    if assign.shape[1:] != (model.L, model.E):
+        raise ConfigError(f"placement shape {assign.shape[1:]} != model [{model.L}, {model.E}]")
+    d_assign = _lib.to_dev(assign, t.int32)
+    d_topo = _lib.to_dev(np.asarray(topo_of, dtype=np.int32), t.int32)
+    tables = t.empty((model.L, 256, W), dtype=t.int32, device=dev)
+    err = _lib.new_err()
+    _lib.call("mp_pack_tables", _lib.ptr(cost), len(uniq), _lib.ptr(d_assign), _lib.ptr(d_topo), len(placements),
+              model.L, model.E, S, _lib.ptr(tables), W, _lib.ptr(err), _lib.stream_handle())
+    _lib.check_err(err, "evaluate: unplaced expert")
+    max_p = max(c.max_p for c in uniq)
+    return tables, max_p
+
+
+def _lanes_for(n: int) -> int:
+    return 1 if n <= 4 else 2 if n <= 8 else 4
+
+
+def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs) -> np.ndarray:
+    """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_u8``)."""
+    t = _lib.torch()
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("evaluate: empty trace")
+    placements = list(placements)
+    costs = _as_costs(costs, len(placements))
+    planes = trace.device_planes()
+    validate_trace(trace)
+    bounds = _lib.to_dev(trace.chunk_bounds, t.int64)
+    C = trace.n_chunks
+    out = np.zeros((len(placements), C), dtype=np.int64)
+    for g0 in range(0, len(placements), MAX_LANES):
+        grp = placements[g0:g0 + MAX_LANES]
+        W = _lanes_for(len(grp))
+        tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], m, W)
+        sums = t.zeros((4 * W, C), dtype=t.int64, device=planes.device)
+        _lib.call("mp_score_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
+                  _lib.ptr(bounds), C, _lib.ptr(tables), W, max_p, _lib.ptr(sums), _lib.stream_handle())
+        out[g0:g0 + len(grp)] = sums[:len(grp)].cpu().numpy()
+    return out
+
+
+def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs) -> list[EvalReport]:
+    """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies):
+    up to 16 placements per pass over the trace (extension A18)."""
+    placements = list(placements)
+    sums = score_sums(trace, placements, costs)
+    tokens = trace.chunk_token_counts()
+    return [report_from_sums(sums[i], tokens, placements[i].label) for i in range(len(placements))]
+
+
+def evaluate(trace: ActivationTrace, placement: Placement, cost: CostMatrix) -> EvalReport:
+    """per-chunk hop sums on the GPU; mean = token-weighted grand mean, std =
+    std of per-chunk means; empty chunks excluded with a warning count."""
+    return evaluate_many(trace, [placement], cost)[0]
+
+
+def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement], cost: CostMatrix):
+    """One fused pass (``mp_hist_score_u8``): the trace's FrequencyTable plus the EvalReports of
+    up to 4 placements on one cost matrix.  Used for the train split, where the ILPLoad
+    frequencies and the train-side metric come from the same tokens."""
+    t = _lib.torch()
+    m = trace.model
+    placements = list(placements)
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("evaluate: empty trace")
+    if not 1 <= len(placements) <= 4:
+        raise ConfigError("evaluate_with_stats takes 1..4 placements")
+    planes = trace.device_planes()
+    validate_trace(trace)
+    tables, max_p = _group_tables(placements, [cost] * len(placements), m, 1)
+    bounds = _lib.to_dev(trace.chunk_bounds, t.int64)
+    C = trace.n_chunks
+    counts = t.zeros((m.L, m.E), dtype=t.int64, device=planes.device)
+    sums = t.zeros((4, C), dtype=t.int64, device=planes.device)
+    err = _lib.new_err()
+    _lib.call("mp_hist_score_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K, m.E,
+              _lib.ptr(bounds), C, _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err),
+              _lib.stream_handle())
+    _lib.check_err(err, "evaluate_with_stats")
+    freq = frequencies_from_counts(counts.cpu().numpy(), trace.n_tokens, m.K)
+    s = sums.cpu().numpy()
+    tokens = trace.chunk_token_counts()
+    return freq, [report_from_sums(s[i], tokens, placements[i].label) for i in range(len(placements))]
+
+
+def token_hops(selections, placement: Placement, cost: CostMatrix) -> int:
+    """sum over layers and selected experts of p[l, device(l, e)] for ONE token
+    (``selections`` = L lists of selected experts).  Runs through the device scorer."""
+    sel = [list(s) for s in selections]
+    L, E = placement.assign.shape
+    if len(sel) != L or not sel:
+        raise ConfigError(f"selections must list {L} layers")
+    K = len(sel[0])
+    if any(len(s) != K for s in sel):
+        raise ConfigError("every layer must select the same number of experts")
+    arr = np.asarray(sel, dtype=np.int64).reshape(1, L, K)
+    if arr.min() < 0 or arr.max() >= E:
+        raise MoeplaceError("token_hops: expert index is not placed (outside [0, E))")
+    tr = ActivationTrace.from_tokens(ModelSpec(L, E, K), arr.astype(np.uint8))
+    return int(score_sums(tr, [placement], cost)[0].sum())
+
+
+def objective_value(placement: Placement, freq: FrequencyTable, cost: CostMatrix) -> float:
+    """sum_{l,e} f[l,e] * p[l, device(l,e)].  Equals evaluate(train).mean / K
+    for the trace f was estimated from."""
+    f = np.asarray(freq.f, dtype=np.float64)
+    a = placement.assign
+    if f.shape != a.shape:
+        raise ConfigError(f"frequency table {f.shape} and placement {a.shape} differ")
+    p = cost.numpy()
+    if a.min() < 0 or a.max() >= p.shape[1]:
+        raise MoeplaceError("objective_value: expert placed outside the topology")
+    pe = p[np.arange(a.shape[0])[:, None], a].astype(np.float64)
+    return float(np.sum(f * pe))
+
+
+def gain(baseline_hops: float, method_hops: float) -> float:
+    """100 * (baseline - method) / method, in percent."""
+    if not method_hops > 0:
+        raise ConfigError(f"gain: method_hops must be positive, got {method_hops}")
+    return 100.0 * (baseline_hops - method_hops) / method_hops
+
+
+def communication_map(trace: ActivationTrace, placement: Placement, topology: Union[CostMatrix, tuple]) -> CommMap:
+    """SPEC.md:371-379.  ``topology`` is the CostMatrix (it carries the distance matrix and the
+    attention placement) or a (DistanceMatrix, AttentionPlacement) pair.  Accumulated on the GPU
+    from the trace's exact (l, e) load counts (the map is linear in them)."""
+    from .model_trace import trace_counts
+    t = _lib.torch()
+    if isinstance(topology, CostMatrix):
+        dist, attn = topology.dist, topology.attn
+    else:
+        dist, attn = topology
+    if dist is None or attn is None:
+        raise ConfigError("communication_map needs the distance matrix and the attention placement")
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("communication_map: empty trace")
+    g = dist.graph
+    counts = trace_counts(trace)
+    n = g.n_servers
+    traffic = t.zeros((n, n), dtype=t.int64, device=counts.device)
+    # keep every argument tensor referenced until the launch is enqueued (the caching allocator
+    # would otherwise hand a freed temporary's memory to the next argument)
+    d_assign = _lib.to_dev(placement.assign, t.int32)
+    d_server = _lib.to_dev(g.device_server, t.int32)
+    d_disp = _lib.to_dev(attn.dispatch, t.int32)
+    d_coll = _lib.to_dev(attn.collect, t.int32)
+    err = _lib.new_err()
+    _lib.call("mp_comm_map", _lib.ptr(counts), _lib.ptr(d_assign), _lib.ptr(d_server), _lib.ptr(dist.server_dist), n,
+              _lib.ptr(d_disp), _lib.ptr(d_coll), m.L, m.E, g.n_devices, _lib.ptr(traffic), _lib.ptr(err),
+              _lib.stream_handle())
+    _lib.check_err(err, "communication_map")
+    raw = traffic.cpu().numpy()
+    sym = (raw + raw.T) / 2.0 / trace.n_tokens
+    return CommMap(sym, raw)

@@ -1,0 +1,426 @@
+"""``moeplace.model_trace`` — model shape, activation traces and load statistics.
+
+Device layout of a trace ("layer planes"): ``planes`` is uint8 [L, stride] and
+byte ``t*K + k`` of plane ``l`` is the k-th expert that token ``t`` selected in MoE layer ``l``.
+Expert ids are single bytes (E <= 256).  Tokens are grouped by chunk in ascending chunk-id order,
+so a chunk, a train/test split or a multi-GPU shard is a token range — a zero-copy view.
+
+Hot path: ``generate_trace`` (kernel ``mp_gen_trace``) and ``estimate_frequencies`` (kernel
+``mp_hist_u8``).  ``parse_trace``/``write_trace`` are host text IO that feed the same planes.
+"""
+from __future__ import annotations
+
+import re
+from dataclasses import dataclass, field
+from typing import Any, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, MoeplaceError, TraceParseError
+
+MAX_EXPERTS = 256  # one-byte expert ids on the device
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    """L MoE layers, E routed experts per layer, top-K routing."""
+
+    num_moe_layers: int
+    experts_per_layer: int
+    topk: int
+
+    def __post_init__(self):
+        L, E, K = self.num_moe_layers, self.experts_per_layer, self.topk
+        for name, v in (("num_moe_layers", L), ("experts_per_layer", E), ("topk", K)):
+            if not isinstance(v, (int, np.integer)) or v < 1:
+                raise ConfigError(f"ModelSpec.{name} must be an integer >= 1, got {v!r}")
+        if K > E:
+            raise ConfigError(f"topk ({K}) must be <= experts_per_layer ({E})")
+
+    @property
+    def L(self) -> int:
+        return self.num_moe_layers
+
+    @property
+    def E(self) -> int:
+        return self.experts_per_layer
+
+    @property
+    def K(self) -> int:
+        return self.topk
+
+
+@dataclass
+class AttentionPlacement:
+    """dispatch device d_l and collect device c_l per layer."""
+
+    dispatch: np.ndarray  # int32 [L]
+    collect: np.ndarray   # int32 [L]
+
+    def __post_init__(self):
+        self.dispatch = np.asarray(self.dispatch, dtype=np.int32)
+        self.collect = np.asarray(self.collect, dtype=np.int32)
+        if self.dispatch.shape != self.collect.shape or self.dispatch.ndim != 1:
+            raise ConfigError("dispatch and collect must be 1-D arrays of equal length")
+
+
+@dataclass
+class FrequencyTable:
+    """f[l, e] = count(l, e) / (K * n_tokens).  ``counts`` keeps the exact
+    integer statistics the device produced; ``f`` is derived from them on the host."""
+
+    f: np.ndarray                       # float64 [L, E]
+    counts: Optional[np.ndarray] = None  # int64 [L, E]
+    n_tokens: int = 0
+    topk: int = 0
+
+
+@dataclass
+class ActivationTrace:
+    """SPEC.md:104-107.  ``planes[:, t*K:(t+1)*K]`` are token t's selections, tokens
+    ``[tok_begin, tok_begin + n_tokens)`` belong to this view, chunk c spans tokens
+    ``[chunk_bounds[c], chunk_bounds[c+1])`` and carries label ``chunk_ids[c]``."""
+
+    model: Optional[ModelSpec]
+    planes: Any                # torch.uint8 [L, stride] (CUDA, or CPU until first device use)
+    tok_begin: int
+    n_tokens: int
+    chunk_ids: np.ndarray      # int64 [C], ascending
+    chunk_bounds: np.ndarray   # int64 [C+1], absolute token indices into planes
+    source_is_file: bool = False
+    _validated: bool = field(default=False, repr=False)
+
+    @property
+    def n_chunks(self) -> int:
+        return int(self.chunk_ids.shape[0])
+
+    @property
+    def tok_end(self) -> int:
+        return self.tok_begin + self.n_tokens
+
+    def __len__(self) -> int:
+        return self.n_tokens
+
+    def chunk_token_counts(self) -> np.ndarray:
+        return np.diff(self.chunk_bounds).astype(np.int64)
+
+    def token_chunk_ids(self) -> np.ndarray:
+        return np.repeat(self.chunk_ids, self.chunk_token_counts())
+
+    def device_planes(self):
+        """The planes on the CUDA device (uploaded once, host->device, if the trace came from a file)."""
+        t = _lib.torch()
+        dev = _lib.require_cuda()
+        if not self.planes.is_cuda:
+            self.planes = self.planes.to(dev, non_blocking=True)
+        return self.planes
+
+    def tokens(self) -> np.ndarray:
+        """Host copy in token-major form, uint8 [N, L, K] (for IO and small-case inspection)."""
+        m = self.model
+        if m is None or self.n_tokens == 0:
+            K = m.K if m else 0
+            L = m.L if m else 0
+            return np.zeros((0, L, K), dtype=np.uint8)
+        K = m.K
+        x = self.planes[:, self.tok_begin * K:self.tok_end * K].cpu().numpy()
+        return np.ascontiguousarray(x.reshape(m.L, self.n_tokens, K).transpose(1, 0, 2))
+
+    def view(self, chunk_lo: int, chunk_hi: int) -> "ActivationTrace":
+        """Zero-copy sub-trace made of chunks [chunk_lo, chunk_hi) (in id order)."""
+        b = self.chunk_bounds
+        return ActivationTrace(self.model, self.planes, int(b[chunk_lo]), int(b[chunk_hi] - b[chunk_lo]),
+                               self.chunk_ids[chunk_lo:chunk_hi].copy(), b[chunk_lo:chunk_hi + 1].copy(),
+                               self.source_is_file, self._validated)
+
+    @classmethod
+    def from_tokens(cls, model: ModelSpec, selections, chunk_of_token: Optional[Sequence[int]] = None,
+                    device=None) -> "ActivationTrace":
+        """Build a trace from token-major selections [N, L, K] and per-token chunk labels.
+        Tokens are stably regrouped by ascending chunk id (evaluation is invariant under
+        permutation within a chunk)."""
+        sel = np.asarray(selections)
+        if sel.ndim != 3 or sel.shape[1:] != (model.L, model.K):
+            raise ConfigError(f"selections must have shape [N, {model.L}, {model.K}], got {sel.shape}")
+        if sel.size and (sel.min() < 0 or sel.max() >= model.E):
+            raise MoeplaceError(f"expert index outside [0, {model.E})")
+        N = sel.shape[0]
+        cid = np.zeros(N, dtype=np.int64) if chunk_of_token is None else np.asarray(chunk_of_token, dtype=np.int64)
+        if cid.shape != (N,):
+            raise ConfigError("chunk_of_token must have one label per token")
+        order = np.argsort(cid, kind="stable")
+        sel, cid = sel[order], cid[order]
+        ids, counts = np.unique(cid, return_counts=True)
+        bounds = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        return cls(model, _planes_from_tokens(model, sel.astype(np.uint8), device), 0, N, ids.astype(np.int64), bounds)
+
+
+def _plane_stride(n_tokens: int, K: int) -> int:
+    return max(16, (n_tokens * K + 15) // 16 * 16)
+
+
+def _planes_from_tokens(model: ModelSpec, sel: np.ndarray, device=None):
+    t = _lib.torch()
+    N = sel.shape[0]
+    stride = _plane_stride(N, model.K)
+    host = np.zeros((model.L, stride), dtype=np.uint8)
+    host[:, :N * model.K] = sel.transpose(1, 0, 2).reshape(model.L, N * model.K)
+    x = t.from_numpy(host)
+    if device is not None:
+        x = x.to(device)
+    elif t.cuda.is_available():
+        x = x.to(_lib.require_cuda())
+    return x
+
+
+def default_attention_placement(model: ModelSpec, order: Sequence[int]) -> AttentionPlacement:
+    """d_l = order[floor(l*S/L)], c_l = d_{l+1}, c_{L-1} = d_{L-1}."""
+    order = list(order)
+    S, L = len(order), model.L
+    if S < 1:
+        raise ConfigError("at least one device is required")
+    d = np.array([order[(l * S) // L] for l in range(L)], dtype=np.int32)
+    c = np.concatenate([d[1:], d[-1:]]).astype(np.int32)
+    return AttentionPlacement(d, c)
+
+
+# ---- synthetic traces ----------------------------------------------
+
+_W_SCALE = 1 << 30
+
+
+def zipf_weights(E: int, s: float) -> np.ndarray:
+    """Integer Zipf(s) weights over ranks 1..E: max(1, floor(2^30 * r^-s / sum_j j^-s))."""
+    if s < 0:
+        raise ConfigError(f"zipf_s must be >= 0, got {s}")
+    r = np.arange(1, E + 1, dtype=np.float64)
+    raw = r ** (-float(s))
+    return np.maximum(1, np.floor(raw / raw.sum() * _W_SCALE)).astype(np.int64)
+
+
+def zipf_cdf(E: int, s: float) -> np.ndarray:
+    w = zipf_weights(E, s)
+    return np.concatenate([[0], np.cumsum(w)]).astype(np.uint32)
+
+
+_M0, _M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+_W0, _W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+PERM_STREAM = 0x40000000  # counter word 3 of the permutation stream (draws use k/4 < 2^30)
+
+
+def philox4x32_10(c0, c1, c2, c3, seed: int):
+    """Vectorised Philox4x32-10 over uint32 arrays (Salmon et al., SC'11); key = seed lo/hi."""
+    c0, c1, c2, c3 = (np.asarray(c, dtype=np.uint32).copy() for c in (c0, c1, c2, c3))
+    k0 = np.uint32(seed & 0xFFFFFFFF)
+    k1 = np.uint32((seed >> 32) & 0xFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = _M0 * c0.astype(np.uint64)
+            p1 = _M1 * c2.astype(np.uint64)
+            hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), p0.astype(np.uint32)
+            hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), p1.astype(np.uint32)
+            c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+            k0 = np.uint32((int(k0) + int(_W0)) & 0xFFFFFFFF)
+            k1 = np.uint32((int(k1) + int(_W1)) & 0xFFFFFFFF)
+    return c0, c1, c2, c3
+
+
+def layer_permutations(seed: int, L: int, E: int) -> np.ndarray:
+    """Per-layer rank -> expert permutation: Fisher-Yates, j drawn from
+    Philox(counter = (i, 0, l, PERM_STREAM)) as floor(u * (i+1) / 2^32)."""
+    seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    i = np.arange(E, dtype=np.uint32)
+    perm = np.tile(np.arange(E, dtype=np.int64), (L, 1))
+    for l in range(L):
+        u, _, _, _ = philox4x32_10(i, np.zeros(E, np.uint32), np.full(E, l, np.uint32),
+                                   np.full(E, PERM_STREAM, np.uint32), seed)
+        j = (u.astype(np.uint64) * (i.astype(np.uint64) + np.uint64(1))) >> np.uint64(32)
+        p = perm[l]
+        for k in range(E - 1, 0, -1):
+            jj = int(j[k])
+            p[k], p[jj] = p[jj], p[k]
+    return perm.astype(np.uint8 if E <= 256 else np.int64)
+
+
+def chunk_bounds_even(n_tokens: int, n_chunks: int) -> np.ndarray:
+    """Tokens evenly labelled into chunks: chunk(t) = floor(t*C/N), i.e. chunk c owns
+    tokens [ceil(c*N/C), ceil((c+1)*N/C))."""
+    N, C = int(n_tokens), int(n_chunks)
+    return np.array([(c * N + C - 1) // C for c in range(C + 1)], dtype=np.int64)
+
+
+def generate_trace(model: ModelSpec, zipf_s: float, n_tokens: int, n_chunks: int, seed: int,
+                   tok_range: Optional[tuple[int, int]] = None) -> ActivationTrace:
+    """SPEC.md:123-131.  Generated on the GPU (``mp_gen_trace``).  ``tok_range=(a, b)`` generates
+    only tokens [a, b) of the n_tokens-token trace (a shard): bit-identical to the same tokens of
+    the full trace, with chunk labels of the full trace."""
+    t = _lib.torch()
+    if model.E > MAX_EXPERTS:
+        raise ConfigError(f"E = {model.E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
+    if n_tokens < 0 or n_chunks < 1:
+        raise ConfigError("n_tokens must be >= 0 and n_chunks >= 1")
+    a, b = (0, int(n_tokens)) if tok_range is None else (int(tok_range[0]), int(tok_range[1]))
+    if not (0 <= a <= b <= n_tokens):
+        raise ConfigError(f"tok_range {tok_range} outside [0, {n_tokens}]")
+    dev = _lib.require_cuda()
+    L, E, K = model.L, model.E, model.K
+    n = b - a
+    planes = t.empty((L, _plane_stride(n, K)), dtype=t.uint8, device=dev)
+    cdf = _lib.to_dev(zipf_cdf(E, zipf_s).astype(np.int64), t.int64).to(t.int32)  # bit pattern of uint32
+    perm = _lib.to_dev(layer_permutations(seed, L, E), t.uint8)
+    _lib.call("mp_gen_trace", int(seed) & 0xFFFFFFFFFFFFFFFF, a, b, L, K, E, _lib.ptr(cdf), _lib.ptr(perm),
+              _lib.ptr(planes), planes.shape[1], _lib.stream_handle())
+    full = chunk_bounds_even(n_tokens, n_chunks)
+    bounds = np.clip(full, a, b) - a
+    return ActivationTrace(model, planes, 0, n, np.arange(n_chunks, dtype=np.int64), bounds, _validated=True)
+
+
+# ---- text format ---------------------------------------------------
+
+_HEADER = re.compile(r"^#moeplace-trace v1 L=(\d+) E=(\d+) K=(\d+)\s*$")
+_FIELD = re.compile(r"^(?:layer)?(\d+):(.*)$")
+
+
+def parse_trace(path) -> ActivationTrace:
+    """Parse the text trace format; errors carry the 1-based line number (header = line 1)."""
+    with open(path, "r") as f:
+        text = f.read()
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        t = _lib.torch()
+        return ActivationTrace(None, t.zeros((0, 16), dtype=t.uint8), 0, 0, np.zeros(0, np.int64),
+                               np.zeros(1, np.int64), source_is_file=True)
+    m = _HEADER.match(lines[0])
+    if not m:
+        raise TraceParseError("missing or malformed header '#moeplace-trace v1 L=<L> E=<E> K=<K>'", 1)
+    try:
+        model = ModelSpec(int(m.group(1)), int(m.group(2)), int(m.group(3)))
+    except ConfigError as e:
+        raise TraceParseError(str(e), 1) from None
+    L, E, K = model.L, model.E, model.K
+    N = len(lines) - 1
+    sel = np.empty((N, L, K), dtype=np.int64)
+    cid = np.empty(N, dtype=np.int64)
+    for i, line in enumerate(lines[1:]):
+        ln = i + 2
+        parts = line.rstrip("\r").split("\t")
+        if len(parts) != L + 1:
+            raise TraceParseError(f"expected {L} layer fields, found {len(parts) - 1}", ln)
+        try:
+            cid[i] = int(parts[0])
+        except ValueError:
+            raise TraceParseError(f"bad chunk id {parts[0]!r}", ln) from None
+        if cid[i] < 0:
+            raise TraceParseError(f"negative chunk id {cid[i]}", ln)
+        for l in range(L):
+            fm = _FIELD.match(parts[l + 1])
+            if not fm or int(fm.group(1)) != l:
+                raise TraceParseError(f"malformed field {parts[l + 1]!r} (expected layer{l}:e,...)", ln)
+            items = fm.group(2).split(",")
+            if len(items) != K:
+                raise TraceParseError(f"layer {l}: expected {K} experts, found {len(items)}", ln)
+            try:
+                vals = [int(v) for v in items]
+            except ValueError:
+                raise TraceParseError(f"layer {l}: non-integer expert index", ln) from None
+            for v in vals:
+                if v < 0 or v >= E:
+                    raise TraceParseError(f"layer {l}: expert index {v} outside [0, {E})", ln)
+            if len(set(vals)) != K:
+                raise TraceParseError(f"layer {l}: repeated expert index", ln)
+            sel[i, l] = vals
+    if E > MAX_EXPERTS:
+        raise ConfigError(f"E = {E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
+    tr = ActivationTrace.from_tokens(model, sel.astype(np.uint8), cid, device="cpu")
+    tr.source_is_file = True
+    tr._validated = True
+    return tr
+
+
+def write_trace(trace: ActivationTrace, path) -> None:
+    """Canonical text form: header, then one line per token in chunk-grouped order."""
+    m = trace.model
+    with open(path, "w") as f:
+        if m is None:
+            return
+        f.write(f"#moeplace-trace v1 L={m.L} E={m.E} K={m.K}\n")
+        sel = trace.tokens()
+        cid = trace.token_chunk_ids()
+        prefixes = [f"layer{l}:" for l in range(m.L)]
+        for t in range(sel.shape[0]):
+            f.write(str(int(cid[t])) + "\t" + "\t".join(
+                prefixes[l] + ",".join(str(int(v)) for v in sel[t, l]) for l in range(m.L)) + "\n")
+
+
+def validate_trace(trace: ActivationTrace) -> None:
+    """Check the ActivationTrace invariants on the device (``mp_validate_u8``)."""
+    if trace._validated or trace.n_tokens == 0:
+        return
+    m = trace.model
+    planes = trace.device_planes()
+    err = _lib.new_err()
+    _lib.call("mp_validate_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K, m.E,
+              _lib.ptr(err), _lib.stream_handle())
+    flag, enc, _, n = _lib.read_err(err)
+    if flag:
+        key = (2 ** 63 - 1) - enc
+        code, tl = key % 8, key // 8
+        tok, layer = tl // m.L, tl % m.L
+        what = "expert index >= E" if code == _lib.DATA_EXPERT_RANGE else "repeated expert index"
+        if trace.source_is_file:
+            raise TraceParseError(f"layer {layer}: {what}", tok - trace.tok_begin + 2)
+        raise MoeplaceError(f"token {tok - trace.tok_begin}, layer {layer}: {what} ({n} bad records)")
+    trace._validated = True
+
+
+# ---- statistics -----------------------------------------------------------
+
+def trace_counts(trace: ActivationTrace):
+    """Exact per-(layer, expert) selection counts as a device int64 [L, E] tensor (``mp_hist_u8``)."""
+    t = _lib.torch()
+    m = trace.model
+    planes = trace.device_planes()
+    validate_trace(trace)
+    counts = t.zeros((m.L, m.E), dtype=t.int64, device=planes.device)
+    err = _lib.new_err()
+    _lib.call("mp_hist_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K, m.E,
+              _lib.ptr(counts), _lib.ptr(err), _lib.stream_handle())
+    _lib.check_err(err, "estimate_frequencies")
+    return counts
+
+
+def frequencies_from_counts(counts: np.ndarray, n_tokens: int, K: int) -> FrequencyTable:
+    counts = np.asarray(counts, dtype=np.int64)
+    return FrequencyTable(counts / (K * n_tokens), counts, int(n_tokens), int(K))
+
+
+def estimate_frequencies(trace: ActivationTrace, model: Optional[ModelSpec] = None) -> FrequencyTable:
+    """f[l, e] = count(l, e) / (K * n_tokens), counted on the GPU."""
+    model = model or trace.model
+    if trace.n_tokens == 0 or model is None:
+        raise MoeplaceError("estimate_frequencies: empty trace (no silent uniform fallback)")
+    if trace.model is not None and trace.model != model:
+        raise ConfigError(f"trace shape {trace.model} does not match model {model}")
+    counts = trace_counts(trace).cpu().numpy()
+    return frequencies_from_counts(counts, trace.n_tokens, model.K)
+
+
+def split_trace(trace: ActivationTrace, train_chunks: int, test_chunks: int):
+    """the first ``train_chunks`` chunks (in id order) train, the next
+    ``test_chunks`` test.  Both are zero-copy views of the same device planes."""
+    if train_chunks < 0 or test_chunks < 0 or train_chunks + test_chunks > trace.n_chunks:
+        raise ConfigError(f"cannot split {trace.n_chunks} chunks into {train_chunks} train + {test_chunks} test")
+    return trace.view(0, train_chunks), trace.view(train_chunks, train_chunks + test_chunks)
+
+
+def trace_stats(trace: ActivationTrace) -> dict:
+    """Summary used by ``moeplace trace stats``."""
+    freq = estimate_frequencies(trace)
+    top = freq.f.max(axis=1)
+    return {"n_tokens": trace.n_tokens, "n_chunks": trace.n_chunks,
+            "L": trace.model.L, "E": trace.model.E, "K": trace.model.K,
+            "max_f": float(top.max()), "mean_top1_f": float(top.mean()),
+            "uniform_f": 1.0 / trace.model.E}

@@ -1,0 +1,322 @@
+"""GPU parity: every device kernel against the CPU oracle, bit-exact (integers) on identical
+seeded inputs, through the public API and hence the C-ABI (libmoeplace_cuda.so)."""
+import numpy as np
+import pytest
+
+import moeplace.eval as ev
+import moeplace.model_trace as mt
+import moeplace.placement as mpl
+import moeplace.solver as sv
+import moeplace.topology as topo
+from moeplace.errors import ConfigError, MoeplaceError, TopologyError, TraceParseError
+from oracle import evaluate as oe
+from oracle import gen as og
+from oracle import stats as ost
+from oracle import topology as ot
+
+from helpers import B16, R1, oracle_cost, oracle_sums, random_assign, setup_topology
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [R1, B16, (3, 5, 2), (2, 4, 4), (1, 256, 1), (5, 200, 7)]
+
+
+def _planes_tokens(tr):
+    return tr.tokens()
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("s", [0.0, 1.2, 2.0])
+def test_generate_matches_oracle(shape, s):
+    L, E, K = shape
+    N, C, seed = 1001, 7, 12345
+    tr = mt.generate_trace(mt.ModelSpec(L, E, K), s, N, C, seed)
+    sel, bounds = og.generate(L, E, K, s, N, C, seed)
+    assert np.array_equal(tr.tokens(), sel)
+    assert np.array_equal(tr.chunk_bounds, bounds)
+
+
+@pytest.mark.parametrize("shape", [R1, B16])
+def test_generate_shard_is_bit_identical(shape):
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    full = mt.generate_trace(m, 1.2, 5000, 13, 99).tokens()
+    for a, b in [(0, 1), (17, 1234), (4999, 5000), (2500, 5000)]:
+        part = mt.generate_trace(m, 1.2, 5000, 13, 99, tok_range=(a, b))
+        assert np.array_equal(part.tokens(), full[a:b])
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("s", [0.0, 1.2, 2.0])
+def test_hist_matches_oracle(shape, s):
+    L, E, K = shape
+    N = 3001
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, s, N, 10, 7)
+    sel, _ = og.generate(L, E, K, s, N, 10, 7)
+    want = ost.counts(sel, E)
+    f = mt.estimate_frequencies(tr, m)
+    assert np.array_equal(f.counts, want)
+    assert np.array_equal(f.counts, ost.counts_bincount(sel, E))
+    assert np.array_equal(f.f, ost.frequencies(want, N, K))
+
+
+@pytest.mark.parametrize("shape", [R1, B16, (3, 5, 2)])
+def test_hist_on_unaligned_views(shape):
+    """Token ranges whose byte offsets are not 16-aligned (split views) and tiny ranges."""
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 2000, 40, 3)
+    sel = tr.tokens()
+    for lo, hi in [(0, 1), (3, 4), (1, 39), (13, 27), (39, 40), (0, 40)]:
+        v = tr.view(lo, hi)
+        got = mt.estimate_frequencies(v, m).counts
+        a, b = tr.chunk_bounds[lo], tr.chunk_bounds[hi]
+        assert np.array_equal(got, ost.counts(sel[a:b], E)), (lo, hi)
+
+
+def _assert_scores(tr, placements, costs_np, sel, bounds, t0=0):
+    got = ev.score_sums(tr, placements, [c for c, _ in costs_np])
+    for i, (pl, (_, p)) in enumerate(zip(placements, costs_np)):
+        want = oracle_sums(sel, p, pl.assign, bounds, t0)
+        assert np.array_equal(got[i], want), i
+
+
+@pytest.mark.parametrize("P", [1, 3, 4, 5, 8, 9, 16, 17, 33])
+def test_score_matches_oracle_R1(P):
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("FatTree", 8, 4, 8, m)
+    _, p = oracle_cost(g, attn)
+    assert np.array_equal(cost.numpy(), p)
+    tr = mt.generate_trace(m, 1.2, 4099, 33, 5)
+    sel, bounds = og.generate(L, E, K, 1.2, 4099, 33, 5)
+    rng = np.random.default_rng(P)
+    pls = [mpl.Placement(random_assign(rng, L, E, g.n_devices)) for _ in range(P)]
+    _assert_scores(tr, pls, [(cost, p)] * P, sel, bounds)
+
+
+@pytest.mark.parametrize("kind", ["FatTree", "FatTreeHier", "Dragonfly", "DragonflySparse"])
+def test_score_multi_topology_16B(kind):
+    """16B shape: 162 B/token is not 16-byte aligned; several topologies in one batch."""
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 2777, 11, 8)
+    sel, bounds = og.generate(L, E, K, 1.2, 2777, 11, 8)
+    costs, pls = [], []
+    for i, kd in enumerate([kind, "FatTree", "Dragonfly"]):
+        g, dist, order, attn, cost = setup_topology(kd, 4, 2, 4, m)
+        _, p = oracle_cost(g, attn)
+        for j in range(3):
+            pls.append(mpl.Placement(random_assign(np.random.default_rng(10 * i + j), L, E, g.n_devices)))
+            costs.append((cost, p))
+    _assert_scores(tr, pls, costs, sel, bounds)
+
+
+def test_score_views_and_empty_chunks():
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 2.0, 90, 150, 1)  # N < C: many empty chunks
+    sel, bounds = og.generate(L, E, K, 2.0, 90, 150, 1)
+    g, dist, order, attn, cost = setup_topology("Dragonfly", 8, 1, 4, m)
+    _, p = oracle_cost(g, attn)
+    pl = mpl.Placement(random_assign(np.random.default_rng(0), L, E, g.n_devices))
+    rep = ev.evaluate(tr, pl, cost)
+    want = oracle_sums(sel, p, pl.assign, bounds)
+    assert rep.chunk_hop_sums == want.tolist()
+    r = oe.report(want, np.diff(bounds))
+    assert rep.mean_hops_per_token == r["mean"] and rep.std_hops == r["std"]
+    assert rep.empty_chunks == r["empty_chunks"] == 60
+    train, test = mt.split_trace(tr, 100, 50)
+    rt = ev.evaluate(test, pl, cost)
+    assert rt.chunk_hop_sums == want[100:150].tolist()
+
+
+@pytest.mark.parametrize("maxp_kind", ["small", "mid", "large"])
+def test_score_widening_paths(maxp_kind):
+    """u8-lane widening intervals (max_p <= 15, <= 63, <= 255) give identical sums."""
+    L, E, K = (4, 64, 8)
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 3333, 5, 2)
+    sel, bounds = og.generate(L, E, K, 1.2, 3333, 5, 2)
+    hi = {"small": 15, "mid": 63, "large": 255}[maxp_kind]
+    rng = np.random.default_rng(hi)
+    S = 16
+    p = rng.integers(0, hi + 1, size=(L, S)).astype(np.uint8)
+    p[0, 0] = hi
+    import torch
+    cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(6)]
+    _assert_scores(tr, pls, [(cost, p)] * 6, sel, bounds)
+
+
+def test_fused_hist_score_matches():
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("DragonflySparse", 16, 4, 4, m)
+    _, p = oracle_cost(g, attn)
+    tr = mt.generate_trace(m, 1.2, 3001, 20, 4)
+    sel, bounds = og.generate(L, E, K, 1.2, 3001, 20, 4)
+    train, _ = mt.split_trace(tr, 13, 7)
+    rng = np.random.default_rng(1)
+    pls = [mpl.Placement(random_assign(rng, L, E, g.n_devices)) for _ in range(4)]
+    freq, reps = ev.evaluate_with_stats(train, pls, cost)
+    b = bounds[13]
+    assert np.array_equal(freq.counts, ost.counts(sel[:b], E))
+    for pl, rep in zip(pls, reps):
+        assert rep.chunk_hop_sums == oracle_sums(sel[:b], p, pl.assign, bounds[:14]).tolist()
+
+
+@pytest.mark.parametrize("kind,leaves,spl,gps", [
+    ("FatTree", 16, 4, 4), ("FatTreeHier", 16, 4, 4), ("Dragonfly", 16, 4, 4), ("DragonflySparse", 16, 4, 4),
+    ("DragonflySparse", 64, 1, 1), ("Dragonfly", 64, 1, 1), ("FatTree", 8, 4, 8), ("DragonflyPlus", 16, 4, 4),
+    ("SlimFly", 18, 1, 2), ("SlimFly", 50, 1, 1), ("FatTreeHier", 3, 2, 1), ("DragonflySparse", 1, 1, 4)])
+def test_apsp_matches_bfs_oracle(kind, leaves, spl, gps):
+    import networkx as nx
+    g = topo.build_topology(topo.TopologySpec(kind, leaves, spl, gps))
+    d = topo.all_pairs_hops(g)
+    want = ot.server_hops(g.n_nodes, g.links.tolist(), g.n_servers)
+    assert np.array_equal(d.server_numpy(), want)
+    G = nx.Graph()
+    G.add_nodes_from(range(g.n_nodes))
+    G.add_edges_from(g.links.tolist())
+    sp = dict(nx.all_pairs_shortest_path_length(G))
+    assert all(want[a, b] == sp[a][b] for a in range(g.n_servers) for b in range(g.n_servers))
+    D = d.numpy()
+    assert np.array_equal(D, ot.device_hops(want, g.device_server))
+    assert (D == D.T).all() and (np.diag(D) == 0).all()
+
+
+def test_apsp_disconnected_raises():
+    g = topo.build_topology(topo.TopologySpec("FatTree", 2, 1, 1, {"spines": 1}))
+    g.links = g.links[:-1]  # drop a leaf-spine link
+    with pytest.raises(TopologyError):
+        topo.all_pairs_hops(g)
+
+
+def test_cost_matrix_matches_oracle():
+    for kind in ("FatTree", "FatTreeHier", "Dragonfly", "DragonflySparse"):
+        m = mt.ModelSpec(58, 256, 8)
+        g, dist, order, attn, cost = setup_topology(kind, 16, 4, 4, m)
+        _, p = oracle_cost(g, attn)
+        assert np.array_equal(cost.numpy(), p)
+
+
+@pytest.mark.parametrize("uniform", [True, False])
+def test_coefficients_bit_exact(uniform):
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("Dragonfly", 2, 2, 8, m)
+    tr = mt.generate_trace(m, 1.2, 5000, 10, 3)
+    c = mpl.Constraints(54, 2)
+    if uniform:
+        inst = sv.build_instance(cost, sv.UniformFrequencies(E), c)
+        f = np.full((L, E), 1.0 / E)
+    else:
+        freq = mt.estimate_frequencies(tr, m)
+        inst = sv.build_instance(cost, freq, c)
+        f = freq.counts / (K * 5000)
+    w, wi = ot.coefficients(f, cost.numpy())
+    assert np.array_equal(inst.w_numpy(), w)  # bit-identical float64
+    assert np.array_equal(inst.w_int_numpy(), wi)
+
+
+def test_comm_map_matches_oracle():
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("FatTreeHier", 8, 2, 2, m)
+    tr = mt.generate_trace(m, 1.2, 2000, 10, 3)
+    pl = mpl.place_greedy(m, attn, cost, mpl.Constraints(64, 2))
+    cm = ev.communication_map(tr, pl, cost)
+    cnt = ost.counts(tr.tokens(), E)
+    sym, raw = oe.comm_map(cnt, pl.assign, g.device_server, dist.server_numpy(), attn.dispatch, attn.collect, 2000)
+    assert np.array_equal(cm.raw, raw)
+    assert np.array_equal(cm.traffic, sym)
+    rep = ev.evaluate(tr, pl, cost)
+    assert abs(cm.traffic.sum() - rep.mean_hops_per_token) <= 1e-9 * rep.mean_hops_per_token
+    assert np.allclose(cm.traffic, cm.traffic.T) and (np.diag(cm.traffic) == 0).all()
+
+
+def test_golden_fixture(golden_dir):
+    z = np.load(golden_dir / "oracle_small.npz")
+    L, E, K, N, C = (int(z[k]) for k in ("L", "E", "K", "N", "C"))
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, float(z["zipf_s"]), N, C, int(z["seed"]))
+    assert np.array_equal(tr.tokens(), z["sel"])
+    assert np.array_equal(mt.estimate_frequencies(tr, m).counts, z["counts"])
+    import torch
+    cost = mpl.CostMatrix(torch.as_tensor(z["p"].astype(np.uint8), device="cuda"))
+    rep = ev.evaluate(tr, mpl.Placement(z["assign"]), cost)
+    assert rep.chunk_hop_sums == z["sums"].tolist()
+
+
+def test_token_hops_spec_examples():
+    import torch
+    p = mpl.CostMatrix(torch.as_tensor(np.array([[4, 2]], np.uint8), device="cuda"))
+    assert ev.token_hops([[0, 1]], mpl.Placement(np.array([[0, 1]])), p) == 6
+    p0 = mpl.CostMatrix(torch.as_tensor(np.array([[0, 4, 4]], np.uint8), device="cuda"))
+    assert ev.token_hops([[0, 2]], mpl.Placement(np.array([[0, 0, 0]])), p0) == 0
+
+
+def test_data_errors_are_reported():
+    m = mt.ModelSpec(2, 4, 2)
+    sel = np.array([[[0, 1], [2, 3]], [[1, 1], [0, 2]]], dtype=np.uint8)  # token 1 layer 0 repeats
+    tr = mt.ActivationTrace.from_tokens(m, sel)
+    with pytest.raises(MoeplaceError):
+        mt.estimate_frequencies(tr, m)
+    bad = np.array([[[0, 9], [2, 3]]], dtype=np.uint8)
+    import torch
+    tr2 = mt.ActivationTrace(m, mt._planes_from_tokens(m, bad), 0, 1, np.zeros(1, np.int64),
+                             np.array([0, 1], np.int64))
+    with pytest.raises(MoeplaceError):
+        mt.estimate_frequencies(tr2, m)
+    with pytest.raises(MoeplaceError):
+        mt.estimate_frequencies(tr.view(0, 0), m)
+
+
+def test_parse_file_errors_carry_line_numbers(tmp_path):
+    m = mt.ModelSpec(2, 4, 2)
+    tr = mt.generate_trace(m, 1.2, 5, 2, 1)
+    f = tmp_path / "t.txt"
+    mt.write_trace(tr, f)
+    lines = f.read_text().splitlines()
+    lines[3] = lines[3].replace("layer1:", "layer1:4,")  # wrong count at line 4
+    f.write_text("\n".join(lines) + "\n")
+    with pytest.raises(TraceParseError) as ei:
+        mt.parse_trace(f)
+    assert ei.value.line_no == 4
+
+
+def test_large_trace_properties():
+    """At BASELINE's full R1 size (10M tokens): size-independent properties + a sampled oracle
+    check on a shard regenerated independently on the CPU."""
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    N, C = 10_000_000, 150
+    tr = mt.generate_trace(m, 1.2, N, C, 0)
+    cnt = mt.estimate_frequencies(tr, m).counts
+    assert (cnt.sum(axis=1) == N * K).all()
+    import torch
+    S = 64
+    q = np.full((L, S), 3, np.uint8)
+    cost = mpl.CostMatrix(torch.as_tensor(q, device="cuda"))
+    rng = np.random.default_rng(0)
+    pl = mpl.Placement(random_assign(rng, L, E, S))
+    rep = ev.evaluate(tr, pl, cost)
+    assert rep.hop_sum == 3 * N * L * K  # constant p -> every pick costs 3
+    # linearity: score(p1) + score(p2) == score(p1 + p2)
+    p1 = rng.integers(0, 8, (L, S)).astype(np.uint8)
+    p2 = rng.integers(0, 8, (L, S)).astype(np.uint8)
+    c1, c2, c12 = (mpl.CostMatrix(torch.as_tensor(x, device="cuda")) for x in (p1, p2, p1 + p2))
+    s = ev.score_sums(tr, [pl, pl, pl], [c1, c2, c12])
+    assert np.array_equal(s[0] + s[1], s[2])
+    # identity with the histogram: sum_{l,e} count * pe == total hops
+    pe = oe.pe_table(p1, pl.assign)
+    assert int((cnt * pe).sum()) == int(s[0].sum())
+    # sampled oracle check: tokens [a, b) regenerated on the CPU
+    a, b = 4_321_000, 4_331_000
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 0, tok_range=(a, b))
+    sh = mt.generate_trace(m, 1.2, N, C, 0, tok_range=(a, b))
+    assert np.array_equal(sh.tokens(), sel)
+    got = ev.score_sums(sh, [pl], c1)[0]
+    assert np.array_equal(got, oe.chunk_sums(sel, pe, bounds, a))
