@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the moeplace hot path on B200 (driver contract).
+
+Workload (BASELINE.json configs[1], "config 2"): DeepSeek-R1 shape (L=58 MoE layers, E=256 experts,
+top-K=8), 10M synthetic Zipf(s=1.2) tokens per GPU in 150 chunks per 10M tokens, FatTree
+8 leaves x 4 servers x 8 GPUs (256 devices, 32 servers, 4 spines), c_layer=1, c_exp=64.
+Placements scored: RR, Greedy, ILP and ILPLoad (P=4), computed in the untimed setup.
+
+One step = one pass over the resident trace that builds the per-(layer, expert) load counts
+(estimate_frequencies) AND scores the P=4 placements (per-chunk hop sums of evaluate), i.e.
+"hist over all N and score of P=4 over all N" — by default with the fused kernel
+(mp_hist_score_u8), or with --mode separate as mp_hist_u8 + mp_score_u8.  For N GPUs each rank
+owns a contiguous 10M-token shard of one N*10M-token trace (weak scaling) and the packed int64
+[counts | hop sums] buffer is combined with one NCCL all_reduce inside the timed step.
+
+value  = token-layers scored x placements per second, whole job: N*10M*58*4 / step time.
+e2e    = the same metric through the public API (moeplace.eval.evaluate_with_stats) on a trace
+         held in pinned HOST memory: the H2D copy (streamed in slices, overlapped with the
+         kernels), the kernels and the D2H of counts + sums are all inside the timed region.
+--impl reference: the CPU restatement of the reference path (oracle/, numba, all host cores)
+         on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L, E, K = 58, 256, 8
+ZIPF_S, SEED = 1.2, 0
+TOK_PER_GPU = 10_000_000
+CHUNKS_PER_GPU = 150
+P = 4
+METRIC = "token-layers scored/sec (x placements) and achieved HBM GB/s"
+UNIT = "token-layers*placements/s"
+
+
+def workload(n_gpus: int, tok: int, mode: str) -> dict:
+    return {"workload": "config2: DeepSeek-R1 shape (L=58, E=256, K=8), Zipf(1.2) synthetic trace, "
+                        f"{tok} tokens/GPU, {CHUNKS_PER_GPU} chunks/GPU, FatTree 8 leaves x 4 servers x 8 GPUs "
+                        "(256 devices), c_layer=1, c_exp=64; per step: load histogram + hop sums of P=4 "
+                        "placements (RR, Greedy, ILP, ILPLoad) over every token",
+            "tokens_per_gpu": tok, "tokens_total": tok * n_gpus, "placements": P, "kernel_mode": mode,
+            "l2": f"inputs larger than L2: {tok * L * K / 1e9:.2f} GB trace per GPU vs 126 MB L2, no flush needed",
+            "parallelism": f"token shards x{n_gpus} + 1 NCCL all_reduce of int64 counts|sums" if n_gpus > 1
+            else "single GPU"}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle-reason sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        srt = sorted(sm)
+        loaded = [x for x in srt if x > 0.5 * max(mx)] or srt
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(trace, n_sample: int):
+    """Token-major host copy of the first n_sample tokens of the device trace (same bytes)."""
+    import torch
+    v = trace.planes[:, trace.tok_begin * K:(trace.tok_begin + n_sample) * K].cpu().numpy()
+    return np.ascontiguousarray(v.reshape(L, n_sample, K).transpose(1, 0, 2))
+
+
+def time_oracle(sel, bounds, p, assigns, reps: int = 3):
+    """Seconds per pass of the CPU restatement: counts + per-chunk hop sums of every placement."""
+    from oracle import evaluate as oe
+    from oracle import stats as ost
+    pes = [oe.pe_table(p, a) for a in assigns]
+    ost.counts(sel[:64], E)
+    oe.chunk_sums(sel[:64], pes[0], np.array([0, 64]))  # numba compile outside timing
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ost.counts(sel, E)
+        for pe in pes:
+            oe.chunk_sums(sel, pe, bounds)
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def cpu_threads() -> int:
+    try:
+        import numba
+        return int(numba.get_num_threads())
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference path's CPU implementation (our oracle restatement of
+    SPEC.md; the reference ships no code) on the host cores, bounded sample per step."""
+    if rank != 0:
+        return
+    import numba
+    from oracle import gen as og
+    from oracle import topology as ot
+    n_sample = args.ref_tokens
+    sel, _ = og.generate(L, E, K, ZIPF_S, TOK_PER_GPU, CHUNKS_PER_GPU, SEED, tok_range=(0, n_sample))
+    bounds = np.minimum(np.array([(c * TOK_PER_GPU + CHUNKS_PER_GPU - 1) // CHUNKS_PER_GPU
+                                  for c in range(CHUNKS_PER_GPU + 1)]), n_sample)
+    # FatTree 8x4x8 server graph: servers 0..31, leaves 32..39, spines 40..43
+    links = [(s, 32 + s // 4) for s in range(32)] + [(32 + l, 40 + sp) for l in range(8) for sp in range(4)]
+    dsrv = ot.server_hops(44, links, 32)
+    dev_srv = np.repeat(np.arange(32), 8)
+    disp = np.array([(l * 256) // L for l in range(L)])
+    coll = np.concatenate([disp[1:], disp[-1:]])
+    p = ot.cost_matrix(dsrv, dev_srv, disp, coll)
+    rng = np.random.default_rng(0)
+    assigns = [np.stack([rng.permutation(256) for _ in range(L)]).astype(np.int32) for _ in range(P)]
+    threads = numba.get_num_threads()
+    time_oracle(sel[:1000], bounds, p, assigns, reps=1)
+    for _ in range(args.warmup):
+        time_oracle(sel, bounds, p, assigns, reps=1)
+    times = [time_oracle(sel, bounds, p, assigns, reps=1) for _ in range(args.steps)]
+    t = float(np.mean(times))
+    value = n_sample * L * P / t
+    sample = (f"{n_sample} tokens (first {n_sample} of the config-2 trace, regenerated on the CPU), counts + "
+              f"hop sums of {P} placements per step; numba parallel, {threads} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": workload(world, TOK_PER_GPU, "cpu-oracle"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
+    ap.add_argument("--tokens", type=int, default=TOK_PER_GPU, help="tokens per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-tokens", type=int, default=1_000_000, help="cpu_baseline sample (tokens)")
+    ap.add_argument("--ref-tokens", type=int, default=1_000_000, help="--impl reference sample per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import moeplace.eval as ev
+    import moeplace.model_trace as mt
+    import moeplace.placement as mpl
+    import moeplace.solver as sv
+    import moeplace.topology as topo
+    from paper_2508_09229_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---------------- setup (untimed) ----------------
+    n = args.tokens
+    model = mt.ModelSpec(L, E, K)
+    c = mpl.Constraints(64, 1)
+    g = topo.build_topology(topo.TopologySpec("FatTree", 8, 4, 8, {"spines": 4}))
+    dmat = topo.all_pairs_hops(g)
+    order = topo.locality_order(g, dmat)
+    attn = mt.default_attention_placement(model, order)
+    cost = mpl.cost_matrix(dmat, attn)
+    n_total, c_total = n * world, CHUNKS_PER_GPU * world
+    trace = mt.generate_trace(model, ZIPF_S, n_total, c_total, SEED, tok_range=(rank * n, (rank + 1) * n))
+    counts0 = mt.trace_counts(trace)
+    if world > 1:
+        dist.all_reduce(counts0)
+    freq = mt.frequencies_from_counts(counts0.cpu().numpy(), n_total, K)
+    rr = mpl.place_round_robin(model, attn, order, c)
+    gr = mpl.place_greedy(model, attn, cost, c)
+    ilp, _ = sv.solve_exact(sv.build_instance(cost, sv.UniformFrequencies(E), c))
+    ilpl, _ = sv.solve_exact(sv.build_instance(cost, freq, c))
+    placements = [rr, gr, ilp, ilpl]
+    for lbl, pl in zip(("rr", "greedy", "ilp", "ilpload"), placements):
+        pl.label = lbl
+    tables, max_p = ev._group_tables(placements, [cost] * P, model, 1)
+    C = trace.n_chunks
+    buf = torch.zeros(L * E + P * C, dtype=torch.int64, device=dev)  # packed [counts | sums]
+    counts, sums = buf[:L * E], buf[L * E:]
+    bounds = _lib.to_dev(trace.chunk_bounds, torch.int64)
+    err = _lib.new_err()
+    planes = trace.planes
+    stride = planes.shape[1]
+    t0, t1 = trace.tok_begin, trace.tok_end
+    stream = torch.cuda.current_stream()
+    sh = _lib.stream_handle()
+    k_start, k_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k2_start, k2_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernel_ms, kernel2_ms = [], []
+    sums1 = torch.zeros(4 * C, dtype=torch.int64, device=dev)
+
+    def step(timed: bool):
+        buf.zero_()
+        if args.mode == "fused":
+            if timed:
+                k_start.record(stream)
+            _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err), sh)
+            if timed:
+                k_end.record(stream)
+        else:
+            if timed:
+                k_start.record(stream)
+            _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(counts), _lib.ptr(err), sh)
+            if timed:
+                k_end.record(stream)
+                k2_start.record(stream)
+            _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C, _lib.ptr(tables),
+                      1, max_p, _lib.ptr(sums), sh)
+            if timed:
+                k2_end.record(stream)
+        if world > 1:
+            dist.all_reduce(buf)
+
+    launches_per_step = 1 if args.mode == "fused" else 2
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    # correctness gate before timing: integers of this pass == setup histogram
+    if not torch.equal(counts.view(L, E), counts0):
+        raise SystemExit("bench: fused histogram differs from the setup histogram")
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    ev_b.record(stream)
+    torch.cuda.synchronize()
+    # per-kernel times: re-run with per-launch events (kernel share), same stream
+    for _ in range(args.steps):
+        step(True)
+        k_end.synchronize()
+        kernel_ms.append(k_start.elapsed_time(k_end))
+        if args.mode == "separate":
+            k2_end.synchronize()
+            kernel2_ms.append(k2_start.elapsed_time(k2_end))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    total_ms = ev_a.elapsed_time(ev_b)
+    t_step = torch.tensor([total_ms / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
+    ms = float(t_step.item())
+    value = n_total * L * P / (ms / 1e3)
+
+    # roofline of the dominant kernel (algorithmic bytes: one u8 id per (token, layer, pick))
+    peak, peak_src = measured_peak()
+    kms = float(np.mean(kernel_ms))
+    kname = "mp_hist_score_u8 (fused hist+score, W=1)" if args.mode == "fused" else "mp_hist_u8"
+    if args.mode == "separate" and np.mean(kernel2_ms) > kms:
+        kms, kname = float(np.mean(kernel2_ms)), "mp_score_u8 (W=1)"
+    alg_bytes = n * L * K
+    achieved = alg_bytes / (kms / 1e3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            tr = json.loads(tfile.read_text())
+            key = "fused" if args.mode == "fused" else ("score" if "score" in kname else "hist")
+            if tr.get(key, {}).get("tokens") == n:
+                traffic = tr[key]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": kname, "kernel_ms": kms, "alg_bytes_per_launch": alg_bytes,
+                "peak_source": peak_src}
+    if args.mode == "separate":
+        roofline["other_kernel_ms"] = float(np.mean(kernel2_ms)) if "hist" in kname else float(np.mean(kernel_ms))
+
+    # ---------------- e2e through the public API, host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        host = trace.to_host(pin=True)
+        evs = []
+        ev.evaluate_with_stats(host, placements, cost)  # warm-up
+        for _ in range(args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            f_h, reps = ev.evaluate_with_stats(host, placements, cost)  # H2D + kernels + D2H + floats
+            b.record(stream)
+            torch.cuda.synchronize()
+            evs.append(a.elapsed_time(b))
+        if not np.array_equal(f_h.counts, counts0.cpu().numpy() if world == 1 else f_h.counts):
+            raise SystemExit("bench: e2e histogram differs")
+        t_e = torch.tensor([float(np.mean(evs))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e_ms = float(t_e.item())
+        e2e = {"value": n_total * L * P / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(n * L * K * world), "d2h_bytes_per_step": int((L * E + P * C) * 8 * world),
+               "api": "moeplace.eval.evaluate_with_stats(trace in pinned host memory, 4 placements, cost)"}
+        del host
+
+    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ns = min(args.cpu_tokens, n)
+        sel = cpu_sample(trace, ns)
+        bnd = np.minimum(np.asarray(trace.chunk_bounds, dtype=np.int64), ns)
+        p_np = cost.numpy()
+        assigns = [pl.assign for pl in placements]
+        t_cpu = time_oracle(sel, bnd, p_np, assigns, reps=3)
+        thr = cpu_threads()
+        cpu = {"value": ns * L * P / t_cpu, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P} "
+                         f"placements, oracle/ numba parallel, best of 3",
+               "ms_per_sample": t_cpu * 1e3}
+        try:
+            import numba
+            numba.set_num_threads(1)
+            t1c = time_oracle(sel[:ns // 8], np.minimum(bnd, ns // 8), p_np, assigns, reps=1)
+            cpu["value_1_thread"] = (ns // 8) * L * P / t1c
+            numba.set_num_threads(thr)
+        except Exception:
+            pass
+        try:
+            cpu["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+        except Exception:
+            pass
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
+                "config": workload(world, n, args.mode), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+                "hbm_gbs_step": n_total * L * K / (ms / 1e3) / 1e9 / world}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -133,6 +133,13 @@ int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev
                 int n_srv, const int32_t* dispatch, const int32_t* collect, int L, int E, int S,
                 int64_t* traffic, int64_t* err, void* stream);
 
+/* ---- host -> device staging of a token slice of layer planes (end-to-end path) ---------------
+ * Copies `rows` plane rows of `width` bytes from pinned host memory (pitch src_stride) into device
+ * memory (pitch dst_stride) with one 2-D async copy on `stream`.  Used to stream a host-resident
+ * trace through double-buffered device slices while the kernels run on the previous slice.   */
+int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t src_stride, int64_t width, int rows,
+                       void* stream);
+
 /* ---- solve_exact: min-cost flow on the class-compressed FlowNetwork ------
  * HOST function (the ILP solve stays on the host).  Costs w_int[l][e][s] are int64 >= 0 in
  * host memory.  When p (host uint8[L][S]) is given, w_int must depend on s only through

@@ -150,4 +150,12 @@ int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev
                                 S(stream)));
 }
 
+int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t src_stride, int64_t width, int rows,
+                       void* stream) {
+  if (!dst || !src || width < 0 || rows < 0 || dst_stride < width || src_stride < width) return MP_ERR_ARG;
+  if (width == 0 || rows == 0) return MP_OK;
+  return status(cudaMemcpy2DAsync(dst, (size_t)dst_stride, src, (size_t)src_stride, (size_t)width, (size_t)rows,
+                                  cudaMemcpyHostToDevice, S(stream)));
+}
+
 }  // extern "C"

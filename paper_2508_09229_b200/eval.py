@@ -17,7 +17,8 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, MoeplaceError
-from .model_trace import ActivationTrace, FrequencyTable, ModelSpec, frequencies_from_counts, validate_trace
+from .model_trace import (ActivationTrace, FrequencyTable, ModelSpec, frequencies_from_counts, sweep,
+                          validate_trace)
 from .placement import CostMatrix, Placement
 
 MAX_LANES = 16  # placements scored per pass (W = 4 words of four u8 lanes)
@@ -132,19 +133,24 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs) -
         raise MoeplaceError("evaluate: empty trace")
     placements = list(placements)
     costs = _as_costs(costs, len(placements))
-    planes = trace.device_planes()
-    validate_trace(trace)
-    bounds = _lib.to_dev(trace.chunk_bounds, t.int64)
     C = trace.n_chunks
-    out = np.zeros((len(placements), C), dtype=np.int64)
+    dev = _lib.require_cuda()
+    groups = []
     for g0 in range(0, len(placements), MAX_LANES):
         grp = placements[g0:g0 + MAX_LANES]
         W = _lanes_for(len(grp))
         tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], m, W)
-        sums = t.zeros((4 * W, C), dtype=t.int64, device=planes.device)
-        _lib.call("mp_score_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
-                  _lib.ptr(bounds), C, _lib.ptr(tables), W, max_p, _lib.ptr(sums), _lib.stream_handle())
-        out[g0:g0 + len(grp)] = sums[:len(grp)].cpu().numpy()
+        groups.append((g0, len(grp), W, tables, max_p, t.zeros((4 * W, C), dtype=t.int64, device=dev)))
+
+    def launch(planes, stride, t0, t1, bounds):
+        for _, _, W, tables, max_p, sums in groups:
+            _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(sums), _lib.stream_handle())
+
+    sweep(trace, launch)
+    out = np.zeros((len(placements), C), dtype=np.int64)
+    for g0, n, _, _, _, sums in groups:
+        out[g0:g0 + n] = sums[:n].cpu().numpy()
     return out
 
 
@@ -174,17 +180,18 @@ def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement],
         raise MoeplaceError("evaluate: empty trace")
     if not 1 <= len(placements) <= 4:
         raise ConfigError("evaluate_with_stats takes 1..4 placements")
-    planes = trace.device_planes()
-    validate_trace(trace)
+    dev = _lib.require_cuda()
     tables, max_p = _group_tables(placements, [cost] * len(placements), m, 1)
-    bounds = _lib.to_dev(trace.chunk_bounds, t.int64)
     C = trace.n_chunks
-    counts = t.zeros((m.L, m.E), dtype=t.int64, device=planes.device)
-    sums = t.zeros((4, C), dtype=t.int64, device=planes.device)
+    counts = t.zeros((m.L, m.E), dtype=t.int64, device=dev)
+    sums = t.zeros((4, C), dtype=t.int64, device=dev)
     err = _lib.new_err()
-    _lib.call("mp_hist_score_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K, m.E,
-              _lib.ptr(bounds), C, _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err),
-              _lib.stream_handle())
+
+    def launch(planes, stride, t0, t1, bounds):
+        _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, m.E, _lib.ptr(bounds), C,
+                  _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err), _lib.stream_handle())
+
+    sweep(trace, launch)
     _lib.check_err(err, "evaluate_with_stats")
     freq = frequencies_from_counts(counts.cpu().numpy(), trace.n_tokens, m.K)
     s = sums.cpu().numpy()

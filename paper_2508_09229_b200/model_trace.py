@@ -116,6 +116,15 @@ class ActivationTrace:
             self.planes = self.planes.to(dev, non_blocking=True)
         return self.planes
 
+    def to_host(self, pin: bool = True) -> "ActivationTrace":
+        """A copy whose planes live in (pinned) host memory: evaluating it streams the trace
+        through the device slice by slice (the end-to-end path), without caching it there."""
+        h = self.planes.cpu()
+        if pin:
+            h = h.pin_memory()
+        return ActivationTrace(self.model, h, self.tok_begin, self.n_tokens, self.chunk_ids.copy(),
+                               self.chunk_bounds.copy(), self.source_is_file, self._validated)
+
     def tokens(self) -> np.ndarray:
         """Host copy in token-major form, uint8 [N, L, K] (for IO and small-case inspection)."""
         m = self.model
@@ -378,16 +387,80 @@ def validate_trace(trace: ActivationTrace) -> None:
 
 # ---- statistics -----------------------------------------------------------
 
+STREAM_BLOCK_TOKENS = 1 << 20  # host-streaming slice (R1: 464 MB per slice)
+
+
+def sweep(trace: ActivationTrace, launch) -> None:
+    """Run ``launch(planes, stride, t0, t1, bounds)`` over the whole trace.
+
+    Device-resident planes: one call.  Pinned host planes (the end-to-end path): the trace is
+    streamed through two device slices — the 2-D H2D copy of slice i+1 (``mp_copy_planes_h2d`` on
+    a copy stream) overlaps the kernels on slice i — and ``launch`` accumulates per slice (every
+    kernel output is additive over token ranges).  Other host planes are uploaded once and cached.
+    """
+    t = _lib.torch()
+    planes = trace.planes
+    if planes.is_cuda or not planes.is_pinned():
+        planes = trace.device_planes()
+        validate_trace(trace)
+        bounds = _lib.to_dev(trace.chunk_bounds, t.int64)
+        launch(planes, planes.shape[1], trace.tok_begin, trace.tok_end, bounds)
+        return
+    m = trace.model
+    dev = _lib.require_cuda()
+    K = m.K
+    T = min(STREAM_BLOCK_TOKENS, trace.n_tokens)
+    blocks = [(a, min(a + T, trace.tok_end)) for a in range(trace.tok_begin, trace.tok_end, T)]
+    rel = np.stack([np.clip(trace.chunk_bounds, a, b) - a for a, b in blocks]).astype(np.int64)
+    d_rel = _lib.to_dev(rel, t.int64)
+    stride = max(16, (T * K + 15) // 16 * 16)
+    bufs = [t.empty((m.L, stride), dtype=t.uint8, device=dev) for _ in range(min(2, len(blocks)))]
+    comp = t.cuda.current_stream()
+    copy = t.cuda.Stream()
+    copied = [t.cuda.Event() for _ in bufs]
+    free = [t.cuda.Event() for _ in bufs]
+    copy.wait_stream(comp)  # d_rel and the outputs are ready before the first slice lands
+    src_stride = planes.shape[1]
+    for i, (a, b) in enumerate(blocks):
+        j = i % len(bufs)
+        with t.cuda.stream(copy):
+            if i >= len(bufs):
+                copy.wait_event(free[j])
+            _lib.call("mp_copy_planes_h2d", _lib.ptr(bufs[j]), stride, C_void(planes.data_ptr() + a * K), src_stride,
+                      (b - a) * K, m.L, C_void(copy.cuda_stream))
+            copied[j].record(copy)
+        comp.wait_event(copied[j])
+        if not trace._validated:
+            err = _lib.new_err()
+            _lib.call("mp_validate_u8", _lib.ptr(bufs[j]), stride, 0, b - a, m.L, K, m.E, _lib.ptr(err),
+                      _lib.stream_handle())
+            flag, enc, _, n = _lib.read_err(err)
+            if flag:
+                key = (2 ** 63 - 1) - enc
+                raise MoeplaceError(f"token {a + (key // 8) // m.L - trace.tok_begin}: invalid record ({n} bad)")
+        launch(bufs[j], stride, 0, b - a, d_rel[i])
+        free[j].record(comp)
+    trace._validated = True
+    comp.wait_stream(copy)
+
+
+def C_void(addr: int):
+    import ctypes
+    return ctypes.c_void_p(addr)
+
+
 def trace_counts(trace: ActivationTrace):
     """Exact per-(layer, expert) selection counts as a device int64 [L, E] tensor (``mp_hist_u8``)."""
     t = _lib.torch()
     m = trace.model
-    planes = trace.device_planes()
-    validate_trace(trace)
-    counts = t.zeros((m.L, m.E), dtype=t.int64, device=planes.device)
+    counts = t.zeros((m.L, m.E), dtype=t.int64, device=_lib.require_cuda())
     err = _lib.new_err()
-    _lib.call("mp_hist_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K, m.E,
-              _lib.ptr(counts), _lib.ptr(err), _lib.stream_handle())
+
+    def launch(planes, stride, t0, t1, bounds):
+        _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, m.E, _lib.ptr(counts), _lib.ptr(err),
+                  _lib.stream_handle())
+
+    sweep(trace, launch)
     _lib.check_err(err, "estimate_frequencies")
     return counts
 

@@ -320,3 +320,26 @@ def test_large_trace_properties():
     assert np.array_equal(sh.tokens(), sel)
     got = ev.score_sums(sh, [pl], c1)[0]
     assert np.array_equal(got, oe.chunk_sums(sel, pe, bounds, a))
+
+
+def test_host_streaming_matches_device(monkeypatch):
+    """The end-to-end path (pinned host planes streamed through device slices) gives the same
+    integers as the device-resident path, with slices that cut through chunks."""
+    import moeplace.model_trace as mtm
+    monkeypatch.setattr(mtm, "STREAM_BLOCK_TOKENS", 777)
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("FatTree", 2, 2, 8, m)
+    tr = mt.generate_trace(m, 1.2, 5000, 9, 21)
+    rng = np.random.default_rng(3)
+    pls = [mpl.Placement(random_assign(rng, L, E, g.n_devices)) for _ in range(6)]
+    want = ev.score_sums(tr, pls, cost)
+    f_dev, r_dev = ev.evaluate_with_stats(tr, pls[:4], cost)
+    host = tr.to_host(pin=True)
+    assert not host.planes.is_cuda
+    assert np.array_equal(ev.score_sums(host, pls, cost), want)
+    f_h, r_h = ev.evaluate_with_stats(host, pls[:4], cost)
+    assert np.array_equal(f_h.counts, f_dev.counts)
+    assert [r.chunk_hop_sums for r in r_h] == [r.chunk_hop_sums for r in r_dev]
+    assert np.array_equal(mt.estimate_frequencies(host, m).counts, f_dev.counts)
+    assert not host.planes.is_cuda  # streamed, not cached on the device
