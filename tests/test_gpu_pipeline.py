@@ -1,0 +1,148 @@
+"""End-to-end pipeline on the GPU: run_experiment / CLI (config 1 shape), the SPEC acceptance
+criteria that need the engine (2, 3, 6, 8, 9) and the sharded path at world size 1."""
+import json
+
+import numpy as np
+import pytest
+
+import moeplace.cli as cli
+import moeplace.eval as ev
+import moeplace.model_trace as mt
+import moeplace.placement as mpl
+import moeplace.solver as sv
+from oracle import evaluate as oe
+from oracle import gen as og
+
+from helpers import setup_topology
+
+pytestmark = pytest.mark.gpu
+
+CFG1 = {"model": "16b", "L": 27, "E": 64, "K": 6, "c_exp": 54, "c_layer": 2, "topology": "FatTree",
+        "num_leaf_switches": 2, "num_nodes_per_leaf": 2, "num_gpus_per_server": 8, "spines": 4,
+        "zipf_s": 1.2, "n_tokens": 30000, "n_chunks": 150, "seed": 0, "train_chunks": 100, "test_chunks": 50}
+
+
+def test_run_experiment_config1(tmp_path):
+    cfg = dict(CFG1, output_dir=str(tmp_path / "out"))
+    res = cli.run_experiment(cfg)
+    out = tmp_path / "out"
+    for f in ("topology.json", "distance.csv", "comparison.csv", "placement_rr.csv", "eval_ilpload.json",
+              "solve_ilpload.json"):
+        assert (out / f).exists(), f
+    rows = (out / "comparison.csv").read_text().splitlines()
+    assert rows[0] == "network,placement,hops_mean,hops_std,gain_pct" and len(rows) == 5
+    assert len(list(out.glob("commmap_*.csv"))) == 2
+    r = res["results"]["FatTree"]
+    # acceptance #2: evaluate(train).mean == K * objective_value(f_train) within 1e-6 relative
+    for m, d in r.items():
+        tr, obj = d["train"].mean_hops_per_token, d["test"].objective_train
+        assert abs(tr - 6 * obj) <= 1e-6 * tr, m
+    # acceptance #3: ILPLoad's train objective <= every other method's
+    best = r["ilpload"]["test"].objective_train
+    assert all(best <= d["test"].objective_train + 1e-12 for d in r.values())
+    # acceptance #9: byte-identical comparison CSV on a re-run
+    cfg2 = dict(cfg, output_dir=str(tmp_path / "out2"))
+    cli.run_experiment(cfg2)
+    assert (tmp_path / "out2" / "comparison.csv").read_bytes() == (out / "comparison.csv").read_bytes()
+
+
+def test_run_experiment_matches_oracle_reports(tmp_path):
+    """Every EvalReport of the pipeline equals the oracle's floats computed from its own integers."""
+    cfg = dict(CFG1, output_dir=str(tmp_path / "o"), n_tokens=6000, methods=["rr", "greedy"])
+    res = cli.run_experiment(cfg)
+    sel, bounds = og.generate(27, 64, 6, 1.2, 6000, 150, 0)
+    g, dist, order, attn, cost = setup_topology("FatTree", 2, 2, 8, mt.ModelSpec(27, 64, 6), {"spines": 4})
+    p = cost.numpy()
+    for m in ("rr", "greedy"):
+        asg = mpl.read_placement(tmp_path / "o" / f"placement_{m}.csv", mt.ModelSpec(27, 64, 6)).assign
+        sums = oe.chunk_sums(sel, oe.pe_table(p, asg), bounds)
+        r = oe.report(sums[100:150], np.diff(bounds)[100:150])
+        rep = res["results"]["FatTree"][m]["test"]
+        assert rep.mean_hops_per_token == r["mean"] and rep.std_hops == r["std"]
+
+
+def test_acceptance8_sparse_dragonfly_ordering(tmp_path):
+    """Acceptance #8: Zipf(1.2), >= 20k tokens, 150 chunks, 100/50 split, 256-device Sparse
+    Dragonfly, c_layer=1: test hops ILPLoad <= Greedy <= RR and ILPLoad gains >= 5% over RR."""
+    cfg = {"L": 58, "E": 256, "K": 8, "c_exp": 64, "c_layer": 1, "topology": "DragonflySparse",
+           "num_leaf_switches": 16, "num_nodes_per_leaf": 4, "num_gpus_per_server": 4, "zipf_s": 1.2,
+           "n_tokens": 20000, "n_chunks": 150, "seed": 0, "train_chunks": 100, "test_chunks": 50,
+           "output_dir": str(tmp_path / "a8")}
+    res = cli.run_experiment(cfg)["results"]["DragonflySparse"]
+    h = {m: d["test"].mean_hops_per_token for m, d in res.items()}
+    assert h["ilpload"] <= h["greedy"] <= h["rr"], h
+    assert ev.gain(h["rr"], h["ilpload"]) >= 5.0, h
+
+
+def test_acceptance6_paper_configs_feasible():
+    """Acceptance #6: every placer passes validate on the paper-shaped configs."""
+    for (L, E, K, cexp, cl, spec) in [(58, 256, 8, 64, 1, ("Dragonfly", 16, 4, 4)),
+                                      (58, 256, 8, 64, 8, ("FatTree", 16, 4, 4)),
+                                      (27, 64, 6, 54, 1, ("DragonflySparse", 64, 1, 1))]:
+        m = mt.ModelSpec(L, E, K)
+        g, dist, order, attn, cost = setup_topology(*spec, m)
+        c = mpl.Constraints(cexp, cl)
+        tr = mt.generate_trace(m, 1.2, 3000, 10, 1)
+        pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c),
+               sv.solve_exact(sv.build_instance(cost, sv.UniformFrequencies(E), c))[0],
+               sv.solve_exact(sv.build_instance(cost, mt.estimate_frequencies(tr, m), c))[0]]
+        for pl in pls:
+            assert mpl.validate(pl, c, m, g.n_devices) == []
+
+
+def test_ablation_monotone(tmp_path):
+    cfg = dict(CFG1, output_dir=str(tmp_path / "ab"), n_tokens=6000, methods=["ilpload"], num_gpus_per_server=16)
+    rows = cli.ablate_clayer(cfg, [2, 4, 8])
+    objs = [r[5] for r in rows]
+    assert objs[0] >= objs[1] >= objs[2]
+    assert (tmp_path / "ab" / "ablation.csv").exists()
+
+
+def test_cli_subcommands(tmp_path):
+    base = ["--L", "4", "--E", "16", "--K", "2", "--c-exp", "16", "--c-layer", "1", "--topology", "Dragonfly",
+            "--num-leaf-switches", "4", "--num-nodes-per-leaf", "2", "--num-gpus-per-server", "2",
+            "--n-tokens", "400", "--n-chunks", "10", "--train-chunks", "6", "--test-chunks", "4"]
+    assert cli.main(["topo", "build", *base, "--out", str(tmp_path / "t.json"), "--dist-csv", str(tmp_path / "d.csv")]) == 0
+    assert cli.main(["trace", "gen", *base, "--out", str(tmp_path / "tr.txt")]) == 0
+    assert cli.main(["trace", "stats", "--trace", str(tmp_path / "tr.txt")]) == 0
+    assert cli.main(["place", "greedy", *base, "--out", str(tmp_path / "p.csv")]) == 0
+    assert cli.main(["eval", *base, "--placement", str(tmp_path / "p.csv")]) == 0
+    assert cli.main(["compare", *base, "--output-dir", str(tmp_path / "cmp")]) == 0
+    assert cli.main(["compare", *base, "--c-exp", "1", "--output-dir", str(tmp_path / "x")]) == 3  # infeasible
+    # parse error exit code 4
+    (tmp_path / "bad.txt").write_text("#moeplace-trace v1 L=1 E=2 K=1\n0\tlayer0:5\n")
+    assert cli.main(["trace", "stats", "--trace", str(tmp_path / "bad.txt")]) == 4
+
+
+def test_file_trace_roundtrip_on_device(tmp_path):
+    m = mt.ModelSpec(27, 64, 6)
+    tr = mt.generate_trace(m, 1.2, 500, 7, 3)
+    f = tmp_path / "t.txt"
+    mt.write_trace(tr, f)
+    tr2 = mt.parse_trace(f)
+    assert np.array_equal(tr2.tokens(), tr.tokens())
+    mt.write_trace(tr2, tmp_path / "u.txt")
+    assert (tmp_path / "u.txt").read_bytes() == f.read_bytes()
+    assert np.array_equal(mt.estimate_frequencies(tr2, m).counts, mt.estimate_frequencies(tr, m).counts)
+
+
+def test_sharded_evaluate_world1_matches():
+    from paper_2508_09229_b200.shard import sharded_evaluate
+    m = mt.ModelSpec(58, 256, 8)
+    g, dist, order, attn, cost = setup_topology("FatTree", 8, 4, 8, m)
+    c = mpl.Constraints(64, 1)
+    pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c)]
+    freq, reps = sharded_evaluate(m, 1.2, 50_000, 30, 5, pls, cost)
+    tr = mt.generate_trace(m, 1.2, 50_000, 30, 5)
+    f2, r2 = ev.evaluate_with_stats(tr, pls, cost)
+    assert np.array_equal(freq.counts, f2.counts)
+    assert [r.chunk_hop_sums for r in reps] == [r.chunk_hop_sums for r in r2]
+    # emulated 8-way sharding on one GPU: sum of shard partials == whole
+    from paper_2508_09229_b200.shard import shard_range
+    tot = np.zeros_like(f2.counts)
+    for r in range(8):
+        a, b = shard_range(50_000, r, 8)
+        sh = mt.generate_trace(m, 1.2, 50_000, 30, 5, tok_range=(a, b))
+        if b > a:
+            tot += mt.estimate_frequencies(sh, m).counts
+    assert np.array_equal(tot, f2.counts)
