@@ -97,7 +97,21 @@ struct Stream {
     }
   }
 
-  // all bytes [xa, xb) of one plane
+  __device__ __forceinline__ void widen(uint32_t (&acc16)[2 * (W > 0 ? W : 1)], ScoreAcc<(W > 0 ? W : 1)>& acc) {
+    if constexpr (W > 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        acc.tot[4 * w + 0] += acc16[2 * w] & 0xffffu;
+        acc.tot[4 * w + 2] += acc16[2 * w] >> 16;
+        acc.tot[4 * w + 1] += acc16[2 * w + 1] & 0xffffu;
+        acc.tot[4 * w + 3] += acc16[2 * w + 1] >> 16;
+        acc16[2 * w] = 0;
+        acc16[2 * w + 1] = 0;
+      }
+    }
+  }
+
+  // all bytes [xa, xb) of one plane (xb - xa <= kMaxPiece, so vector offsets fit in 32 bits)
   __device__ __forceinline__ void range(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb,
                                         ScoreAcc<(W > 0 ? W : 1)>& acc) {
     constexpr int WW = W > 0 ? W : 1;
@@ -105,33 +119,25 @@ struct Stream {
     const int64_t tb = max(ha, xb & ~(int64_t)15);
     for (int64_t x = xa + threadIdx.x; x < ha; x += blockDim.x) one(plane[x], acc);
     for (int64_t x = tb + threadIdx.x; x < xb; x += blockDim.x) one(plane[x], acc);
-    const int4* pv = reinterpret_cast<const int4*>(plane);
-    const int64_t v1 = tb >> 4;
+    const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
+    const uint32_t nv = (uint32_t)((tb - ha) >> 4);
+    const uint32_t T = blockDim.x;
     uint32_t acc16[2 * WW];
 #pragma unroll
     for (int i = 0; i < 2 * WW; ++i) acc16[i] = 0;
-    for (int64_t v = (ha >> 4) + threadIdx.x; v < v1; v += (int64_t)blockDim.x * UNROLL) {
+    uint32_t v = threadIdx.x;
+    // main loop: UNROLL vectors in flight per thread, no bounds checks
+    for (; v + (UNROLL - 1) * T < nv; v += UNROLL * T) {
       int4 x[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int64_t j = v + (int64_t)u * blockDim.x;
-        x[u] = j < v1 ? ldg_stream(pv + j) : make_int4(0, 0, 0, 0);
-      }
+      for (int u = 0; u < UNROLL; ++u) x[u] = ldg_stream(pv + v + u * T);
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        if (v + (int64_t)u * blockDim.x < v1) vec(x[u], acc16);
-      }
-      if constexpr (W > 0) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          acc.tot[4 * w + 0] += acc16[2 * w] & 0xffffu;
-          acc.tot[4 * w + 2] += acc16[2 * w] >> 16;
-          acc.tot[4 * w + 1] += acc16[2 * w + 1] & 0xffffu;
-          acc.tot[4 * w + 3] += acc16[2 * w + 1] >> 16;
-          acc16[2 * w] = 0;
-          acc16[2 * w + 1] = 0;
-        }
-      }
+      for (int u = 0; u < UNROLL; ++u) vec(x[u], acc16);
+      widen(acc16, acc);
+    }
+    for (; v < nv; v += T) {  // tail: fewer than UNROLL vectors left for this thread
+      vec(ldg_stream(pv + v), acc16);
+      widen(acc16, acc);
     }
   }
 };

@@ -1,0 +1,75 @@
+"""Times each streaming kernel variant on the config-2 trace (R1, 10M tokens) with CUDA events.
+  python tools/time_kernels.py [--tokens N] [--reps R] [--s zipf]"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import moeplace.eval as ev  # noqa: E402
+import moeplace.model_trace as mt  # noqa: E402
+import moeplace.placement as mpl  # noqa: E402
+import moeplace.topology as topo  # noqa: E402
+from paper_2508_09229_b200 import _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--tokens", type=int, default=10_000_000)
+ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--s", type=float, default=1.2)
+ap.add_argument("--out")
+a = ap.parse_args()
+L, E, K = 58, 256, 8
+m = mt.ModelSpec(L, E, K)
+g = topo.build_topology(topo.TopologySpec("FatTree", 8, 4, 8, {"spines": 4}))
+d = topo.all_pairs_hops(g)
+order = topo.locality_order(g, d)
+attn = mt.default_attention_placement(m, order)
+cost = mpl.cost_matrix(d, attn)
+c = mpl.Constraints(64, 1)
+pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c)] * 8
+tr = mt.generate_trace(m, a.s, a.tokens, 150, 0)
+P, st = tr.planes, tr.planes.shape[1]
+C = tr.n_chunks
+b = _lib.to_dev(tr.chunk_bounds, torch.int64)
+tabs = {W: ev._group_tables(pls[:4 * W], [cost] * 4 * W, m, W) for W in (1, 2, 4)}
+cnt = torch.zeros(L * E, dtype=torch.int64, device="cuda")
+s = torch.zeros(16 * C, dtype=torch.int64, device="cuda")
+err = _lib.new_err()
+sh = _lib.stream_handle()
+
+
+def run(w):
+    if w == "fused":
+        t, mp_ = tabs[1]
+        _lib.call("mp_hist_score_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t), mp_,
+                  _lib.ptr(cnt), _lib.ptr(s), _lib.ptr(err), sh)
+    elif w == "hist":
+        _lib.call("mp_hist_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(cnt), _lib.ptr(err), sh)
+    else:
+        W = int(w[-1])
+        t, mp_ = tabs[W]
+        _lib.call("mp_score_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t), W, mp_,
+                  _lib.ptr(s), sh)
+
+
+res = {}
+bytes_ = a.tokens * L * K
+for w in ("hist", "score1", "score2", "score4", "fused"):
+    for _ in range(3):
+        run(w)
+    ts = []
+    for _ in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run(w)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.mean(ts))
+    res[w] = {"ms": ms, "min_ms": float(min(ts)), "GBps": bytes_ / ms / 1e6, "frac_6548": bytes_ / ms / 1e6 / 6548.2}
+    print(f"{w:8s} {ms:7.3f} ms (min {min(ts):.3f})  {bytes_ / ms / 1e6:8.1f} GB/s  {100 * bytes_ / ms / 1e6 / 6548.2:5.1f}%")
+if a.out:
+    json.dump(res, open(a.out, "w"), indent=1)
