@@ -25,7 +25,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -66,60 +65,48 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clock / throttle-reason sampling during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML polling thread
+    (every ~2 ms), with `nvidia-smi -lms 100` as the fallback when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    # clocks_event_reasons bits (nvml.h): sw_power_cap 0x4, hw_slowdown 0x8, sw_thermal 0x20, hw_thermal 0x40
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.th = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
-            self.th.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            def poll():
+                while not self._stop.is_set():
+                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for n, b in self.BITS.items():
+                        if r & b:
+                            self.reasons.add(n)
+                    time.sleep(0.002)
+
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+        except Exception:
+            self.th = None
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        srt = sorted(sm)
-        loaded = [x for x in srt if x > 0.5 * max(mx)] or srt
-        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self._stop.set()
+        if self.th is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.th.join(timeout=1)
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"], "samples": 0}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "sm_min_mhz": float(min(self.sm)), "source": "nvml"}
 
 
 def cpu_sample(trace, n_sample: int):
@@ -129,20 +116,17 @@ def cpu_sample(trace, n_sample: int):
     return np.ascontiguousarray(v.reshape(L, n_sample, K).transpose(1, 0, 2))
 
 
-def time_oracle(sel, bounds, p, assigns, reps: int = 3):
-    """Seconds per pass of the CPU restatement: counts + per-chunk hop sums of every placement."""
+def time_oracle(sel, bounds, p, assigns, reps: int = 3, t0: int = 0):
+    """Seconds per pass of the CPU restatement: counts + per-chunk hop sums of every placement
+    in one token-block-parallel pass over the trace (oracle.evaluate.fused_pass)."""
     from oracle import evaluate as oe
-    from oracle import stats as ost
     pes = [oe.pe_table(p, a) for a in assigns]
-    ost.counts(sel[:64], E)
-    oe.chunk_sums(sel[:64], pes[0], np.array([0, 64]))  # numba compile outside timing
+    oe.fused_pass(sel[:64], pes, bounds, E, t0)  # numba compile outside timing
     best = float("inf")
     for _ in range(reps):
-        t0 = time.perf_counter()
-        ost.counts(sel, E)
-        for pe in pes:
-            oe.chunk_sums(sel, pe, bounds)
-        best = min(best, time.perf_counter() - t0)
+        t_a = time.perf_counter()
+        oe.fused_pass(sel, pes, bounds, E, t0)
+        best = min(best, time.perf_counter() - t_a)
     return best
 
 

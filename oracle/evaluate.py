@@ -112,3 +112,68 @@ def comm_map(cnt: np.ndarray, assign: np.ndarray, device_server: np.ndarray, dsr
             raw[a, s] += c * int(dsrv[a, s])
             raw[s, b] += c * int(dsrv[s, b])
     return (raw + raw.T) / 2.0 / n_tokens, raw
+
+
+@nb.njit(cache=True, parallel=True)
+def _fused_pass(sel, packed, P, bounds, t0, E, nblk):
+    N, L, K = sel.shape
+    C = bounds.shape[0] - 1
+    G = packed.shape[0]
+    cnt = np.zeros((nblk, L, E), dtype=np.int32)
+    sums = np.zeros((nblk, 4 * G, C), dtype=np.int64)
+    step = (N + nblk - 1) // nblk
+    for b in nb.prange(nblk):
+        lo = b * step
+        hi = min(N, lo + step)
+        if lo >= hi:
+            continue
+        acc = np.zeros(4 * G, dtype=np.int64)
+        c = np.searchsorted(bounds, lo + t0, side="right") - 1
+        for t in range(lo, hi):
+            while bounds[c + 1] <= t + t0:
+                for q in range(4 * G):
+                    sums[b, q, c] += acc[q]
+                    acc[q] = 0
+                c += 1
+            for l in range(L):
+                for k in range(K):
+                    cnt[b, l, sel[t, l, k]] += 1
+                for g in range(G):
+                    w = np.uint64(0)
+                    for k in range(K):
+                        w += packed[g, l, sel[t, l, k]]
+                    acc[4 * g] += np.int64(w & np.uint64(0xFFFF))
+                    acc[4 * g + 1] += np.int64((w >> np.uint64(16)) & np.uint64(0xFFFF))
+                    acc[4 * g + 2] += np.int64((w >> np.uint64(32)) & np.uint64(0xFFFF))
+                    acc[4 * g + 3] += np.int64(w >> np.uint64(48))
+        for q in range(4 * G):
+            sums[b, q, c] += acc[q]
+    out = np.zeros((L, E), dtype=np.int64)
+    for b in range(nblk):
+        out += cnt[b]
+    return out, sums.sum(axis=0)
+
+
+def fused_pass(sel, pes, bounds, E: int, t0: int = 0, blocks: int = 0):
+    """One pass over the trace: counts [L, E] and per-chunk hop sums [P, C] of every placement —
+    the CPU baseline's best form: token blocks in parallel with private partials and an integer
+    merge, and the P placements' per-expert costs packed four 16-bit lanes to a 64-bit word so a
+    pick costs one table gather per 4 placements (per-layer lane sums <= K*255 < 2^16)."""
+    sel = np.ascontiguousarray(sel)
+    pes = [np.asarray(x, dtype=np.int64) for x in pes]
+    P = len(pes)
+    L, Ee = pes[0].shape
+    if K_max_ok(sel.shape[2], max(int(x.max(initial=0)) for x in pes)) is False:
+        raise ValueError("per-layer lane sum would overflow 16 bits")
+    G = (P + 3) // 4
+    packed = np.zeros((G, L, E), dtype=np.uint64)
+    for q, x in enumerate(pes):
+        packed[q // 4, :, :Ee] |= x.astype(np.uint64) << np.uint64(16 * (q % 4))
+    nblk = blocks or nb.get_num_threads()  # one private partial per thread: merge cost O(threads*L*E)
+    cnt, sums = _fused_pass(sel, packed, P, np.asarray(bounds, dtype=np.int64), np.int64(t0), E,
+                            max(1, min(nblk, sel.shape[0])))
+    return cnt, sums[:P]
+
+
+def K_max_ok(K: int, max_p: int) -> bool:
+    return K * max_p < (1 << 16)

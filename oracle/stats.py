@@ -25,14 +25,14 @@ def _counts(sel, E, nblk):
     return part.sum(axis=0)
 
 
-def counts(sel: np.ndarray, E: int, blocks: int = 64) -> np.ndarray:
+def counts(sel: np.ndarray, E: int, blocks: int = 0) -> np.ndarray:
     """int64 [L, E] selection counts of token-major uint8 selections [N, L, K]."""
     sel = np.ascontiguousarray(sel)
     if sel.shape[0] == 0:
         return np.zeros((sel.shape[1], E), dtype=np.int64)
     if sel.max(initial=0) >= E:
         raise ValueError("expert index >= E")
-    return _counts(sel, E, max(1, min(blocks, sel.shape[0])))
+    return _counts(sel, E, max(1, min(blocks or nb.get_num_threads(), sel.shape[0])))
 
 
 def counts_bincount(sel: np.ndarray, E: int) -> np.ndarray:
