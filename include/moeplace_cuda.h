@@ -71,6 +71,19 @@ int mp_gen_trace(uint64_t seed, int64_t tok_begin, int64_t tok_end, int L, int K
 int mp_validate_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
                    int L, int K, int E, int64_t* err, void* stream);
 
+/* ---- text ingestion: parse_trace on the device ----------------------
+ * mp_count_newlines: counts[b] = #'\n' in text[b*65536, (b+1)*65536), b < ceil(n/65536).
+ * mp_find_newlines: positions of every '\n', in order; offsets[b] = exclusive prefix of counts.
+ * mp_parse_trace_text: line t (0-based, after the header) spans [first_start or ends[t-1]+1,
+ *   ends[t]); parses "cid\t[layer]0:e,..,e\t...", writes planes[l][t*K + k] and chunk_ids[t].
+ *   err[0] (caller sets INT64_MAX) = min over bad lines of t*16 + code (1 structure, 2 layer
+ *   label, 3 id >= E, 4 id count, 5 duplicate id, 6 chunk id overflow).  The text buffer must
+ *   be readable (padded) up to the 16-byte boundary after its last byte.  K <= 32.            */
+int mp_count_newlines(const uint8_t* text, int64_t n, int64_t* counts, void* stream);
+int mp_find_newlines(const uint8_t* text, int64_t n, const int64_t* offsets, int64_t* positions, void* stream);
+int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
+                        int E, uint8_t* planes, int64_t plane_stride, int64_t* chunk_ids, int64_t* err, void* stream);
+
 /* ---- load statistics: estimate_frequencies ------------------------
  * counts[l*E + e] += #{(t,k) : t in [tok_begin,tok_end), planes[l][t*K+k] == e}.
  * Ids >= E are not counted; they raise MP_DATA_EXPERT_RANGE in err.                          */
@@ -99,6 +112,22 @@ int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, 
 int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
                      int L, int K, int E, const int64_t* chunk_bounds, int C, const uint32_t* tables,
                      int max_p, int64_t* counts, int64_t* hop_sums, int64_t* err, void* stream);
+
+/* ---- unique-destination scoring (extension A17; not a SPEC metric) ------------------------
+ * For up to 4 placements (W = 1 tables) and per chunk c:
+ *   hop_sums[q*C+c]   += SPEC hops (identical to mp_score_u8)
+ *   uniq_sums[q*C+c]  += sum over (t,l) of |{server_q(e_k)} \ {src_srv[q*L+l]}|
+ *   dedup_sums[q*C+c] += sum over (t,l) of sum over distinct servers s of the picks of pe_q[l][s]
+ * srv_tables: uint32 [L][256], byte q = server id (< 256) hosting expert e under placement q
+ * (built by mp_pack_server_tables); src_srv: device uint8 [4][L], the dispatch server per layer.
+ * K <= 32.                                                                                   */
+int mp_score_dedup_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                      const int64_t* chunk_bounds, int C, const uint32_t* tables, const uint32_t* srv_tables,
+                      const uint8_t* src_srv, int64_t* hop_sums, int64_t* uniq_sums, int64_t* dedup_sums,
+                      void* stream);
+/* srv_tables for mp_score_dedup_u8: server_of: device int32 [T][S] (device -> server per topology). */
+int mp_pack_server_tables(const int32_t* server_of, int T, const int32_t* assign, const int32_t* topo_of, int P,
+                          int L, int E, int S, uint32_t* srv_tables, int64_t* err, void* stream);
 
 /* ---- topology: all_pairs_hops -------------------------------------
  * Unit-weight BFS over the undirected switch/server graph in CSR form (row_ptr[n_nodes+1],

@@ -177,3 +177,49 @@ def fused_pass(sel, pes, bounds, E: int, t0: int = 0, blocks: int = 0):
 
 def K_max_ok(K: int, max_p: int) -> bool:
     return K * max_p < (1 << 16)
+
+
+@nb.njit(cache=True, parallel=True)
+def _dedup_sums(sel, pe, srv_e, src, bounds, t0):
+    C = bounds.shape[0] - 1
+    N, L, K = sel.shape
+    hop = np.zeros(C, dtype=np.int64)
+    uq = np.zeros(C, dtype=np.int64)
+    dd = np.zeros(C, dtype=np.int64)
+    for c in nb.prange(C):
+        lo = max(bounds[c], t0) - t0
+        hi = min(bounds[c + 1], t0 + N) - t0
+        h = 0
+        u = 0
+        d = 0
+        for t in range(lo, hi):
+            for l in range(L):
+                seen = np.empty(K, dtype=np.int64)
+                ns = 0
+                for k in range(K):
+                    e = sel[t, l, k]
+                    s = srv_e[l, e]
+                    h += pe[l, e]
+                    new = True
+                    for j in range(ns):
+                        if seen[j] == s:
+                            new = False
+                    if new:
+                        seen[ns] = s
+                        ns += 1
+                        d += pe[l, e]
+                        if s != src[l]:
+                            u += 1
+        hop[c] = h
+        uq[c] = u
+        dd[c] = d
+    return hop, uq, dd
+
+
+def dedup_sums(sel, pe, srv_e, src, bounds, t0: int = 0):
+    """Extension A17 restated: per chunk (SPEC hops, unique remote destination servers,
+    hops with one message per destination server).  srv_e[l, e] = server hosting expert e,
+    src[l] = dispatch server of layer l."""
+    return _dedup_sums(np.ascontiguousarray(sel), np.ascontiguousarray(pe, dtype=np.int64),
+                       np.ascontiguousarray(srv_e, dtype=np.int64), np.asarray(src, dtype=np.int64),
+                       np.asarray(bounds, dtype=np.int64), np.int64(t0))

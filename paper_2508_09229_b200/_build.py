@@ -18,7 +18,7 @@ LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libmoeplace_cuda.so"
 ROOT = PKG.parent
 
-CU_SOURCES = ["stream.cu", "gen.cu", "topo.cu", "capi.cu"]
+CU_SOURCES = ["stream.cu", "gen.cu", "topo.cu", "dedup.cu", "parse.cu", "capi.cu"]
 CXX_SOURCES = ["solver.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         jobs.append((cmd, obj))
     for src in CXX_SOURCES:
         obj = objdir / (src + ".o")
-        cmd = [nvcc, *common, "-x", "c++", "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc, *common, "-Wno-deprecated-gpu-targets", "-x", "c++", "-c", str(CSRC / src), "-o", str(obj)]
         jobs.append((cmd, obj))
     procs = [(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True), cmd, obj)
              for cmd, obj in jobs]

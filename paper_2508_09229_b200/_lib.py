@@ -24,10 +24,15 @@ SIGNATURES = {
     "mp_status_string": (C.c_char_p, [_i32]),
     "mp_gen_trace": (_i32, [_u64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p, _i64, _p]),
     "mp_validate_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p]),
+    "mp_count_newlines": (_i32, [_p, _i64, _p, _p]),
+    "mp_find_newlines": (_i32, [_p, _i64, _p, _p, _p]),
+    "mp_parse_trace_text": (_i32, [_p, _p, _i64, _i64, _i32, _i32, _i32, _p, _i64, _p, _p, _p]),
     "mp_hist_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p]),
     "mp_pack_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _i32, _p, _p]),
     "mp_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p]),
     "mp_hist_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _i32, _p, _p, _p, _p]),
+    "mp_score_dedup_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p]),
+    "mp_pack_server_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _p, _p]),
     "mp_apsp_bfs": (_i32, [_p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),
     "mp_expand_dist": (_i32, [_p, _i32, _p, _i32, _p, _p]),
     "mp_cost_matrix": (_i32, [_p, _i32, _p, _i32, _p, _p, _i32, _p, _p]),

@@ -22,6 +22,16 @@ cudaError_t launch_coeffs(const int64_t* counts, int64_t denom, const uint8_t* p
 cudaError_t launch_comm(const int64_t* counts, const int32_t* assign, const int32_t* server, const uint8_t* dsrv,
                         int n_srv, const int32_t* disp, const int32_t* coll, int L, int E, int S, int64_t* traffic,
                         int64_t* err, cudaStream_t s);
+cudaError_t launch_dedup(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
+                         const int64_t* bounds, int C, const uint32_t* tables, const uint32_t* srv_tables,
+                         const uint8_t* src_srv, int64_t* hop_sums, int64_t* uniq_sums, int64_t* dedup_sums,
+                         cudaStream_t s);
+cudaError_t launch_pack_srv(const int32_t* server_of, int T, const int32_t* assign, const int32_t* topo_of, int P,
+                            int L, int E, int S, uint32_t* tables, int64_t* err, cudaStream_t s);
+cudaError_t launch_count_nl(const uint8_t* text, int64_t n, int64_t* counts, cudaStream_t s);
+cudaError_t launch_find_nl(const uint8_t* text, int64_t n, const int64_t* offsets, int64_t* pos, cudaStream_t s);
+cudaError_t launch_parse(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
+                         int E, uint8_t* planes, int64_t stride, int64_t* chunk_ids, int64_t* err, cudaStream_t s);
 }  // namespace mp
 
 namespace {
@@ -148,6 +158,49 @@ int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev
     return MP_ERR_ARG;
   return status(mp::launch_comm(counts, assign, dev_server, dsrv, n_srv, dispatch, collect, L, E, S_, traffic, err,
                                 S(stream)));
+}
+
+int mp_score_dedup_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                      const int64_t* chunk_bounds, int C, const uint32_t* tables, const uint32_t* srv_tables,
+                      const uint8_t* src_srv, int64_t* hop_sums, int64_t* uniq_sums, int64_t* dedup_sums,
+                      void* stream) {
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (K > 32) return MP_ERR_UNSUPPORTED;
+  if (!chunk_bounds || C <= 0 || !tables || !srv_tables || !src_srv || !hop_sums || !uniq_sums || !dedup_sums)
+    return MP_ERR_ARG;
+  if (tok_end == tok_begin) return MP_OK;
+  return status(mp::launch_dedup(planes, plane_stride, tok_begin, tok_end, L, K, chunk_bounds, C, tables, srv_tables,
+                                 src_srv, hop_sums, uniq_sums, dedup_sums, S(stream)));
+}
+
+int mp_pack_server_tables(const int32_t* server_of, int T, const int32_t* assign, const int32_t* topo_of, int P, int L,
+                          int E, int S_, uint32_t* srv_tables, int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  if (!server_of || !assign || !topo_of || !srv_tables || T <= 0 || P <= 0 || P > 4 || L <= 0 || E <= 0 || S_ <= 0)
+    return MP_ERR_ARG;
+  return status(mp::launch_pack_srv(server_of, T, assign, topo_of, P, L, E, S_, srv_tables, err, S(stream)));
+}
+
+int mp_count_newlines(const uint8_t* text, int64_t n, int64_t* counts, void* stream) {
+  if (!text || n < 0 || !counts) return MP_ERR_ARG;
+  return status(mp::launch_count_nl(text, n, counts, S(stream)));
+}
+
+int mp_find_newlines(const uint8_t* text, int64_t n, const int64_t* offsets, int64_t* positions, void* stream) {
+  if (!text || n < 0 || !offsets || !positions) return MP_ERR_ARG;
+  return status(mp::launch_find_nl(text, n, offsets, positions, S(stream)));
+}
+
+int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
+                        int E, uint8_t* planes, int64_t plane_stride, int64_t* chunk_ids, int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  if (K > 32) return MP_ERR_UNSUPPORTED;
+  if (!text || !ends || n_lines < 0 || first_start < 0 || !chunk_ids || !err || E <= 0) return MP_ERR_ARG;
+  int r = check_trace(planes, plane_stride, 0, n_lines, L, K);
+  if (r) return r;
+  return status(mp::launch_parse(text, ends, first_start, n_lines, L, K, E, planes, plane_stride, chunk_ids, err,
+                                 S(stream)));
 }
 
 int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t src_stride, int64_t width, int rows,

@@ -1,0 +1,158 @@
+// Unique-destination scoring (extension A17; BASELINE north_star "each token's top-k destinations
+// are deduplicated per server").  Not a SPEC metric: SPEC.md:339 counts every selected expert, and
+// the SPEC hop sums are produced alongside, unchanged.
+//
+// For placement q, token t, layer l with picks e_0..e_{K-1}:
+//   S = { server_q(e_k) }                          (servers hosting the picked experts)
+//   uniq  = |S \ { server(d_l) }|                   (one message per remote destination server)
+//   dedup = sum_{s in S} pe_q[l, s]                 (round-trip hops, one message per server;
+//                                                    pe depends on the device only via its server)
+// One thread per (token, layer) record; K = 8 records are one aligned 8-byte load.  Layer state in
+// shared memory as 256 rows x 256 B: the packed pe word (4 placements) at lane*4 and the packed
+// server-id word at 128 + lane*4, both replicated per lane (conflict-free, one PRMT per address).
+// First occurrence of a server inside a record is detected by comparing against the record's
+// earlier picks (K <= 32), so any server count <= 256 works.
+#include "common.cuh"
+
+namespace mp {
+
+constexpr int kDedupMaxK = 32;
+
+__global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0,
+                                                    int64_t t1, int L, int K, const int64_t* __restrict__ bounds,
+                                                    int C, const uint32_t* __restrict__ tables,
+                                                    const uint32_t* __restrict__ srv_tables,
+                                                    const uint8_t* __restrict__ src_srv, int64_t* __restrict__ hop_sums,
+                                                    int64_t* __restrict__ uniq_sums, int64_t* __restrict__ dedup_sums) {
+  extern __shared__ __align__(128) uint8_t sm[];  // 256 rows x 256 B
+  __shared__ uint32_t s_src;                      // 4 source-server bytes of this layer
+  uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
+  const int lane = threadIdx.x & 31;
+  const uint32_t base = smem_addr(sm);
+  const uint32_t slot = (uint32_t)(lane << 2);
+  const int64_t n = t1 - t0;
+  const int64_t total = n * (int64_t)L;
+  int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  int64_t g = min(total, (int64_t)blockIdx.x * per);
+  const int64_t g1 = min(total, g + per);
+  while (g < g1) {
+    const int l = (int)(g / n);
+    const int64_t r0 = t0 + (g - (int64_t)l * n);
+    const int64_t r1 = min(t0 + n, r0 + (g1 - g));
+    const uint8_t* plane = planes + (int64_t)l * stride;
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int e = i >> 5, j = i & 31;
+      smw[e * 64 + j] = __ldg(tables + (int64_t)l * 256 + e);
+      smw[e * 64 + 32 + j] = __ldg(srv_tables + (int64_t)l * 256 + e);
+    }
+    if (threadIdx.x == 0) {
+      uint32_t w = 0;
+      for (int q = 0; q < 4; ++q) w |= (uint32_t)src_srv[q * L + l] << (8 * q);
+      s_src = w;
+    }
+    __syncthreads();
+    const uint32_t src = s_src;
+    for (int64_t t = r0; t < r1;) {
+      // chunk piece [t, te)
+      int lo = 0, hi = C;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(bounds + mid) <= t) lo = mid; else hi = mid;
+      }
+      const int c = lo;
+      const int64_t te = min(r1, __ldg(bounds + c + 1));
+      uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};
+      for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
+        uint32_t ids[kDedupMaxK];
+        if (K == 8) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(plane + r * 8));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) { ids[k] = (v.x >> (8 * k)) & 0xffu; ids[k + 4] = (v.y >> (8 * k)) & 0xffu; }
+        } else {
+          for (int k = 0; k < K; ++k) ids[k] = plane[r * K + k];
+        }
+        uint32_t srvw[kDedupMaxK];
+        for (int k = 0; k < K; ++k) {
+          const uint32_t a = base + ((ids[k] << 8) | slot);
+          const uint32_t pw = lds32(a);
+          const uint32_t sw = lds32(a + 128);
+          srvw[k] = sw;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t s = (sw >> (8 * q)) & 0xffu;
+            const uint32_t p = (pw >> (8 * q)) & 0xffu;
+            hop[q] += p;
+            bool first = true;
+            for (int j = 0; j < k; ++j) first &= ((srvw[j] >> (8 * q)) & 0xffu) != s;
+            if (first) {
+              dd[q] += p;
+              uq[q] += (s != ((src >> (8 * q)) & 0xffu)) ? 1u : 0u;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned long long h = warp_sum_u64(hop[q]), u = warp_sum_u64(uq[q]), d = warp_sum_u64(dd[q]);
+        if (lane == 0) {
+          if (h) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)h);
+          if (u) atomic_add_i64(uniq_sums + (int64_t)q * C + c, (int64_t)u);
+          if (d) atomic_add_i64(dedup_sums + (int64_t)q * C + c, (int64_t)d);
+        }
+      }
+      t = te;
+    }
+    g += r1 - r0;
+  }
+}
+
+cudaError_t launch_dedup(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
+                         const int64_t* bounds, int C, const uint32_t* tables, const uint32_t* srv_tables,
+                         const uint8_t* src_srv, int64_t* hop_sums, int64_t* uniq_sums, int64_t* dedup_sums,
+                         cudaStream_t s) {
+  const int smem = 256 * 256;
+  cudaError_t e = cudaFuncSetAttribute(dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dedup_kernel, 256, smem);
+  const int64_t records = (t1 - t0) * (int64_t)L;
+  int64_t grid = (int64_t)nsm * max(1, per_sm);
+  grid = max((int64_t)1, min(grid, (records + 4095) / 4096));
+  dedup_kernel<<<(unsigned)grid, 256, smem, s>>>(planes, stride, t0, t1, L, K, bounds, C, tables, srv_tables, src_srv,
+                                                 hop_sums, uniq_sums, dedup_sums);
+  return cudaGetLastError();
+}
+
+// server-id tables: byte j of tables[(l*256 + e)] = server_of[topo_of[q]][assign[q][l][e]] for q = j
+__global__ void pack_srv_kernel(const int32_t* __restrict__ server_of, int T, const int32_t* __restrict__ assign,
+                                const int32_t* __restrict__ topo_of, int P, int L, int E, int S,
+                                uint32_t* __restrict__ tables, int64_t* err) {
+  const int64_t n = (int64_t)L * 256;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i % 256), l = (int)(i / 256);
+    uint32_t w = 0;
+    if (e < E) {
+      for (int q = 0; q < P; ++q) {
+        const int32_t s = assign[((int64_t)q * L + l) * E + e];
+        const int32_t tp = topo_of[q];
+        if (s < 0 || s >= S || tp < 0 || tp >= T) { report_err(err, MP_DATA_UNPLACED, l, e); continue; }
+        const int32_t sv = server_of[(int64_t)tp * S + s];
+        if (sv < 0 || sv > 255) { report_err(err, MP_DATA_UNPLACED, l, e); continue; }
+        w |= (uint32_t)sv << (8 * q);
+      }
+    }
+    tables[i] = w;
+  }
+}
+
+cudaError_t launch_pack_srv(const int32_t* server_of, int T, const int32_t* assign, const int32_t* topo_of, int P,
+                            int L, int E, int S, uint32_t* tables, int64_t* err, cudaStream_t s) {
+  const int64_t n = (int64_t)L * 256;
+  pack_srv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(server_of, T, assign, topo_of, P, L, E, S, tables, err);
+  return cudaGetLastError();
+}
+
+}  // namespace mp

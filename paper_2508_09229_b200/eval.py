@@ -199,6 +199,80 @@ def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement],
     return freq, [report_from_sums(s[i], tokens, placements[i].label) for i in range(len(placements))]
 
 
+@dataclass
+class DedupReport:
+    """Extension A17 (north_star): per-token unique destination servers and deduplicated hops
+    (one message per destination server).  ``spec`` is the unchanged SPEC EvalReport — the
+    deduplicated numbers never replace it (SPEC.md:339 counts every selected expert)."""
+
+    spec: EvalReport
+    unique_dest_per_token: float
+    dedup_hops_per_token: float
+    label: str = ""
+    chunk_uniq_sums: Optional[list] = None
+    chunk_dedup_sums: Optional[list] = None
+
+
+def evaluate_dedup(trace: ActivationTrace, placements: Sequence[Placement], costs) -> list[DedupReport]:
+    """SPEC hops plus unique-destination counts per (token, layer) for each placement, in one
+    pass per group of 4 placements (``mp_score_dedup_u8``).  Each cost matrix must carry its
+    DistanceMatrix and AttentionPlacement (the server map and the dispatch servers)."""
+    t = _lib.torch()
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("evaluate_dedup: empty trace")
+    placements = list(placements)
+    costs = _as_costs(costs, len(placements))
+    dev = _lib.require_cuda()
+    C = trace.n_chunks
+    tokens = trace.chunk_token_counts()
+    out = []
+    for g0 in range(0, len(placements), 4):
+        grp, gcost = placements[g0:g0 + 4], costs[g0:g0 + 4]
+        for c in gcost:
+            if c.dist is None or c.attn is None:
+                raise ConfigError("evaluate_dedup needs cost matrices built by cost_matrix(dist, attn)")
+        tables, max_p = _group_tables(grp, gcost, m, 1)
+        uniq: list = []
+        topo_of = []
+        for c in gcost:
+            for i, u in enumerate(uniq):
+                if u is c:
+                    topo_of.append(i)
+                    break
+            else:
+                uniq.append(c)
+                topo_of.append(len(uniq) - 1)
+        S = uniq[0].S
+        server_of = _lib.to_dev(np.stack([c.dist.graph.device_server for c in uniq]).astype(np.int32), t.int32)
+        d_assign = _lib.to_dev(np.stack([p.assign for p in grp]), t.int32)
+        d_topo = _lib.to_dev(np.asarray(topo_of, dtype=np.int32), t.int32)
+        srv_tables = t.empty((m.L, 256), dtype=t.int32, device=dev)
+        err = _lib.new_err()
+        _lib.call("mp_pack_server_tables", _lib.ptr(server_of), len(uniq), _lib.ptr(d_assign), _lib.ptr(d_topo),
+                  len(grp), m.L, m.E, S, _lib.ptr(srv_tables), _lib.ptr(err), _lib.stream_handle())
+        _lib.check_err(err, "evaluate_dedup: unplaced expert")
+        src = np.zeros((4, m.L), dtype=np.uint8)
+        for q, c in enumerate(gcost):
+            src[q] = c.dist.graph.device_server[c.attn.dispatch]
+        d_src = _lib.to_dev(src, t.uint8)
+        hop = t.zeros((4, C), dtype=t.int64, device=dev)
+        uq = t.zeros((4, C), dtype=t.int64, device=dev)
+        dd = t.zeros((4, C), dtype=t.int64, device=dev)
+
+        def launch(planes, stride, t0, t1, bounds):
+            _lib.call("mp_score_dedup_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), _lib.ptr(srv_tables), _lib.ptr(d_src), _lib.ptr(hop), _lib.ptr(uq),
+                      _lib.ptr(dd), _lib.stream_handle())
+
+        sweep(trace, launch)
+        h, u, d = hop.cpu().numpy(), uq.cpu().numpy(), dd.cpu().numpy()
+        for i, pl in enumerate(grp):
+            out.append(DedupReport(report_from_sums(h[i], tokens, pl.label), int(u[i].sum()) / trace.n_tokens,
+                                   int(d[i].sum()) / trace.n_tokens, pl.label, u[i].tolist(), d[i].tolist()))
+    return out
+
+
 def token_hops(selections, placement: Placement, cost: CostMatrix) -> int:
     """sum over layers and selected experts of p[l, device(l, e)] for ONE token
     (``selections`` = L lists of selected experts).  Runs through the device scorer."""

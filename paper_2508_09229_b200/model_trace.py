@@ -291,8 +291,87 @@ _HEADER = re.compile(r"^#moeplace-trace v1 L=(\d+) E=(\d+) K=(\d+)\s*$")
 _FIELD = re.compile(r"^(?:layer)?(\d+):(.*)$")
 
 
-def parse_trace(path) -> ActivationTrace:
-    """Parse the text trace format; errors carry the 1-based line number (header = line 1)."""
+_PARSE_ERR = {1: "malformed line (expected chunk_id<TAB>layer<l>:e,...,e fields)", 2: "layer fields out of order",
+              3: "expert index outside [0, E)", 4: "wrong number of experts in a layer field",
+              5: "repeated expert index", 6: "chunk id too large"}
+
+
+def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
+    """SPEC.md:132-139.  Parse the text trace format; errors raise ``TraceParseError`` with the
+    1-based line number (header = line 1).  ``engine="cuda"`` (default) parses on the GPU
+    (``mp_count_newlines``/``mp_find_newlines``/``mp_parse_trace_text``) straight into the
+    device planes; ``engine="host"`` is the host parser for CPU-only tooling."""
+    if engine == "host":
+        return _parse_trace_host(path)
+    if engine != "cuda":
+        raise ConfigError(f"unknown parse engine {engine!r}")
+    t = _lib.torch()
+    dev = _lib.require_cuda()
+    raw = np.fromfile(path, dtype=np.uint8)
+    n = int(raw.size)
+    if n == 0:
+        return ActivationTrace(None, t.zeros((0, 16), dtype=t.uint8), 0, 0, np.zeros(0, np.int64),
+                               np.zeros(1, np.int64), source_is_file=True)
+    head_end = raw[:4096].tobytes().find(b"\n")
+    header = raw[:head_end if head_end >= 0 else min(n, 4096)].tobytes().decode("utf-8", "replace")
+    m = _HEADER.match(header.rstrip("\r"))
+    if not m:
+        raise TraceParseError("missing or malformed header '#moeplace-trace v1 L=<L> E=<E> K=<K>'", 1)
+    try:
+        model = ModelSpec(int(m.group(1)), int(m.group(2)), int(m.group(3)))
+    except ConfigError as e:
+        raise TraceParseError(str(e), 1) from None
+    if model.E > MAX_EXPERTS or model.K > 32:
+        raise ConfigError(f"E = {model.E} / K = {model.K} outside the device format (E <= 256, K <= 32)")
+    if head_end < 0:
+        head_end = n
+    L, K = model.L, model.K
+    pad = (n + 32 + 15) // 16 * 16
+    host = t.empty(pad, dtype=t.uint8, pin_memory=True)
+    host[:n].copy_(t.from_numpy(raw))
+    host[n:].fill_(0)
+    text = host.to(dev, non_blocking=True)
+    nb = (n + 65535) // 65536
+    counts = t.empty(nb, dtype=t.int64, device=dev)
+    sh = _lib.stream_handle()
+    _lib.call("mp_count_newlines", _lib.ptr(text), n, _lib.ptr(counts), sh)
+    offsets = t.cumsum(counts, 0) - counts
+    total = int(counts.sum().item())
+    pos = t.empty(max(total, 1), dtype=t.int64, device=dev)
+    _lib.call("mp_find_newlines", _lib.ptr(text), n, _lib.ptr(offsets), _lib.ptr(pos), sh)
+    pos = pos[:total]
+    ends = pos[1:] if total and int(pos[0].item()) == head_end else pos
+    if n > head_end + 1 and raw[-1] != 10:  # last line without a trailing newline
+        ends = t.cat([ends, t.tensor([n], dtype=t.int64, device=dev)])
+    ends = ends.contiguous()
+    N = int(ends.numel())
+    planes = t.empty((L, _plane_stride(N, K)), dtype=t.uint8, device=dev)
+    cids = t.empty(max(N, 1), dtype=t.int64, device=dev)
+    err = t.full((1,), 2 ** 63 - 1, dtype=t.int64, device=dev)
+    _lib.call("mp_parse_trace_text", _lib.ptr(text), _lib.ptr(ends), head_end + 1, N, L, K, model.E, _lib.ptr(planes),
+              planes.shape[1], _lib.ptr(cids), _lib.ptr(err), sh)
+    e = int(err.item())
+    if e != 2 ** 63 - 1:
+        line, code = e // 16, e % 16
+        raise TraceParseError(_PARSE_ERR.get(code, f"parse error {code}"), int(line) + 2)
+    del text, host
+    cids = cids[:N]
+    if N and not bool((cids[1:] >= cids[:-1]).all().item()):
+        order = t.sort(cids, stable=True).indices  # regroup by chunk id (SPEC.md:382)
+        cids = cids[order]
+        planes3 = planes[:, :N * K].view(L, N, K)
+        planes[:, :N * K].copy_(planes3[:, order].reshape(L, N * K))
+    if N:
+        ids, cnt = t.unique_consecutive(cids, return_counts=True)
+        ids, cnt = ids.cpu().numpy(), cnt.cpu().numpy()
+    else:
+        ids, cnt = np.zeros(0, np.int64), np.zeros(0, np.int64)
+    bounds = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+    return ActivationTrace(model, planes, 0, N, ids.astype(np.int64), bounds, source_is_file=True, _validated=True)
+
+
+def _parse_trace_host(path) -> ActivationTrace:
+    """Host text parser (engine="host"): for CPU-only tooling and as the error-message reference."""
     with open(path, "r") as f:
         text = f.read()
     lines = text.split("\n")

@@ -343,3 +343,87 @@ def test_host_streaming_matches_device(monkeypatch):
     assert [r.chunk_hop_sums for r in r_h] == [r.chunk_hop_sums for r in r_dev]
     assert np.array_equal(mt.estimate_frequencies(host, m).counts, f_dev.counts)
     assert not host.planes.is_cuda  # streamed, not cached on the device
+
+
+@pytest.mark.parametrize("shape,kind", [(R1, "FatTree"), (B16, "Dragonfly"), ((3, 16, 5), "DragonflySparse")])
+def test_dedup_matches_oracle(shape, kind):
+    """Extension A17: unique destination servers and deduplicated hops, bit-exact vs the oracle;
+    the SPEC hop sums produced alongside equal mp_score_u8's."""
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology(kind, 4, 2, 4, m)
+    _, p = oracle_cost(g, attn)
+    tr = mt.generate_trace(m, 1.2, 2345, 9, 6)
+    sel, bounds = og.generate(L, E, K, 1.2, 2345, 9, 6)
+    rng = np.random.default_rng(2)
+    pls = [mpl.Placement(random_assign(rng, L, E, g.n_devices)) for _ in range(6)]
+    reps = ev.evaluate_dedup(tr, pls, cost)
+    spec = ev.score_sums(tr, pls, cost)
+    src = g.device_server[attn.dispatch]
+    for i, (pl, rep) in enumerate(zip(pls, reps)):
+        pe = oe.pe_table(p, pl.assign)
+        h, u, d = oe.dedup_sums(sel, pe, g.device_server[pl.assign], src, bounds)
+        assert rep.spec.chunk_hop_sums == h.tolist() == spec[i].tolist()
+        assert rep.chunk_uniq_sums == u.tolist()
+        assert rep.chunk_dedup_sums == d.tolist()
+        assert (d <= h).all()
+
+
+def _write_lines(path, lines, trailing="\n"):
+    path.write_text("\n".join(lines) + trailing)
+
+
+@pytest.mark.parametrize("lines,line_no", [
+    (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,3", "0\tlayer0:0,4\tlayer1:2,3"], 3),
+    (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1"], 2),
+    (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,2"], 2),
+    (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,3", "1\tlayer1:0,1\tlayer0:2,3"], 3),
+    (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1,2\tlayer1:2,3"], 2),
+    (["#moeplace-trace v1 L=2 E=4 K=2", "x\tlayer0:0,1\tlayer1:2,3"], 2),
+    (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,3", ""], 3),
+    (["garbage"], 1),
+])
+def test_device_parser_errors_match_host(tmp_path, lines, line_no):
+    f = tmp_path / "t.txt"
+    _write_lines(f, lines)
+    for engine in ("host", "cuda"):
+        with pytest.raises(TraceParseError) as e:
+            mt.parse_trace(f, engine=engine)
+        assert e.value.line_no == line_no, engine
+
+
+def test_device_parser_roundtrip_and_regroup(tmp_path):
+    m = mt.ModelSpec(27, 64, 6)
+    tr = mt.generate_trace(m, 1.2, 3001, 17, 5)
+    f = tmp_path / "t.txt"
+    mt.write_trace(tr, f)
+    d = mt.parse_trace(f)  # device engine
+    h = mt.parse_trace(f, engine="host")
+    assert d.planes.is_cuda
+    assert np.array_equal(d.tokens(), tr.tokens()) and np.array_equal(h.tokens(), tr.tokens())
+    assert np.array_equal(d.chunk_bounds, tr.chunk_bounds) and np.array_equal(d.chunk_ids, tr.chunk_ids)
+    g = tmp_path / "u.txt"
+    mt.write_trace(d, g)
+    assert g.read_bytes() == f.read_bytes()
+    # prefix-less fields, CRLF, no trailing newline, interleaved chunk ids -> stable regroup
+    lines = ["#moeplace-trace v1 L=2 E=5 K=2", "7\t0:0,1\t1:2,3\r", "3\tlayer0:4,1\tlayer1:0,3", "7\tlayer0:2,1\t1:2,4"]
+    _write_lines(tmp_path / "v.txt", lines, trailing="")
+    a = mt.parse_trace(tmp_path / "v.txt")
+    b = mt.parse_trace(tmp_path / "v.txt", engine="host")
+    assert np.array_equal(a.tokens(), b.tokens())
+    assert a.chunk_ids.tolist() == [3, 7] and a.chunk_bounds.tolist() == [0, 1, 3]
+    assert a.tokens()[:, 0, :].tolist() == [[4, 1], [0, 1], [2, 1]]
+
+
+def test_device_parser_R1_scale(tmp_path):
+    """A 20k-token R1 file through the device parser equals the generator's planes, and the
+    stats/score computed from it equal the oracle's."""
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 20000, 30, 9)
+    f = tmp_path / "r1.txt"
+    mt.write_trace(tr, f)
+    d = mt.parse_trace(f)
+    assert np.array_equal(d.tokens(), tr.tokens())
+    sel, _ = og.generate(L, E, K, 1.2, 20000, 30, 9)
+    assert np.array_equal(mt.estimate_frequencies(d, m).counts, ost.counts(sel, E))

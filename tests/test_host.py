@@ -332,21 +332,21 @@ def test_parse_trace_errors(tmp_path):
     f = tmp_path / "t.txt"
     _write(f, ["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,3", "0\tlayer0:0,4\tlayer1:2,3"])
     with pytest.raises(TraceParseError) as e:
-        mt.parse_trace(f)  # expert index E -> error at that line
+        mt.parse_trace(f, engine="host")  # expert index E -> error at that line
     assert e.value.line_no == 3
     _write(f, ["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1"])
     with pytest.raises(TraceParseError) as e:
-        mt.parse_trace(f)
+        mt.parse_trace(f, engine="host")
     assert e.value.line_no == 2
     _write(f, ["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,2"])
     with pytest.raises(TraceParseError):
-        mt.parse_trace(f)
+        mt.parse_trace(f, engine="host")
     _write(f, ["garbage"])
     with pytest.raises(TraceParseError) as e:
-        mt.parse_trace(f)
+        mt.parse_trace(f, engine="host")
     assert e.value.line_no == 1
     f.write_text("")
-    assert mt.parse_trace(f).n_tokens == 0
+    assert mt.parse_trace(f, engine="host").n_tokens == 0
 
 
 def test_parse_write_roundtrip_host(tmp_path):
@@ -354,14 +354,14 @@ def test_parse_write_roundtrip_host(tmp_path):
     lines = ["#moeplace-trace v1 L=2 E=5 K=2", "0\tlayer0:0,1\tlayer1:2,3", "0\tlayer0:4,1\tlayer1:0,3",
              "3\tlayer0:2,1\tlayer1:2,4"]
     _write(f, lines)
-    tr = mt.parse_trace(f)
+    tr = mt.parse_trace(f, engine="host")
     assert tr.n_tokens == 3 and tr.chunk_ids.tolist() == [0, 3] and tr.chunk_bounds.tolist() == [0, 2, 3]
     g = tmp_path / "u.txt"
     mt.write_trace(tr, g)
     assert g.read_text() == f.read_text()
     # prefix-less fields are accepted
     _write(f, ["#moeplace-trace v1 L=1 E=3 K=1", "1\t0:2"])
-    assert mt.parse_trace(f).tokens().tolist() == [[[2]]]
+    assert mt.parse_trace(f, engine="host").tokens().tolist() == [[[2]]]
 
 
 def test_split_trace_host():
