@@ -177,16 +177,24 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", type=int, choices=[2, 3, 4, 5], default=2,
+                    help="BASELINE config: 2 (default, the metric's config), 3 multi-topology, 4 4096 candidates, "
+                         "5 100M tokens strong scaling")
     ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
-    ap.add_argument("--tokens", type=int, default=TOK_PER_GPU, help="tokens per GPU")
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (configs 2-4) / total (config 5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-tokens", type=int, default=1_000_000, help="cpu_baseline sample (tokens)")
+    ap.add_argument("--cpu-tokens", type=int, default=None, help="cpu_baseline sample (tokens)")
     ap.add_argument("--ref-tokens", type=int, default=1_000_000, help="--impl reference sample per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -214,191 +222,285 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    # ---------------- setup (untimed) ----------------
-    n = args.tokens
+    wl = args.workload
     model = mt.ModelSpec(L, E, K)
     c = mpl.Constraints(64, 1)
-    g = topo.build_topology(topo.TopologySpec("FatTree", 8, 4, 8, {"spines": 4}))
-    dmat = topo.all_pairs_hops(g)
-    order = topo.locality_order(g, dmat)
-    attn = mt.default_attention_placement(model, order)
-    cost = mpl.cost_matrix(dmat, attn)
-    n_total, c_total = n * world, CHUNKS_PER_GPU * world
-    trace = mt.generate_trace(model, ZIPF_S, n_total, c_total, SEED, tok_range=(rank * n, (rank + 1) * n))
+
+    def topology(kind, leaves, spl, gps, extra=None):
+        g = topo.build_topology(topo.TopologySpec(kind, leaves, spl, gps, extra or {}))
+        d = topo.all_pairs_hops(g)
+        order = topo.locality_order(g, d)
+        attn = mt.default_attention_placement(model, order)
+        return g, d, order, attn, mpl.cost_matrix(d, attn)
+
+    def methods(freq, g, order, attn, cost, which=("rr", "greedy", "ilp", "ilpload")):
+        out = []
+        for m in which:
+            if m == "rr":
+                pl = mpl.place_round_robin(model, attn, order, c)
+            elif m == "greedy":
+                pl = mpl.place_greedy(model, attn, cost, c)
+            elif m == "ilp":
+                pl = sv.solve_exact(sv.build_instance(cost, sv.UniformFrequencies(E), c))[0]
+            else:
+                pl = sv.solve_exact(sv.build_instance(cost, freq, c))[0]
+            pl.label = f"{g.spec.kind}/{m}"
+            out.append(pl)
+        return out
+
+    # ---------------- setup (untimed): trace shard, statistics, placements, tables ----------------
+    if wl == 5:
+        n_total = args.tokens or 100_000_000
+        c_total = 1500
+        a_tok, b_tok = (rank * n_total) // world, ((rank + 1) * n_total) // world
+        scaling = "strong"
+    else:
+        per = args.tokens or (1_000_000 if wl == 4 else TOK_PER_GPU)
+        n_total, c_total = per * world, CHUNKS_PER_GPU * world
+        a_tok, b_tok = rank * per, (rank + 1) * per
+        scaling = "weak"
+    n = b_tok - a_tok
+    trace = mt.generate_trace(model, ZIPF_S, n_total, c_total, SEED, tok_range=(a_tok, b_tok))
     counts0 = mt.trace_counts(trace)
     if world > 1:
         dist.all_reduce(counts0)
     freq = mt.frequencies_from_counts(counts0.cpu().numpy(), n_total, K)
-    rr = mpl.place_round_robin(model, attn, order, c)
-    gr = mpl.place_greedy(model, attn, cost, c)
-    ilp, _ = sv.solve_exact(sv.build_instance(cost, sv.UniformFrequencies(E), c))
-    ilpl, _ = sv.solve_exact(sv.build_instance(cost, freq, c))
-    placements = [rr, gr, ilp, ilpl]
-    for lbl, pl in zip(("rr", "greedy", "ilp", "ilpload"), placements):
-        pl.label = lbl
-    tables, max_p = ev._group_tables(placements, [cost] * P, model, 1)
+    if wl in (2, 5):
+        g, d, order, attn, cost = topology("FatTree", 8, 4, 8, {"spines": 4})
+        placements = methods(freq, g, order, attn, cost)
+        costs = [cost] * len(placements)
+        kinds = ["FatTree 8x4x8"]
+    elif wl == 3:
+        placements, costs, kinds = [], [], []
+        for kind in ("FatTree", "FatTreeHier", "Dragonfly", "DragonflySparse"):
+            g, d, order, attn, cost = topology(kind, 16, 4, 4)
+            pls = methods(freq, g, order, attn, cost)
+            placements += pls
+            costs += [cost] * len(pls)
+            kinds.append(f"{kind} 16x4x4")
+    else:
+        g, d, order, attn, cost = topology("Dragonfly", 16, 4, 4)
+        base = methods(freq, g, order, attn, cost, which=("ilpload",))[0]
+        cand = mpl.perturb_swaps(base, 4096, 64, 1000)
+        placements = [mpl.Placement(cand[i], c, f"cand{i}") for i in range(cand.shape[0])]
+        costs = [cost] * len(placements)
+        kinds = ["Dragonfly 16x4x4"]
+    P_ = len(placements)
     C = trace.n_chunks
-    buf = torch.zeros(L * E + P * C, dtype=torch.int64, device=dev)  # packed [counts | sums]
-    counts, sums = buf[:L * E], buf[L * E:]
+    planes, stride = trace.planes, trace.planes.shape[1]
+    t0, t1 = trace.tok_begin, trace.tok_end
     bounds = _lib.to_dev(trace.chunk_bounds, torch.int64)
     err = _lib.new_err()
-    planes = trace.planes
-    stride = planes.shape[1]
-    t0, t1 = trace.tok_begin, trace.tok_end
     stream = torch.cuda.current_stream()
     sh = _lib.stream_handle()
-    k_start, k_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k2_start, k2_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kernel_ms, kernel2_ms = [], []
-    sums1 = torch.zeros(4 * C, dtype=torch.int64, device=dev)
+    fused = wl in (2, 5) and args.mode == "fused"
+    groups = []  # (W, tables, max_p, n placements)
+    if wl in (2, 5):
+        tables, max_p = ev._group_tables(placements, costs, model, 1)
+        groups.append((1, tables, max_p, P_))
+    else:
+        for g0 in range(0, P_, 16):
+            grp = placements[g0:g0 + 16]
+            W = ev._lanes_for(len(grp))
+            tables, max_p = ev._group_tables(grp, costs[g0:g0 + 16], model, W)
+            groups.append((W, tables, max_p, len(grp)))
+    n_sums = sum(4 * W for W, _, _, _ in groups)
+    with_hist = wl in (2, 5)
+    buf = torch.zeros((L * E if with_hist else 0) + n_sums * C, dtype=torch.int64, device=dev)
+    counts = buf[:L * E] if with_hist else None
+    sums_all = buf[L * E:] if with_hist else buf
+    views, off = [], 0
+    for W, _, _, _ in groups:
+        views.append(sums_all[off:off + 4 * W * C])
+        off += 4 * W * C
+    kev = [_events() for _ in range(2)]
+    kernel_ms = [[], []]
 
     def step(timed: bool):
         buf.zero_()
-        if args.mode == "fused":
+        if with_hist and fused:
             if timed:
-                k_start.record(stream)
+                kev[0][0].record(stream)
+            W, tables, max_p, _ = groups[0]
             _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
-                      _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err), sh)
+                      _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(views[0]), _lib.ptr(err), sh)
             if timed:
-                k_end.record(stream)
+                kev[0][1].record(stream)
         else:
+            if with_hist:
+                if timed:
+                    kev[1][0].record(stream)
+                _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(counts), _lib.ptr(err), sh)
+                if timed:
+                    kev[1][1].record(stream)
             if timed:
-                k_start.record(stream)
-            _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(counts), _lib.ptr(err), sh)
+                kev[0][0].record(stream)
+            for (W, tables, max_p, _), v in zip(groups, views):
+                _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C, _lib.ptr(tables),
+                          W, max_p, _lib.ptr(v), sh)
             if timed:
-                k_end.record(stream)
-                k2_start.record(stream)
-            _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C, _lib.ptr(tables),
-                      1, max_p, _lib.ptr(sums), sh)
-            if timed:
-                k2_end.record(stream)
+                kev[0][1].record(stream)
         if world > 1:
             dist.all_reduce(buf)
 
-    launches_per_step = 1 if args.mode == "fused" else 2
+    launches_per_step = (1 if fused else len(groups) + (1 if with_hist else 0))
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
-    # correctness gate before timing: integers of this pass == setup histogram
-    if not torch.equal(counts.view(L, E), counts0):
-        raise SystemExit("bench: fused histogram differs from the setup histogram")
+    if with_hist and not torch.equal(counts.view(L, E), counts0):
+        raise SystemExit("bench: histogram of the timed pass differs from the setup histogram")
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a, ev_b = _events()
     ev_a.record(stream)
     for _ in range(args.steps):
-        step(True)
+        step(False)
     ev_b.record(stream)
     torch.cuda.synchronize()
-    # per-kernel times: re-run with per-launch events (kernel share), same stream
-    for _ in range(args.steps):
+    for _ in range(args.steps):  # per-kernel shares with launch-bracketing events on the same stream
         step(True)
-        k_end.synchronize()
-        kernel_ms.append(k_start.elapsed_time(k_end))
-        if args.mode == "separate":
-            k2_end.synchronize()
-            kernel2_ms.append(k2_start.elapsed_time(k2_end))
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        kernel_ms[0].append(kev[0][0].elapsed_time(kev[0][1]))
+        if with_hist and not fused:
+            kernel_ms[1].append(kev[1][0].elapsed_time(kev[1][1]))
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
-    total_ms = ev_a.elapsed_time(ev_b)
-    t_step = torch.tensor([total_ms / args.steps], dtype=torch.float64, device=dev)
+    t_step = torch.tensor([ev_a.elapsed_time(ev_b) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
     ms = float(t_step.item())
-    value = n_total * L * P / (ms / 1e3)
+    value = n_total * L * P_ / (ms / 1e3)
 
-    # roofline of the dominant kernel (algorithmic bytes: one u8 id per (token, layer, pick))
+    # ---------------- roofline of the dominant kernel ----------------
     peak, peak_src = measured_peak()
-    kms = float(np.mean(kernel_ms))
-    kname = "mp_hist_score_u8 (fused hist+score, W=1)" if args.mode == "fused" else "mp_hist_u8"
-    if args.mode == "separate" and np.mean(kernel2_ms) > kms:
-        kms, kname = float(np.mean(kernel2_ms)), "mp_score_u8 (W=1)"
-    alg_bytes = n * L * K
-    achieved = alg_bytes / (kms / 1e3) / 1e9
+    k_main = float(np.mean(kernel_ms[0]))
+    if fused:
+        kname, tkey, launches = "mp_hist_score_u8 (fused hist+score, W=1)", "fused", 1
+    else:
+        Ws = sorted({W for W, _, _, _ in groups})
+        kname = f"mp_score_u8 (W={'/'.join(map(str, Ws))}, {len(groups)} launch(es) per step)"
+        tkey, launches = ("score" if Ws == [1] else f"score_w{Ws[-1]}"), len(groups)
+        if with_hist and np.mean(kernel_ms[1]) > k_main:
+            k_main, kname, tkey, launches = float(np.mean(kernel_ms[1])), "mp_hist_u8", "hist", 1
+    alg_bytes = n * L * K  # one u8 id per (token, layer, pick), per launch
+    per_launch_ms = k_main / launches
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
     traffic = None
-    tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():
-        try:
-            tr = json.loads(tfile.read_text())
-            key = "fused" if args.mode == "fused" else ("score" if "score" in kname else "hist")
-            if tr.get(key, {}).get("tokens") == n:
-                traffic = tr[key]["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        ent = tr.get(tkey, {})
+        if ent.get("tokens"):
+            traffic = ent["dram_bytes_per_launch"] * n / ent["tokens"]  # scaled to this launch's tokens
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": kname, "kernel_ms": kms, "alg_bytes_per_launch": alg_bytes,
+                "traffic": traffic, "kernel": kname, "kernel_ms_per_launch": per_launch_ms,
+                "kernel_share_of_step": k_main / ms if world == 1 else None, "alg_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src}
-    if args.mode == "separate":
-        roofline["other_kernel_ms"] = float(np.mean(kernel2_ms)) if "hist" in kname else float(np.mean(kernel_ms))
+    if with_hist and not fused:
+        roofline["hist_ms"] = float(np.mean(kernel_ms[1]))
+    if wl == 4 or (wl == 3):
+        # shared-memory roofline for the W=4 gather: 4 LDS.128 wavefronts per 32 lookups + 4 LDG wavefronts
+        # per 512 B, at 1 wavefront / SM / clock (sm_max_mhz)
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        lookups = n * L * K
+        wf = lookups / 32 * 4 * 4 / 4 + n * L * K / 512 * 4  # per launch group of 16 placements
+        roofline["smem_bound_ms_per_launch"] = wf / 148 / (mhz * 1e6) * 1e3
 
     # ---------------- e2e through the public API, host buffers ----------------
     e2e = None
     if not args.no_e2e:
         host = trace.to_host(pin=True)
+        steps_e = max(1, args.e2e_steps if wl != 5 else 1)
+
+        def api_call():
+            if with_hist:
+                return ev.evaluate_with_stats(host, placements, costs[0])[0].counts
+            return ev.score_sums(host, placements, costs)
+
+        api_call()  # warm-up
         evs = []
-        ev.evaluate_with_stats(host, placements, cost)  # warm-up
-        for _ in range(args.e2e_steps):
+        for _ in range(steps_e):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a, b = _events()
             a.record(stream)
-            f_h, reps = ev.evaluate_with_stats(host, placements, cost)  # H2D + kernels + D2H + floats
+            res = api_call()  # H2D (streamed, overlapped) + kernels + D2H + host floats
             b.record(stream)
             torch.cuda.synchronize()
             evs.append(a.elapsed_time(b))
-        if not np.array_equal(f_h.counts, counts0.cpu().numpy() if world == 1 else f_h.counts):
+        if with_hist and world == 1 and not np.array_equal(res, counts0.cpu().numpy()):
             raise SystemExit("bench: e2e histogram differs")
         t_e = torch.tensor([float(np.mean(evs))], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e_ms = float(t_e.item())
-        e2e = {"value": n_total * L * P / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(n * L * K * world), "d2h_bytes_per_step": int((L * E + P * C) * 8 * world),
-               "api": "moeplace.eval.evaluate_with_stats(trace in pinned host memory, 4 placements, cost)"}
+        api = ("moeplace.eval.evaluate_with_stats(trace in pinned host memory, 4 placements, cost)" if with_hist
+               else f"moeplace.eval.score_sums / evaluate_many(trace in pinned host memory, {P_} placements)")
+        e2e = {"value": n_total * L * P_ / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(n * L * K * world),
+               "d2h_bytes_per_step": int(((L * E if with_hist else 0) + P_ * C) * 8 * world), "api": api}
         del host
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        ns = min(args.cpu_tokens, n)
+        default_ns = {2: 1_000_000, 3: 250_000, 4: 2_000, 5: 1_000_000}[wl]
+        ns = min(args.cpu_tokens or default_ns, n)
         sel = cpu_sample(trace, ns)
         bnd = np.minimum(np.asarray(trace.chunk_bounds, dtype=np.int64), ns)
-        p_np = cost.numpy()
-        assigns = [pl.assign for pl in placements]
-        t_cpu = time_oracle(sel, bnd, p_np, assigns, reps=3)
+        from oracle import evaluate as oe
+        pes = []
+        cache = {}
+        for pl, cs in zip(placements, costs):
+            key = id(cs)
+            if key not in cache:
+                cache[key] = cs.numpy()
+            pes.append(oe.pe_table(cache[key], pl.assign))
+        oe.fused_pass(sel[:16], pes, bnd, E)
+        t_cpu = float("inf")
+        for _ in range(3):
+            t_a = time.perf_counter()
+            oe.fused_pass(sel, pes, bnd, E)
+            t_cpu = min(t_cpu, time.perf_counter() - t_a)
         thr = cpu_threads()
-        cpu = {"value": ns * L * P / t_cpu, "unit": UNIT, "cores": thr, "kind": "port",
-               "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P} "
-                         f"placements, oracle/ numba parallel, best of 3",
+        cpu = {"value": ns * L * P_ / t_cpu, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P_} "
+                         f"placements in one pass, oracle/ numba parallel, best of 3",
                "ms_per_sample": t_cpu * 1e3}
-        try:
-            import numba
-            numba.set_num_threads(1)
-            t1c = time_oracle(sel[:ns // 8], np.minimum(bnd, ns // 8), p_np, assigns, reps=1)
-            cpu["value_1_thread"] = (ns // 8) * L * P / t1c
-            numba.set_num_threads(thr)
-        except Exception:
-            pass
         try:
             cpu["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
         except Exception:
             pass
 
     if rank == 0:
+        cfg = workload(world, n, "fused" if fused else "separate")
+        if wl != 2:
+            cfg = {"workload": {3: "config3: DeepSeek-R1 shape, 10M Zipf(1.2) tokens/GPU, 16 placements (RR, Greedy, "
+                                   "ILP, ILPLoad) x 4 topologies (FatTree, FatTreeHier, Dragonfly, DragonflySparse, "
+                                   "16x4x4 = 256 devices) scored in one W=4 pass",
+                                4: "config4: DeepSeek-R1 shape, 1M Zipf(1.2) tokens/GPU, Dragonfly 16x4x4, 4096 candidate "
+                                   "placements (ILPLoad + 64 within-layer swaps each, seeds 1000+i) scored per step "
+                                   "(256 W=4 passes)",
+                                5: f"config5: DeepSeek-R1 shape, {n_total} Zipf(1.2) tokens total sharded over "
+                                   f"{world} GPU(s), 1500 chunks, FatTree 8x4x8; hist + score of 4 placements"}[wl],
+                   "tokens_per_gpu": n, "tokens_total": n_total, "placements": P_, "topologies": kinds,
+                   "l2": f"inputs larger than L2 ({n * L * K / 1e9:.2f} GB/GPU vs 126 MB)" if n * L * K > 126e6
+                   else f"trace {n * L * K / 1e6:.0f} MB < 126 MB L2: each step streams it {len(groups)}x; "
+                        "first pass per step from HBM, reuse from L2",
+                   "parallelism": f"token shards x{world}" + (" + 1 NCCL all_reduce" if world > 1 else "")}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
-                "config": workload(world, n, args.mode), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-                "hbm_gbs_step": n_total * L * K / (ms / 1e3) / 1e9 / world}
+                "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -184,6 +184,24 @@ def place_greedy(model: ModelSpec, attn: AttentionPlacement, cost: CostMatrix, c
     return Placement(assign, c, "greedy")
 
 
+def perturb_swaps(p: Placement, n_candidates: int, n_swaps: int, seed0: int = 1000) -> np.ndarray:
+    """Candidate placements for batched scoring (BASELINE config 4): candidate i applies
+    ``n_swaps`` within-layer swaps drawn with seed ``seed0 + i`` to ``p``.  Swapping the devices of
+    two experts of the same layer keeps every per-(device, layer) and per-device count, so all
+    candidates satisfy the constraints ``p`` satisfies.  Returns int32 [n_candidates, L, E]."""
+    L, E = p.assign.shape
+    out = np.repeat(p.assign[None], n_candidates, axis=0).astype(np.int32)
+    for i in range(n_candidates):
+        rng = np.random.default_rng(seed0 + i)
+        ls = rng.integers(0, L, n_swaps)
+        a = rng.integers(0, E, n_swaps)
+        b = rng.integers(0, E, n_swaps)
+        c = out[i]
+        for l, x, y in zip(ls, a, b):
+            c[l, x], c[l, y] = c[l, y], c[l, x]
+    return out
+
+
 def write_placement(p: Placement, path) -> None:
     """CSV with header layer,expert,device."""
     with open(path, "w", newline="") as f:
