@@ -174,6 +174,10 @@ def run_reference(args, rank: int, world: int) -> None:
             "config": workload(world, TOK_PER_GPU, "cpu-oracle"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line)
+
+
+def emit(line):  # replaced in main() by a writer to the saved stdout descriptor
     print(json.dumps(line), flush=True)
 
 
@@ -204,6 +208,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # stdout carries exactly one JSON line: route library chatter (NCCL banner, warnings) to stderr
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    global emit
+    emit = lambda line: os.write(json_fd, (json.dumps(line) + "\n").encode())  # noqa: E731
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -501,7 +511,7 @@ def main():
                 "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
                 "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

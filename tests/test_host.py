@@ -417,3 +417,40 @@ def test_exit_codes():
     assert exit_code(TopologyError("x")) == 2
     assert str(TraceParseError("bad", 7)) == "line 7: bad" and TraceParseError("bad", 7).line_no == 7
     assert issubclass(TopologyError, MoeplaceError)
+
+
+def test_perturb_swaps_keep_constraints():
+    rng = np.random.default_rng(0)
+    L, E, S = 6, 16, 16
+    base = np.stack([rng.permutation(S) for _ in range(L)]).astype(np.int32)
+    c = mpl.Constraints(6, 1)
+    cand = mpl.perturb_swaps(mpl.Placement(base), 20, 8, seed0=1000)
+    assert cand.shape == (20, L, E)
+    for i in range(20):
+        assert mpl.validate(mpl.Placement(cand[i]), c, mt.ModelSpec(L, E, 1), S) == []
+        assert (np.sort(cand[i], axis=1) == np.sort(base, axis=1)).all()
+    again = mpl.perturb_swaps(mpl.Placement(base), 20, 8, seed0=1000)
+    assert np.array_equal(cand, again)
+
+
+def test_dedup_oracle_hand_example():
+    from oracle import evaluate as oe
+    # one token, L=1, K=4 picks on devices of servers [0, 1, 1, 2]; dispatch server 0
+    sel = np.array([[[0, 1, 2, 3]]], dtype=np.uint8)
+    pe = np.array([[0, 4, 4, 6]])
+    srv_e = np.array([[0, 1, 1, 2]])
+    h, u, d = oe.dedup_sums(sel, pe, srv_e, np.array([0]), np.array([0, 1]))
+    assert h.tolist() == [14] and u.tolist() == [2] and d.tolist() == [10]
+
+
+def test_cpu_fused_pass_matches_separate():
+    from oracle import evaluate as oe
+    from oracle import gen as og
+    from oracle import stats as ost
+    sel, b = og.generate(5, 32, 4, 1.2, 3000, 7, 2)
+    rng = np.random.default_rng(1)
+    pes = [oe.pe_table(rng.integers(0, 200, (5, 8)), rng.integers(0, 8, (5, 32))) for _ in range(6)]
+    cnt, sums = oe.fused_pass(sel, pes, b, 32)
+    assert np.array_equal(cnt, ost.counts(sel, 32))
+    for q in range(6):
+        assert np.array_equal(sums[q], oe.chunk_sums(sel, pes[q], b))
