@@ -273,6 +273,36 @@ def evaluate_dedup(trace: ActivationTrace, placements: Sequence[Placement], cost
     return out
 
 
+def token_hops_all(trace: ActivationTrace, placements: Sequence[Placement], costs) -> np.ndarray:
+    """``token_hops`` of EVERY token of the trace for each placement:
+    int64 [P, N], from the token-tiled device kernel ``mp_token_hops_u8`` (4 placements per pass).
+    Per-token values are what per-chunk sums cannot give: hop distributions, percentiles, tails."""
+    t = _lib.torch()
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("token_hops_all: empty trace")
+    placements = list(placements)
+    costs = _as_costs(costs, len(placements))
+    planes = trace.device_planes()
+    validate_trace(trace)
+    n = trace.n_tokens
+    out = np.zeros((len(placements), n), dtype=np.int64)
+    for g0 in range(0, len(placements), 4):
+        grp = placements[g0:g0 + 4]
+        tables, max_p = _group_tables(grp, costs[g0:g0 + 4], m, 1)
+        hops = t.empty((4, n), dtype=t.int32, device=planes.device)
+        _lib.call("mp_token_hops_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
+                  _lib.ptr(tables), max_p, _lib.ptr(hops), _lib.stream_handle())
+        out[g0:g0 + len(grp)] = hops[:len(grp)].cpu().numpy().astype(np.int64)
+    return out
+
+
+def hop_distribution(trace: ActivationTrace, placement: Placement, cost: CostMatrix) -> np.ndarray:
+    """Histogram of per-token hops: out[h] = number of tokens whose token_hops == h."""
+    h = token_hops_all(trace, [placement], cost)[0]
+    return np.bincount(h)
+
+
 def token_hops(selections, placement: Placement, cost: CostMatrix) -> int:
     """sum over layers and selected experts of p[l, device(l, e)] for ONE token
     (``selections`` = L lists of selected experts).  Runs through the device scorer."""

@@ -427,3 +427,37 @@ def test_device_parser_R1_scale(tmp_path):
     assert np.array_equal(d.tokens(), tr.tokens())
     sel, _ = og.generate(L, E, K, 1.2, 20000, 30, 9)
     assert np.array_equal(mt.estimate_frequencies(d, m).counts, ost.counts(sel, E))
+
+
+@pytest.mark.parametrize("shape,kind,maxp", [(R1, "FatTree", None), (B16, "DragonflySparse", None),
+                                             ((5, 32, 8), None, 200), ((3, 64, 3), None, 100)])
+def test_token_hops_all_matches_oracle(shape, kind, maxp):
+    """Per-token hops of every token (token-tiled kernel) == the oracle's per-token sums; chunk
+    sums of them == the streaming scorer's."""
+    import torch
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    N = 9000
+    tr = mt.generate_trace(m, 1.2, N, 13, 4)
+    sel, bounds = og.generate(L, E, K, 1.2, N, 13, 4)
+    rng = np.random.default_rng(5)
+    if kind:
+        g, dist, order, attn, cost = setup_topology(kind, 4, 2, 4, m)
+        p = cost.numpy()
+        S = g.n_devices
+    else:
+        S = 16
+        p = rng.integers(0, maxp + 1, (L, S)).astype(np.uint8)
+        cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(6)]
+    got = ev.token_hops_all(tr, pls, cost)
+    sums = ev.score_sums(tr, pls, cost)
+    for i, pl in enumerate(pls):
+        want = oe.per_token_hops(sel, oe.pe_table(p, pl.assign))
+        assert np.array_equal(got[i], want)
+        assert np.array_equal(np.add.reduceat(got[i], bounds[:-1]) if (np.diff(bounds) > 0).all() else sums[i],
+                              sums[i])
+    v = tr.view(2, 9)
+    gv = ev.token_hops_all(v, pls[:1], cost)[0]
+    assert np.array_equal(gv, got[0][bounds[2]:bounds[9]])
+    assert ev.hop_distribution(tr, pls[0], cost).sum() == N
