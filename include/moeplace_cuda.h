@@ -100,7 +100,8 @@ int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int3
 /* ---- traffic evaluator: token_hops / evaluate -----------------
  * For placement q and chunk c:
  *   hop_sums[q*C + c] += sum_{t in chunk c, t in [tok_begin,tok_end)} sum_l sum_k pe_q[l][planes[l][t*K+k]]
- * chunk_bounds: device int64[C+1], ascending token indices; chunk c = [bounds[c], bounds[c+1]).
+ * chunk_bounds: device int64[C+1], ascending token indices; chunk c = [bounds[c], bounds[c+1]);
+ * the caller guarantees bounds[0] <= tok_begin and bounds[C] >= tok_end.
  * max_p: an upper bound on every table byte (selects the u8-lane widening interval).
  * hop_sums is int64[4W][C].                                                                  */
 int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,

@@ -53,15 +53,20 @@ __global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ 
     }
     __syncthreads();
     const uint32_t src = s_src;
-    for (int64_t t = r0; t < r1;) {
-      // chunk piece [t, te)
+    int c = 0;
+    {
       int lo = 0, hi = C;
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(bounds + mid) <= t) lo = mid; else hi = mid;
+        if (__ldg(bounds + mid) <= r0) lo = mid; else hi = mid;
       }
-      const int c = lo;
-      const int64_t te = min(r1, __ldg(bounds + c + 1));
+      c = lo;
+    }
+    int64_t cend = __ldg(bounds + c + 1);
+    for (int64_t t = r0; t < r1;) {
+      // chunk piece [t, te): walk forward from the previous chunk, skipping empty ones
+      while (cend <= t && c + 1 < C) cend = __ldg(bounds + (++c) + 1);
+      const int64_t te = min(r1, cend);
       uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};
       for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
         uint32_t ids[kDedupMaxK];

@@ -152,7 +152,9 @@ __device__ __forceinline__ int chunk_of(const int64_t* __restrict__ bounds, int 
   return lo;
 }
 
-constexpr int64_t kMaxPiece = (int64_t)1 << 30;  // keeps per-thread u32 sums exact
+// Pieces are capped so one warp's hop sum over a piece fits u32 (64 MB / 16 warps x 255 < 2^32),
+// which lets the per-piece flush reduce-scatter u32 values.
+constexpr int64_t kMaxPiece = (int64_t)1 << 26;
 
 template <bool HIST, int W, int WIDEN, int UNROLL>
 __global__ void __launch_bounds__(kThreads, (W == 4 || W == 2) ? 2 : 3)
@@ -193,17 +195,18 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
     __syncthreads();
 
     if constexpr (W > 0) {
+      // chunk of the segment's first byte by binary search, then walk forward (pieces are in order)
+      int c = chunk_of(bounds, C, x0 / K);
+      int64_t cend = __ldg(bounds + c + 1) * K;
       for (int64_t x = x0; x < x1;) {
-        const int c = chunk_of(bounds, C, x / K);
-        const int64_t xe = min(min(x1, __ldg(bounds + c + 1) * K), x + kMaxPiece);
+        while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
+        const int64_t xe = min(min(x1, cend), x + kMaxPiece);
         ScoreAcc<WW> acc;
         acc.zero();
         st.range(plane, x, xe, acc);
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-          const unsigned long long s = warp_sum_u64(acc.tot[q]);
-          if (lane == 0 && s) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)s);
-        }
+        int q = 0;
+        const uint32_t tot = warp_reduce_scatter<P>(acc.tot, lane, &q);
+        if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
         x = xe;
       }
     } else {
