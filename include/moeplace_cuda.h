@@ -90,6 +90,16 @@ int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_
 int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
                int L, int K, int E, int64_t* counts, int64_t* err, void* stream);
 
+/* ---- factorized evaluator (SPEC.md:383 linearity) -------------------------------
+ * mp_hist_chunks_u8: per-chunk histogram, counts[(c*L + l)*E + e] += #{(t,k): t in chunk c, ...}
+ *   (int64 [C][L][E]; same bounds contract as mp_score_u8).
+ * mp_contract_counts: out[q*C + c] += sum_i counts[c*LE + i] * pe[q*LE + i] (int64, exact; each
+ *   count must be < 2^31), pe = uint8 [P][LE] per-expert round-trip costs (LE = L*E).
+ * Together they give exactly mp_score_u8's per-chunk hop sums for any number of placements.    */
+int mp_hist_chunks_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                      int E, const int64_t* chunk_bounds, int C, int64_t* counts, int64_t* err, void* stream);
+int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out, void* stream);
+
 /* ---- placement tables: Placement -> per-expert round-trip hops ---------
  * tables[((l*256 + e)*W + w)] is a u32 whose byte j is pe_q[l][e] = cost[topo_of[q]][l][assign[q][l][e]]
  * for placement q = 4*w + j (q < P; unused lanes and e >= E are 0).  W = 1, 2 or 4 (P <= 4W).

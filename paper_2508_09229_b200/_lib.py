@@ -28,6 +28,8 @@ SIGNATURES = {
     "mp_find_newlines": (_i32, [_p, _i64, _p, _p, _p]),
     "mp_parse_trace_text": (_i32, [_p, _p, _i64, _i64, _i32, _i32, _i32, _p, _i64, _p, _p, _p]),
     "mp_hist_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p]),
+    "mp_hist_chunks_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p]),
+    "mp_contract_counts": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
     "mp_pack_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _i32, _p, _p]),
     "mp_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p]),
     "mp_token_hops_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p]),

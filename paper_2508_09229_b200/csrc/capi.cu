@@ -34,6 +34,10 @@ cudaError_t launch_parse(const uint8_t* text, const int64_t* ends, int64_t first
                          int E, uint8_t* planes, int64_t stride, int64_t* chunk_ids, int64_t* err, cudaStream_t s);
 cudaError_t launch_token_hops(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
                               const uint32_t* tables, int max_p, uint32_t* hops, cudaStream_t s);
+cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                               const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s);
+cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out,
+                            cudaStream_t s);
 }  // namespace mp
 
 namespace {
@@ -90,6 +94,23 @@ int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, i
   if (tok_end == tok_begin) return MP_OK;
   return status(mp::launch_stream(true, 0, 0, planes, plane_stride, tok_begin, tok_end, L, K, E, nullptr, 1, nullptr,
                                   counts, nullptr, err, S(stream)));
+}
+
+int mp_hist_chunks_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                      int E, const int64_t* chunk_bounds, int C, int64_t* counts, int64_t* err, void* stream) {
+  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (E <= 0 || !counts || !chunk_bounds || C <= 0) return MP_ERR_ARG;
+  if (tok_end == tok_begin) return MP_OK;
+  return status(mp::launch_hist_chunks(planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C, counts, err,
+                                       S(stream)));
+}
+
+int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out, void* stream) {
+  if (!counts || !pe || !out || C <= 0 || P <= 0 || LE <= 0) return MP_ERR_ARG;
+  if (C > 65535 * 16) return MP_ERR_UNSUPPORTED;
+  return status(mp::launch_contract(counts, C, pe, P, LE, out, S(stream)));
 }
 
 int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,

@@ -156,7 +156,7 @@ __device__ __forceinline__ int chunk_of(const int64_t* __restrict__ bounds, int 
 // which lets the per-piece flush reduce-scatter u32 values.
 constexpr int64_t kMaxPiece = (int64_t)1 << 26;
 
-template <bool HIST, int W, int WIDEN, int UNROLL>
+template <bool HIST, int W, int WIDEN, int UNROLL, bool CHUNKED = false>
 __global__ void __launch_bounds__(kThreads, (W == 4 || W == 2) ? 2 : 3)
 stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
               const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
@@ -194,7 +194,25 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
     }
     __syncthreads();
 
-    if constexpr (W > 0) {
+    // histogram flush: replica sums of every bin -> dst[l*E + e] (and zero the replicas)
+    auto flush_hist = [&](int64_t* dst) {
+      for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+        uint32_t* row = smw + e * 64 + 32;
+        uint32_t s = 0;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+          const int rr = (r + e) & 31;  // rotate: no bank conflicts
+          s += row[rr];
+          if (CHUNKED) row[rr] = 0;
+        }
+        if (s) {
+          if (e < E) atomic_add_i64(dst + (int64_t)l * E + e, (int64_t)s);
+          else report_err(err, MP_DATA_EXPERT_RANGE, l, e, s);
+        }
+      }
+    };
+
+    if constexpr (W > 0 || CHUNKED) {
       // chunk of the segment's first byte by binary search, then walk forward (pieces are in order)
       int c = chunk_of(bounds, C, x0 / K);
       int64_t cend = __ldg(bounds + c + 1) * K;
@@ -204,9 +222,16 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
         ScoreAcc<WW> acc;
         acc.zero();
         st.range(plane, x, xe, acc);
-        int q = 0;
-        const uint32_t tot = warp_reduce_scatter<P>(acc.tot, lane, &q);
-        if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
+        if constexpr (W > 0) {
+          int q = 0;
+          const uint32_t tot = warp_reduce_scatter<P>(acc.tot, lane, &q);
+          if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
+        }
+        if constexpr (CHUNKED) {  // per-chunk histogram: counts is [C][L][E]
+          __syncthreads();
+          flush_hist(counts + (int64_t)c * L * E);
+          __syncthreads();
+        }
         x = xe;
       }
     } else {
@@ -214,18 +239,9 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
       st.range(plane, x0, x1, dummy);
     }
 
-    if constexpr (HIST) {
+    if constexpr (HIST && !CHUNKED) {
       __syncthreads();
-      for (int e = threadIdx.x; e < 256; e += blockDim.x) {
-        const uint32_t* row = smw + e * 64 + 32;
-        uint32_t s = 0;
-#pragma unroll 8
-        for (int r = 0; r < 32; ++r) s += row[(r + e) & 31];  // rotate: no bank conflicts
-        if (s) {
-          if (e < E) atomic_add_i64(counts + (int64_t)l * E + e, (int64_t)s);
-          else report_err(err, MP_DATA_EXPERT_RANGE, l, e, s);
-        }
-      }
+      flush_hist(counts);
     }
     g += seg;
   }
@@ -233,12 +249,12 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 
 constexpr int kSmemBytes = 256 * 256;
 
-template <bool HIST, int W, int WIDEN>
+template <bool HIST, int W, int WIDEN, bool CHUNKED = false>
 static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                             const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                             int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   constexpr int UNROLL = 4;
-  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL>;
+  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -254,6 +270,59 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
   grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
   kern<<<(unsigned)grid, kThreads, kSmemBytes, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
                                                      hop_sums, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                               const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s) {
+  return launch_t<true, 0, 16, true>(planes, stride, t0, t1, L, K, E, bounds, C, nullptr, counts, nullptr, err, s);
+}
+
+// ---- exact contraction of per-chunk counts with per-expert costs (factorized evaluator) ----
+// out[q*C + c] += sum_i counts[c*LE + i] * pe[q*LE + i]; tiles of 64 placements x 16 chunks,
+// LE streamed in 128-wide slices through shared memory; int64 accumulation (exact).
+constexpr int kCtP = 64, kCtC = 16, kCtI = 128;
+
+__global__ void __launch_bounds__(256) contract_kernel(const int64_t* __restrict__ counts, int C,
+                                                       const uint8_t* __restrict__ pe, int P, int64_t LE,
+                                                       int64_t* __restrict__ out) {
+  __shared__ uint8_t s_pe[kCtP][kCtI];
+  __shared__ int32_t s_cnt[kCtC][kCtI + 1];
+  const int q0 = blockIdx.x * kCtP, c0 = blockIdx.y * kCtC;
+  const int tq = threadIdx.x & 63;   // placement within tile
+  const int tc = threadIdx.x >> 6;   // 4 chunk lanes: chunks tc, tc+4, tc+8, tc+12
+  int64_t acc[4] = {0, 0, 0, 0};
+  for (int64_t i0 = 0; i0 < LE; i0 += kCtI) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kCtP * kCtI; k += blockDim.x) {
+      const int qq = k / kCtI, ii = k % kCtI;
+      s_pe[qq][ii] = (q0 + qq < P && i0 + ii < LE) ? pe[(int64_t)(q0 + qq) * LE + i0 + ii] : 0;
+    }
+    for (int k = threadIdx.x; k < kCtC * kCtI; k += blockDim.x) {
+      const int cc = k / kCtI, ii = k % kCtI;
+      s_cnt[cc][ii] = (c0 + cc < C && i0 + ii < LE) ? (int32_t)counts[(int64_t)(c0 + cc) * LE + i0 + ii] : 0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int ii = 0; ii < kCtI; ++ii) {
+      const int32_t w = s_pe[tq][ii];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += (int64_t)w * s_cnt[tc + 4 * j][ii];
+    }
+  }
+  if (q0 + tq < P)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + tc + 4 * j;
+      if (c < C && acc[j]) atomic_add_i64(out + (int64_t)(q0 + tq) * C + c, acc[j]);
+    }
+}
+
+cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out,
+                            cudaStream_t s) {
+  if (P <= 0 || C <= 0 || LE <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((P + kCtP - 1) / kCtP), (unsigned)((C + kCtC - 1) / kCtC));
+  contract_kernel<<<grid, 256, 0, s>>>(counts, C, pe, P, LE, out);
   return cudaGetLastError();
 }
 

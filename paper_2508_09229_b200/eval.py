@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, MoeplaceError
-from .model_trace import (ActivationTrace, FrequencyTable, ModelSpec, frequencies_from_counts, sweep,
+from .model_trace import (ActivationTrace, FrequencyTable, ModelSpec, chunk_counts, frequencies_from_counts, sweep,
                           validate_trace)
 from .placement import CostMatrix, Placement
 
@@ -154,11 +154,52 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs) -
     return out
 
 
-def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs) -> list[EvalReport]:
-    """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies):
-    up to 16 placements per pass over the trace (extension A18)."""
+def pe_matrix(placements: Sequence[Placement], costs, model: ModelSpec):
+    """uint8 [P, L*E] per-expert round-trip costs pe_q[l, e] = p_q[l, assign_q[l, e]] on the device."""
+    t = _lib.torch()
     placements = list(placements)
-    sums = score_sums(trace, placements, costs)
+    costs = _as_costs(costs, len(placements))
+    dev = _lib.require_cuda()
+    out = t.empty((len(placements), model.L * model.E), dtype=t.uint8, device=dev)
+    for i, (pl, c) in enumerate(zip(placements, costs)):
+        a = _lib.to_dev(pl.assign, t.int64)
+        if int(a.min()) < 0 or int(a.max()) >= c.S:
+            raise MoeplaceError("evaluate: expert placed outside the topology")
+        out[i] = t.gather(c.p, 1, a).reshape(-1)
+    return out
+
+
+def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement], costs) -> np.ndarray:
+    """Per-chunk hop sums via the factorized evaluator: one per-chunk histogram pass
+    (``mp_hist_chunks_u8``) and an exact integer contraction with every placement's per-expert
+    costs (``mp_contract_counts``).  Bit-identical to ``score_sums`` by linearity (SPEC.md:383);
+    cost independent of P per token.  A cross-check and the fast path for large candidate
+    batches — it produces no per-token values (use ``token_hops_all`` / ``evaluate_dedup``)."""
+    t = _lib.torch()
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("evaluate: empty trace")
+    cnt = chunk_counts(trace)
+    C = trace.n_chunks
+    pe = pe_matrix(placements, costs, m)
+    out = t.zeros((pe.shape[0], C), dtype=t.int64, device=cnt.device)
+    _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe), pe.shape[0], m.L * m.E, _lib.ptr(out),
+              _lib.stream_handle())
+    return out.cpu().numpy()
+
+
+def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs,
+                  method: str = "gather") -> list[EvalReport]:
+    """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies):
+    up to 16 placements per pass over the trace (extension A18).  ``method="factorized"`` uses
+    the per-chunk-histogram evaluator instead (identical integers)."""
+    placements = list(placements)
+    if method == "gather":
+        sums = score_sums(trace, placements, costs)
+    elif method == "factorized":
+        sums = score_sums_factorized(trace, placements, costs)
+    else:
+        raise ConfigError(f"unknown evaluate method {method!r}")
     tokens = trace.chunk_token_counts()
     return [report_from_sums(sums[i], tokens, placements[i].label) for i in range(len(placements))]
 

@@ -544,6 +544,24 @@ def trace_counts(trace: ActivationTrace):
     return counts
 
 
+def chunk_counts(trace: ActivationTrace):
+    """Per-chunk load counts, device int64 [C, L, E] (``mp_hist_chunks_u8``): the sufficient
+    statistics of every per-chunk hop sum (SPEC.md:383 linearity)."""
+    t = _lib.torch()
+    m = trace.model
+    C = trace.n_chunks
+    counts = t.zeros((C, m.L, m.E), dtype=t.int64, device=_lib.require_cuda())
+    err = _lib.new_err()
+
+    def launch(planes, stride, t0, t1, bounds):
+        _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, m.E, _lib.ptr(bounds), C,
+                  _lib.ptr(counts), _lib.ptr(err), _lib.stream_handle())
+
+    sweep(trace, launch)
+    _lib.check_err(err, "chunk_counts")
+    return counts
+
+
 def frequencies_from_counts(counts: np.ndarray, n_tokens: int, K: int) -> FrequencyTable:
     counts = np.asarray(counts, dtype=np.int64)
     return FrequencyTable(counts / (K * n_tokens), counts, int(n_tokens), int(K))

@@ -461,3 +461,29 @@ def test_token_hops_all_matches_oracle(shape, kind, maxp):
     gv = ev.token_hops_all(v, pls[:1], cost)[0]
     assert np.array_equal(gv, got[0][bounds[2]:bounds[9]])
     assert ev.hop_distribution(tr, pls[0], cost).sum() == N
+
+
+@pytest.mark.parametrize("shape", [R1, B16, (3, 5, 2)])
+def test_factorized_evaluator_matches_gather(shape):
+    """per-chunk histograms + exact contraction == per-token gather, bit for bit, for
+    many placements over several topologies; per-chunk counts == oracle per chunk."""
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    N, C = 5003, 23
+    tr = mt.generate_trace(m, 1.2, N, C, 8)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 8)
+    cc = mt.chunk_counts(tr).cpu().numpy()
+    for c in range(C):
+        assert np.array_equal(cc[c], ost.counts(sel[bounds[c]:bounds[c + 1]], E)), c
+    costs, pls = [], []
+    for i, kind in enumerate(["FatTree", "Dragonfly", "DragonflySparse"]):
+        g, dist, order, attn, cost = setup_topology(kind, 4, 2, 2, m)
+        for j in range(7):
+            pls.append(mpl.Placement(random_assign(np.random.default_rng(31 * i + j), L, E, g.n_devices)))
+            costs.append(cost)
+    a = ev.score_sums(tr, pls, costs)
+    b = ev.score_sums_factorized(tr, pls, costs)
+    assert np.array_equal(a, b)
+    ra = ev.evaluate_many(tr.view(3, 20), pls[:5], costs[:5])
+    rb = ev.evaluate_many(tr.view(3, 20), pls[:5], costs[:5], method="factorized")
+    assert [r.chunk_hop_sums for r in ra] == [r.chunk_hop_sums for r in rb]
