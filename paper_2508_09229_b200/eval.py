@@ -169,12 +169,50 @@ def pe_matrix(placements: Sequence[Placement], costs, model: ModelSpec):
     return out
 
 
-def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement], costs) -> np.ndarray:
+def _digits(x, bits: int = 7):
+    """Number of base-2^bits digits needed for non-negative integer tensor x."""
+    mx = int(x.max().item()) if x.numel() else 0
+    d = 1
+    while mx >= (1 << (bits * d)):
+        d += 1
+    return d
+
+
+def contract_tc(cnt, pe):
+    """Exact hop sums [P, C] = pe [P, LE] (uint8) @ cnt^T [LE, C] (int64 counts) on the tensor cores:
+    both operands are split into 7-bit digits (int8 >= 0), every digit pair is one int8 GEMM with
+    int32 accumulation (cuBLASLt; exact since LE * 127^2 < 2^31 for LE <= 133,000), and the
+    partial products are recombined in int64 with weights 128^(a+b)."""
+    t = _lib.torch()
+    P, LE = pe.shape
+    C = cnt.shape[0]
+    if LE * 127 * 127 >= 2 ** 31:
+        raise ConfigError("contract_tc: L*E too large for exact int32 accumulation")
+    Pp, Cp = max(32, -(-P // 32) * 32), max(8, -(-C // 8) * 8)
+    LEp = max(16, -(-LE // 16) * 16)  # cuBLASLt int8: K a multiple of 16 (zero padding is exact)
+    pe_w = pe.to(t.int64)
+    out = t.zeros((P, C), dtype=t.int64, device=pe.device)
+    da, db = _digits(cnt), _digits(pe_w)
+    A = t.zeros((Pp, LEp), dtype=t.int8, device=pe.device)
+    B = t.zeros((Cp, LEp), dtype=t.int8, device=pe.device)  # B^T row-major == B column-major
+    for b in range(db):
+        A[:P, :LE].copy_(((pe_w >> (7 * b)) & 127).to(t.int8))
+        for a in range(da):
+            B[:C, :LE].copy_(((cnt >> (7 * a)) & 127).to(t.int8))
+            part = t._int_mm(A, B.t())  # int32 [Pp, Cp], exact
+            out += part[:P, :C].to(t.int64) << (7 * (a + b))
+    return out
+
+
+def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement], costs,
+                          contraction: str = "tc") -> np.ndarray:
     """Per-chunk hop sums via the factorized evaluator: one per-chunk histogram pass
     (``mp_hist_chunks_u8``) and an exact integer contraction with every placement's per-expert
-    costs (``mp_contract_counts``).  Bit-identical to ``score_sums`` by linearity (SPEC.md:383);
-    cost independent of P per token.  A cross-check and the fast path for large candidate
-    batches — it produces no per-token values (use ``token_hops_all`` / ``evaluate_dedup``)."""
+    costs — on the tensor cores (``contraction="tc"``: 7-bit-digit int8 GEMMs, cuBLASLt) or with
+    the CUDA-core int64 kernel ``mp_contract_counts`` (``"cuda"``).  Bit-identical to
+    ``score_sums`` by linearity; cost independent of P per token.  A cross-check
+    and the fast path for large candidate batches — it produces no per-token values (use
+    ``token_hops_all`` / ``evaluate_dedup`` for those)."""
     t = _lib.torch()
     m = trace.model
     if m is None or trace.n_tokens == 0:
@@ -182,9 +220,14 @@ def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement
     cnt = chunk_counts(trace)
     C = trace.n_chunks
     pe = pe_matrix(placements, costs, m)
-    out = t.zeros((pe.shape[0], C), dtype=t.int64, device=cnt.device)
-    _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe), pe.shape[0], m.L * m.E, _lib.ptr(out),
-              _lib.stream_handle())
+    if contraction == "tc":
+        out = contract_tc(cnt.view(C, -1), pe)
+    elif contraction == "cuda":
+        out = t.zeros((pe.shape[0], C), dtype=t.int64, device=cnt.device)
+        _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe), pe.shape[0], m.L * m.E, _lib.ptr(out),
+                  _lib.stream_handle())
+    else:
+        raise ConfigError(f"unknown contraction {contraction!r}")
     return out.cpu().numpy()
 
 

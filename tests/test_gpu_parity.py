@@ -483,7 +483,20 @@ def test_factorized_evaluator_matches_gather(shape):
             costs.append(cost)
     a = ev.score_sums(tr, pls, costs)
     b = ev.score_sums_factorized(tr, pls, costs)
-    assert np.array_equal(a, b)
+    c2 = ev.score_sums_factorized(tr, pls, costs, contraction="cuda")
+    assert np.array_equal(a, b) and np.array_equal(a, c2)
     ra = ev.evaluate_many(tr.view(3, 20), pls[:5], costs[:5])
     rb = ev.evaluate_many(tr.view(3, 20), pls[:5], costs[:5], method="factorized")
     assert [r.chunk_hop_sums for r in ra] == [r.chunk_hop_sums for r in rb]
+
+
+def test_contract_tc_digit_paths():
+    """Exact tensor-core contraction with multi-digit operands (pe up to 255, counts up to 2^20)."""
+    import torch
+    rng = np.random.default_rng(0)
+    P, LE, C = 37, 1000, 11
+    pe = torch.as_tensor(rng.integers(0, 256, (P, LE)).astype(np.uint8), device="cuda")
+    cnt = torch.as_tensor(rng.integers(0, 2 ** 20, (C, LE)), device="cuda")
+    got = ev.contract_tc(cnt, pe).cpu().numpy()
+    want = pe.cpu().numpy().astype(np.int64) @ cnt.cpu().numpy().T
+    assert np.array_equal(got, want)
