@@ -11,4 +11,4 @@ __version__ = "0.1.0"
 
 from . import errors  # noqa: F401  (import order: errors first, no torch needed)
 
-MODULES = ("errors", "topology", "model_trace", "placement", "solver", "eval", "cli")
+MODULES = ("errors", "topology", "model_trace", "placement", "solver", "eval", "cli", "search", "shard")

@@ -1,0 +1,108 @@
+"""GPU-driven placement search (extension beyond the reference).
+
+Local search over placements: every iteration perturbs the incumbent into a batch of candidates
+with random within-layer swaps (which keep every per-(device, layer) and per-device count, so
+constraints stay satisfied — SPEC.md:182-191), scores the whole batch at once with the factorized
+evaluator (per-chunk counts computed ONCE on the device, then one exact tensor-core contraction per
+batch, `eval.contract_tc`) and accepts the best candidate if it improves the objective.
+
+Objectives are functions of the exact per-chunk hop sums, so they can be non-linear where the ILP
+of Eq. (1) is linear:
+  * "mean"       token-weighted mean hops (= K * objective_value; ILPLoad is optimal)
+  * "mean+std"   mean + lam * population std of per-chunk means (robustness across dialogs)
+  * "max"        worst per-chunk mean
+Everything (perturbation, cost gather, contraction, objective, argmin) stays on the GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, MoeplaceError
+from .eval import contract_tc
+from .model_trace import ActivationTrace, chunk_counts
+from .placement import CostMatrix, Placement
+
+
+@dataclass
+class SearchResult:
+    placement: Placement
+    objective: float
+    history: list = field(default_factory=list)  # objective of the incumbent after each iteration
+    evaluated: int = 0                          # candidates scored
+
+
+def _objective(sums, tokens, kind: str, lam: float):
+    """sums: int64 [B, C] (device), tokens: int64 [C] -> float64 [B]."""
+    t = _lib.torch()
+    keep = tokens > 0
+    s = sums[:, keep].to(t.float64)
+    n = tokens[keep].to(t.float64)
+    mean = s.sum(dim=1) / n.sum()
+    if kind == "mean":
+        return mean
+    means = s / n
+    if kind == "mean+std":
+        return mean + lam * means.std(dim=1, unbiased=False)
+    if kind == "max":
+        return means.max(dim=1).values
+    raise ConfigError(f"unknown objective {kind!r}")
+
+
+def perturb(assign, batch: int, n_swaps: int, gen):
+    """[B, L, E] candidates: `n_swaps` random within-layer swaps of `assign` each (device)."""
+    t = _lib.torch()
+    L, E = assign.shape
+    cand = assign.unsqueeze(0).repeat(batch, 1, 1)
+    b = t.arange(batch, device=assign.device)
+    for _ in range(n_swaps):
+        l = t.randint(0, L, (batch,), device=assign.device, generator=gen)
+        x = t.randint(0, E, (batch,), device=assign.device, generator=gen)
+        y = t.randint(0, E, (batch,), device=assign.device, generator=gen)
+        vx = cand[b, l, x].clone()
+        vy = cand[b, l, y].clone()
+        cand[b, l, x] = vy
+        cand[b, l, y] = vx
+    return cand
+
+
+def improve_placement(trace: ActivationTrace, start: Placement, cost: CostMatrix, objective: str = "mean",
+                      lam: float = 1.0, iters: int = 50, batch: int = 1024, n_swaps: int = 2,
+                      seed: int = 0) -> SearchResult:
+    """Batched local search from `start` on `trace` (e.g. the train split)."""
+    t = _lib.torch()
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("improve_placement: empty trace")
+    if start.assign.shape != (m.L, m.E):
+        raise ConfigError("placement shape does not match the trace")
+    dev = _lib.require_cuda()
+    C = trace.n_chunks
+    cnt = chunk_counts(trace).view(C, -1)          # once: [C, L*E]
+    tokens = t.as_tensor(trace.chunk_token_counts(), device=dev)
+    p = cost.p.to(t.int64)                          # [L, S]
+    gen = t.Generator(device=dev)
+    gen.manual_seed(seed)
+    cur = _lib.to_dev(start.assign, t.int64)
+
+    def score(cands):
+        pe = t.gather(p.unsqueeze(0).expand(cands.shape[0], -1, -1), 2, cands)  # [B, L, E]
+        sums = contract_tc(cnt, pe.reshape(cands.shape[0], -1).to(t.uint8))
+        return _objective(sums, tokens, objective, lam)
+
+    best = float(score(cur.unsqueeze(0))[0].item())
+    hist = [best]
+    evaluated = 1
+    for _ in range(iters):
+        cands = perturb(cur, batch, n_swaps, gen)
+        obj = score(cands)
+        evaluated += batch
+        i = int(t.argmin(obj).item())
+        v = float(obj[i].item())
+        if v < best:
+            best, cur = v, cands[i].clone()
+        hist.append(best)
+    out = Placement(cur.to(t.int32).cpu().numpy(), start.constraints, (start.label or "start") + f"+search[{objective}]")
+    return SearchResult(out, best, hist, evaluated)

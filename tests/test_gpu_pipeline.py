@@ -158,3 +158,24 @@ def test_sharded_evaluate_world1_matches():
         if b > a:
             tot += mt.estimate_frequencies(sh, m).counts
     assert np.array_equal(tot, f2.counts)
+
+
+def test_placement_search_improves_and_keeps_constraints():
+    """F4: batched local search (device perturbation + tensor-core scoring) improves the objective
+    monotonically, keeps constraints, and on the linear objective never beats the ILP optimum."""
+    import moeplace.search as se
+    m = mt.ModelSpec(27, 64, 6)
+    g, dist, order, attn, cost = setup_topology("DragonflySparse", 8, 2, 2, m)
+    c = mpl.Constraints(64, 2)
+    tr = mt.generate_trace(m, 1.2, 20000, 40, 3)
+    rr = mpl.place_round_robin(m, attn, order, c)
+    res = se.improve_placement(tr, rr, cost, "mean", iters=20, batch=512, n_swaps=2, seed=1)
+    assert all(a >= b for a, b in zip(res.history, res.history[1:]))
+    assert res.history[-1] < res.history[0]
+    assert mpl.validate(res.placement, c, m, g.n_devices) == []
+    rep = ev.evaluate(tr, res.placement, cost)
+    assert abs(rep.mean_hops_per_token - res.objective) <= 1e-9 * res.objective
+    ilp = sv.solve_exact(sv.build_instance(cost, mt.estimate_frequencies(tr, m), c))[0]
+    assert ev.evaluate(tr, ilp, cost).mean_hops_per_token <= res.objective + 1e-9
+    r2 = se.improve_placement(tr, ilp, cost, "mean+std", lam=2.0, iters=10, batch=256, seed=2)
+    assert r2.history[-1] <= r2.history[0]
