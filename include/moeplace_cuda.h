@@ -84,6 +84,16 @@ int mp_find_newlines(const uint8_t* text, int64_t n, const int64_t* offsets, int
 int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
                         int E, uint8_t* planes, int64_t plane_stride, int64_t* chunk_ids, int64_t* err, void* stream);
 
+/* ---- text encoder: write_trace on the device ---------------------------
+ * mp_format_lengths: lengths[i] = byte length of token (tok_begin+i)'s canonical line
+ *   "cid\tlayer0:e,..,e\t...\n" (cids: device int64 [n], one chunk id per token, >= 0).
+ * mp_format_trace_text: writes each line at out[offsets[i]] (offsets = exclusive prefix sum of
+ *   lengths, so the lines are contiguous and in token order).                                  */
+int mp_format_lengths(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                      const int64_t* cids, int64_t* lengths, void* stream);
+int mp_format_trace_text(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                         const int64_t* cids, const int64_t* offsets, uint8_t* out, void* stream);
+
 /* ---- load statistics: estimate_frequencies ------------------------
  * counts[l*E + e] += #{(t,k) : t in [tok_begin,tok_end), planes[l][t*K+k] == e}.
  * Ids >= E are not counted; they raise MP_DATA_EXPERT_RANGE in err.                          */

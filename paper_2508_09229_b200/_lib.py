@@ -27,6 +27,8 @@ SIGNATURES = {
     "mp_count_newlines": (_i32, [_p, _i64, _p, _p]),
     "mp_find_newlines": (_i32, [_p, _i64, _p, _p, _p]),
     "mp_parse_trace_text": (_i32, [_p, _p, _i64, _i64, _i32, _i32, _i32, _p, _i64, _p, _p, _p]),
+    "mp_format_lengths": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _p, _p]),
+    "mp_format_trace_text": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _p, _p, _p]),
     "mp_hist_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p]),
     "mp_hist_chunks_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p]),
     "mp_contract_counts": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),

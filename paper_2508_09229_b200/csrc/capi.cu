@@ -38,6 +38,8 @@ cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0
                                const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s);
 cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out,
                             cudaStream_t s);
+cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
+                          const int64_t* cids, int64_t* lens_or_offsets, uint8_t* out, cudaStream_t s);
 }  // namespace mp
 
 namespace {
@@ -234,6 +236,24 @@ int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_
   if (r) return r;
   return status(mp::launch_parse(text, ends, first_start, n_lines, L, K, E, planes, plane_stride, chunk_ids, err,
                                  S(stream)));
+}
+
+int mp_format_lengths(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                      const int64_t* cids, int64_t* lengths, void* stream) {
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (!cids || !lengths) return MP_ERR_ARG;
+  return status(mp::launch_format(false, planes, plane_stride, tok_begin, tok_end, L, K, cids, lengths, nullptr,
+                                  S(stream)));
+}
+
+int mp_format_trace_text(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                         const int64_t* cids, const int64_t* offsets, uint8_t* out, void* stream) {
+  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
+  if (r) return r;
+  if (!cids || !offsets || !out) return MP_ERR_ARG;
+  return status(mp::launch_format(true, planes, plane_stride, tok_begin, tok_end, L, K, cids,
+                                  const_cast<int64_t*>(offsets), out, S(stream)));
 }
 
 int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t src_stride, int64_t width, int rows,

@@ -185,3 +185,66 @@ cudaError_t launch_parse(const uint8_t* text, const int64_t* ends, int64_t first
 }
 
 }  // namespace mp
+
+// ---- text encoder: write_trace on the device (canonical "cid\tlayer<l>:e,..,e\t...\n") ------
+namespace mp {
+
+__device__ __forceinline__ int ndigits(uint64_t v) {
+  int n = 1;
+  while (v >= 10) { v /= 10; ++n; }
+  return n;
+}
+
+__device__ __forceinline__ int64_t put_uint(uint8_t* out, int64_t p, uint64_t v) {
+  const int n = ndigits(v);
+  for (int i = n - 1; i >= 0; --i) { out[p + i] = (uint8_t)('0' + v % 10); v /= 10; }
+  return p + n;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(256) format_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0,
+                                                     int64_t n, int L, int K, const int64_t* __restrict__ cids,
+                                                     int64_t* __restrict__ lens_or_offsets, uint8_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + i;
+    if (!WRITE) {
+      int64_t len = ndigits((uint64_t)cids[i]) + 1;  // cid + '\t'
+      for (int l = 0; l < L; ++l) {
+        len += 5 + ndigits((uint64_t)l) + 1 + (K - 1) + 1;  // "layer" l ':' commas '\t'|'\n'
+        const uint8_t* rec = planes + (int64_t)l * stride + t * K;
+        for (int k = 0; k < K; ++k) len += ndigits(rec[k]);
+      }
+      lens_or_offsets[i] = len;
+    } else {
+      int64_t p = lens_or_offsets[i];
+      p = put_uint(out, p, (uint64_t)cids[i]);
+      out[p++] = '\t';
+      for (int l = 0; l < L; ++l) {
+        out[p++] = 'l'; out[p++] = 'a'; out[p++] = 'y'; out[p++] = 'e'; out[p++] = 'r';
+        p = put_uint(out, p, (uint64_t)l);
+        out[p++] = ':';
+        const uint8_t* rec = planes + (int64_t)l * stride + t * K;
+        for (int k = 0; k < K; ++k) {
+          p = put_uint(out, p, rec[k]);
+          if (k + 1 < K) out[p++] = ',';
+        }
+        out[p++] = (l + 1 < L) ? '\t' : '\n';
+      }
+    }
+  }
+}
+
+cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
+                          const int64_t* cids, int64_t* lens_or_offsets, uint8_t* out, cudaStream_t s) {
+  const int64_t n = t1 - t0;
+  if (n <= 0) return cudaSuccess;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)min((n + 255) / 256, (int64_t)nsm * 16);
+  if (write) format_kernel<true><<<grid, 256, 0, s>>>(planes, stride, t0, n, L, K, cids, lens_or_offsets, out);
+  else format_kernel<false><<<grid, 256, 0, s>>>(planes, stride, t0, n, L, K, cids, lens_or_offsets, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mp

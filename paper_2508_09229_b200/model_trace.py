@@ -428,8 +428,46 @@ def _parse_trace_host(path) -> ActivationTrace:
     return tr
 
 
-def write_trace(trace: ActivationTrace, path) -> None:
-    """Canonical text form: header, then one line per token in chunk-grouped order."""
+def write_trace(trace: ActivationTrace, path, engine: str = "auto") -> None:
+    """SPEC.md:132-139, 170.  Canonical text form: header, then one line per token in
+    chunk-grouped order.  ``engine="cuda"`` formats on the device (two passes: per-line lengths,
+    prefix sum, each thread writes its line; ``mp_format_lengths`` / ``mp_format_trace_text``)
+    then writes the buffer; ``"auto"`` uses it when the planes are on the GPU."""
+    m = trace.model
+    if engine == "auto":
+        engine = "cuda" if (m is not None and trace.n_tokens and trace.planes.is_cuda) else "host"
+    if engine == "host":
+        return _write_trace_host(trace, path)
+    if engine != "cuda":
+        raise ConfigError(f"unknown write engine {engine!r}")
+    t = _lib.torch()
+    header = f"#moeplace-trace v1 L={m.L} E={m.E} K={m.K}\n".encode()
+    if trace.n_tokens == 0:
+        with open(path, "wb") as f:
+            f.write(header)
+        return
+    planes = trace.device_planes()
+    dev = planes.device
+    n = trace.n_tokens
+    cids = _lib.to_dev(trace.token_chunk_ids(), t.int64)
+    lens = t.empty(n, dtype=t.int64, device=dev)
+    sh = _lib.stream_handle()
+    _lib.call("mp_format_lengths", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
+              _lib.ptr(cids), _lib.ptr(lens), sh)
+    offs = (t.cumsum(lens, 0) - lens).contiguous()
+    total = int(lens.sum().item())
+    out = t.empty(total, dtype=t.uint8, device=dev)
+    _lib.call("mp_format_trace_text", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
+              _lib.ptr(cids), _lib.ptr(offs), _lib.ptr(out), sh)
+    host = t.empty(total, dtype=t.uint8, pin_memory=True)
+    host.copy_(out)
+    with open(path, "wb") as f:
+        f.write(header)
+        f.write(memoryview(host.numpy()))
+
+
+def _write_trace_host(trace: ActivationTrace, path) -> None:
+    """Host text writer (engine="host")."""
     m = trace.model
     with open(path, "w") as f:
         if m is None:

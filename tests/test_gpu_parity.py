@@ -500,3 +500,19 @@ def test_contract_tc_digit_paths():
     got = ev.contract_tc(cnt, pe).cpu().numpy()
     want = pe.cpu().numpy().astype(np.int64) @ cnt.cpu().numpy().T
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("shape", [R1, B16, (2, 4, 1), (1, 256, 3)])
+def test_device_writer_matches_host_writer(tmp_path, shape):
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 1234, 11, 3)
+    mt.write_trace(tr, tmp_path / "d.txt", engine="cuda")
+    mt.write_trace(tr, tmp_path / "h.txt", engine="host")
+    assert (tmp_path / "d.txt").read_bytes() == (tmp_path / "h.txt").read_bytes()
+    v = tr.view(2, 7)
+    mt.write_trace(v, tmp_path / "dv.txt", engine="cuda")
+    mt.write_trace(v, tmp_path / "hv.txt", engine="host")
+    assert (tmp_path / "dv.txt").read_bytes() == (tmp_path / "hv.txt").read_bytes()
+    back = mt.parse_trace(tmp_path / "d.txt")
+    assert np.array_equal(back.tokens(), tr.tokens())
