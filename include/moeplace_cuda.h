@@ -78,7 +78,7 @@ int mp_validate_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begi
  *   ends[t]); parses "cid\t[layer]0:e,..,e\t...", writes planes[l][t*K + k] and chunk_ids[t].
  *   err[0] (caller sets INT64_MAX) = min over bad lines of t*16 + code (1 structure, 2 layer
  *   label, 3 id >= E, 4 id count, 5 duplicate id, 6 chunk id overflow).  The text buffer must
- *   be readable (padded) up to the 16-byte boundary after its last byte.  K <= 32.            */
+ *   be readable (padded) up to the 16-byte boundary after its last byte.                     */
 int mp_count_newlines(const uint8_t* text, int64_t n, int64_t* counts, void* stream);
 int mp_find_newlines(const uint8_t* text, int64_t n, const int64_t* offsets, int64_t* positions, void* stream);
 int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,

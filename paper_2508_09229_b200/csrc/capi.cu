@@ -230,7 +230,6 @@ int mp_find_newlines(const uint8_t* text, int64_t n, const int64_t* offsets, int
 int mp_parse_trace_text(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
                         int E, uint8_t* planes, int64_t plane_stride, int64_t* chunk_ids, int64_t* err, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
-  if (K > 32) return MP_ERR_UNSUPPORTED;
   if (!text || !ends || n_lines < 0 || first_start < 0 || !chunk_ids || !err || E <= 0) return MP_ERR_ARG;
   int r = check_trace(planes, plane_stride, 0, n_lines, L, K);
   if (r) return r;

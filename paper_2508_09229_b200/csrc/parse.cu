@@ -12,7 +12,7 @@
 //      K-byte records are stored coalesced) plus the chunk id per token.
 // Errors: err[0] = min over bad lines of (line_index * 16 + code) (caller initialises it to
 // INT64_MAX); codes: 1 structure, 2 layer label, 3 id >= E, 4 wrong id count, 5 duplicate id,
-// 6 chunk id overflow.
+// 6 chunk id overflow.  Any K <= E <= 256.
 #include "common.cuh"
 
 namespace mp {
@@ -90,8 +90,10 @@ __global__ void __launch_bounds__(256) parse_kernel(const uint8_t* __restrict__ 
     }
     if (!code && (nd == 0 || p >= end || rd.get(p) != '\t')) code = 1;
     ++p;
-    uint32_t ids[32];
+    uint32_t ids[8];
     for (int l = 0; l < L && !code; ++l) {
+      uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 256-bit set of this record's ids
+      uint8_t* out = planes + (int64_t)l * stride + t * K;
       if (p < end && rd.get(p) == 'l') {  // optional "layer" prefix
         const char* lit = "layer";
         for (int i = 0; i < 5 && !code; ++i, ++p)
@@ -124,10 +126,10 @@ __global__ void __launch_bounds__(256) parse_kernel(const uint8_t* __restrict__ 
         }
         if (nd == 0) { code = 4; break; }
         if (v >= (uint32_t)E) { code = 3; break; }
-        for (int j = 0; j < k; ++j)
-          if (ids[j] == v) code = 5;
-        if (code) break;
-        ids[k] = v;
+        if (seen[v >> 5] & (1u << (v & 31))) { code = 5; break; }
+        seen[v >> 5] |= 1u << (v & 31);
+        if (K == 8) ids[k] = v;
+        else out[k] = (uint8_t)v;
         const uint32_t ch = p < end ? rd.get(p) : '\n';
         const bool last_k = k == K - 1;
         if (!last_k) {
@@ -140,14 +142,11 @@ __global__ void __launch_bounds__(256) parse_kernel(const uint8_t* __restrict__ 
         ++p;
       }
       if (code) break;
-      uint8_t* out = planes + (int64_t)l * stride + t * K;
-      if (K == 8) {
+      if (K == 8) {  // one coalesced 8-byte store per record
         uint2 w;
         w.x = ids[0] | (ids[1] << 8) | (ids[2] << 16) | (ids[3] << 24);
         w.y = ids[4] | (ids[5] << 8) | (ids[6] << 16) | (ids[7] << 24);
         *reinterpret_cast<uint2*>(out) = w;
-      } else {
-        for (int k = 0; k < K; ++k) out[k] = (uint8_t)ids[k];
       }
     }
     if (code) {

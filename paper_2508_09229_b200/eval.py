@@ -88,10 +88,8 @@ def _as_costs(costs, n: int) -> list[CostMatrix]:
     return costs
 
 
-def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec, W: int):
-    """Pack one group (<= 4W placements) into device tables uint32 [L, 256, W]."""
-    t = _lib.torch()
-    dev = _lib.require_cuda()
+def _unique_costs(costs: Sequence[CostMatrix]):
+    """Distinct cost matrices (by identity) and, per placement, the index of its matrix."""
     uniq: list[CostMatrix] = []
     topo_of = []
     for c in costs:
@@ -102,6 +100,14 @@ def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], 
         else:
             uniq.append(c)
             topo_of.append(len(uniq) - 1)
+    return uniq, topo_of
+
+
+def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec, W: int):
+    """Pack one group (<= 4W placements) into device tables uint32 [L, 256, W]."""
+    t = _lib.torch()
+    dev = _lib.require_cuda()
+    uniq, topo_of = _unique_costs(costs)
     S = uniq[0].S
     for c in uniq:
         if c.S != S or c.L != model.L:
@@ -317,16 +323,7 @@ def evaluate_dedup(trace: ActivationTrace, placements: Sequence[Placement], cost
             if c.dist is None or c.attn is None:
                 raise ConfigError("evaluate_dedup needs cost matrices built by cost_matrix(dist, attn)")
         tables, max_p = _group_tables(grp, gcost, m, 1)
-        uniq: list = []
-        topo_of = []
-        for c in gcost:
-            for i, u in enumerate(uniq):
-                if u is c:
-                    topo_of.append(i)
-                    break
-            else:
-                uniq.append(c)
-                topo_of.append(len(uniq) - 1)
+        uniq, topo_of = _unique_costs(gcost)
         S = uniq[0].S
         server_of = _lib.to_dev(np.stack([c.dist.graph.device_server for c in uniq]).astype(np.int32), t.int32)
         d_assign = _lib.to_dev(np.stack([p.assign for p in grp]), t.int32)

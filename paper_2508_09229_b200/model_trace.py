@@ -321,8 +321,8 @@ def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
         model = ModelSpec(int(m.group(1)), int(m.group(2)), int(m.group(3)))
     except ConfigError as e:
         raise TraceParseError(str(e), 1) from None
-    if model.E > MAX_EXPERTS or model.K > 32:
-        raise ConfigError(f"E = {model.E} / K = {model.K} outside the device format (E <= 256, K <= 32)")
+    if model.E > MAX_EXPERTS:
+        raise ConfigError(f"E = {model.E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
     if head_end < 0:
         head_end = n
     L, K = model.L, model.K
@@ -504,6 +504,11 @@ def validate_trace(trace: ActivationTrace) -> None:
 
 # ---- statistics -----------------------------------------------------------
 
+def C_void(addr: int):
+    import ctypes
+    return ctypes.c_void_p(addr)
+
+
 STREAM_BLOCK_TOKENS = 1 << 20  # host-streaming slice (R1: 464 MB per slice)
 
 
@@ -559,11 +564,6 @@ def sweep(trace: ActivationTrace, launch) -> None:
         free[j].record(comp)
     trace._validated = True
     comp.wait_stream(copy)
-
-
-def C_void(addr: int):
-    import ctypes
-    return ctypes.c_void_p(addr)
 
 
 def trace_counts(trace: ActivationTrace):

@@ -516,3 +516,34 @@ def test_device_writer_matches_host_writer(tmp_path, shape):
     assert (tmp_path / "dv.txt").read_bytes() == (tmp_path / "hv.txt").read_bytes()
     back = mt.parse_trace(tmp_path / "d.txt")
     assert np.array_equal(back.tokens(), tr.tokens())
+
+
+@pytest.mark.parametrize("shape", [(3, 64, 16), (2, 256, 32), (4, 1, 1), (1, 33, 33)])
+def test_wide_k_and_degenerate_shapes(tmp_path, shape):
+    """K = 16 / 32 (generic generator, byte paths), E = 1, K = E: generator, histogram, score,
+    fused pass, dedup, per-token hops, parser and writer all agree with the oracle."""
+    import torch
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    N, C = 777, 5
+    tr = mt.generate_trace(m, 1.2, N, C, 2)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 2)
+    assert np.array_equal(tr.tokens(), sel)
+    assert np.array_equal(mt.estimate_frequencies(tr, m).counts, ost.counts(sel, E))
+    rng = np.random.default_rng(9)
+    S = 8
+    p = rng.integers(0, 7, (L, S)).astype(np.uint8)
+    cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(5)]
+    got = ev.score_sums(tr, pls, cost)
+    for i, pl in enumerate(pls):
+        assert np.array_equal(got[i], oracle_sums(sel, p, pl.assign, bounds))
+    f, reps = ev.evaluate_with_stats(tr, pls[:4], cost)
+    assert np.array_equal(f.counts, ost.counts(sel, E))
+    assert [r.chunk_hop_sums for r in reps] == [got[i].tolist() for i in range(4)]
+    th = ev.token_hops_all(tr, pls[:2], cost)
+    for i in range(2):
+        assert np.array_equal(th[i], oe.per_token_hops(sel, oe.pe_table(p, pls[i].assign)))
+    assert np.array_equal(ev.score_sums_factorized(tr, pls, cost), got)
+    mt.write_trace(tr, tmp_path / "t.txt")
+    assert np.array_equal(mt.parse_trace(tmp_path / "t.txt").tokens(), sel)
