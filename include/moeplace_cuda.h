@@ -130,9 +130,10 @@ int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, 
 
 /* ---- per-token hops for every token: token_hops over the whole trace -----
  * hops[q*n + i] = sum_l sum_k pe_q[l][planes[l][(tok_begin+i)*K + k]] for q < 4 (W = 1 tables),
- * n = tok_end - tok_begin, uint32 output (fully written).  Requires L*K*max_p <= 65535.        */
+ * n = tok_end - tok_begin, uint32 output (fully written).  Requires L*K*max_p <= 65535.
+ * scratch: device uint32 [L][256][32] (the lane-replicated tables, 32 KB per layer).           */
 int mp_token_hops_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
-                     const uint32_t* tables, int max_p, uint32_t* hops, void* stream);
+                     const uint32_t* tables, int max_p, uint32_t* scratch, uint32_t* hops, void* stream);
 
 /* ---- fused statistics + traffic pass (one read of the trace) -----------------------------
  * mp_hist_u8 and mp_score_u8 over the same token range in one kernel (W = 1 only).           */

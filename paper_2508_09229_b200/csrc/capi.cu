@@ -33,7 +33,8 @@ cudaError_t launch_find_nl(const uint8_t* text, int64_t n, const int64_t* offset
 cudaError_t launch_parse(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
                          int E, uint8_t* planes, int64_t stride, int64_t* chunk_ids, int64_t* err, cudaStream_t s);
 cudaError_t launch_token_hops(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
-                              const uint32_t* tables, int max_p, uint32_t* hops, cudaStream_t s);
+                              const uint32_t* tables, int max_p, uint32_t* replicated, uint32_t* hops,
+                              cudaStream_t s);
 cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                                const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s);
 cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out,
@@ -137,13 +138,14 @@ int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, 
 }
 
 int mp_token_hops_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
-                     const uint32_t* tables, int max_p, uint32_t* hops, void* stream) {
+                     const uint32_t* tables, int max_p, uint32_t* scratch, uint32_t* hops, void* stream) {
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
-  if (!tables || !hops || max_p < 0) return MP_ERR_ARG;
+  if (!tables || !hops || !scratch || max_p < 0) return MP_ERR_ARG;
   if ((int64_t)L * K * max_p > 65535 || max_p > 255) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;
-  return status(mp::launch_token_hops(planes, plane_stride, tok_begin, tok_end, L, K, tables, max_p, hops, S(stream)));
+  return status(mp::launch_token_hops(planes, plane_stride, tok_begin, tok_end, L, K, tables, max_p, scratch, hops,
+                                      S(stream)));
 }
 
 int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,

@@ -18,6 +18,40 @@ namespace mp {
 
 constexpr int kDedupMaxK = 32;
 
+// 0x80 in every byte where a == b (exact per byte, no borrow between lanes)
+__device__ __forceinline__ uint32_t bytes_eq(uint32_t a, uint32_t b) {
+  const uint32_t x = a ^ b;
+  const uint32_t t = (x & 0x7f7f7f7fu) + 0x7f7f7f7fu;
+  return ~(t | x | 0x7f7f7f7fu);
+}
+
+// K = 8 record, all 4 placements at once (byte lanes): SPEC hops and dedup hops widened into u16
+// lanes ({q0,q2}, {q1,q3}), unique remote destination servers as u8 lanes (<= 8 per record).
+__device__ __forceinline__ void dedup_record8(uint2 v, uint32_t base, uint32_t slot, uint32_t src4,
+                                              uint32_t (&hop16)[2], uint32_t& uq8, uint32_t (&dd16)[2]) {
+  const uint32_t wv[2] = {v.x, v.y};
+  uint32_t sw[8], pw[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t a = base + prmt(wv[k >> 2], slot, sel_row(k & 3));
+    pw[k] = lds32(a);
+    sw[k] = lds32(a + 128);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t seen = 0;
+#pragma unroll
+    for (int j = 0; j < k; ++j) seen |= bytes_eq(sw[k], sw[j]);
+    const uint32_t first = ~seen & 0x80808080u;   // 0x80 where the pick's server is new in the record
+    const uint32_t m = pw[k] & ((first >> 7) * 0xffu);
+    hop16[0] += pw[k] & 0x00ff00ffu;
+    hop16[1] += (pw[k] >> 8) & 0x00ff00ffu;
+    dd16[0] += m & 0x00ff00ffu;
+    dd16[1] += (m >> 8) & 0x00ff00ffu;
+    uq8 += (first & ~bytes_eq(sw[k], src4)) >> 7;  // +1 per lane: new server, not the source
+  }
+}
+
 __global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0,
                                                     int64_t t1, int L, int K, const int64_t* __restrict__ bounds,
                                                     int C, const uint32_t* __restrict__ tables,
@@ -68,15 +102,29 @@ __global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ 
       while (cend <= t && c + 1 < C) cend = __ldg(bounds + (++c) + 1);
       const int64_t te = min(r1, cend);
       uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};
+      if (K == 8) {
+        // SIMD-within-a-register path; lane sums are widened every 32 records (u16: 32*8*255 < 2^16)
+        uint32_t h16[2] = {0, 0}, d16[2] = {0, 0}, u8 = 0;
+        int cnt = 0;
+        for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
+          dedup_record8(__ldg(reinterpret_cast<const uint2*>(plane + r * 8)), base, slot, src, h16, u8, d16);
+          if (++cnt == 31) {
+            hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
+            dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
+            h16[0] = h16[1] = d16[0] = d16[1] = u8 = 0;
+            cnt = 0;
+          }
+        }
+        hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
+        dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
+      } else
       for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
         uint32_t ids[kDedupMaxK];
-        if (K == 8) {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(plane + r * 8));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) { ids[k] = (v.x >> (8 * k)) & 0xffu; ids[k + 4] = (v.y >> (8 * k)) & 0xffu; }
-        } else {
-          for (int k = 0; k < K; ++k) ids[k] = plane[r * K + k];
-        }
+        for (int k = 0; k < K; ++k) ids[k] = plane[r * K + k];
         uint32_t srvw[kDedupMaxK];
         for (int k = 0; k < K; ++k) {
           const uint32_t a = base + ((ids[k] << 8) | slot);

@@ -1,48 +1,76 @@
 // Per-token hop totals for every token (SPEC.md:336-344 token_hops, applied to the whole trace):
 //   hops[q*N + i] = sum_l sum_k pe_q[l][planes[l][(t0+i)*K + k]]      (q < 4, uint32 out)
 // Layer-major planes need a cross-layer sum per token, so this kernel is token-tiled: a CTA owns
-// a tile of TPT*blockDim tokens, walks the L layers, stages each layer's replicated W=1 table in
-// shared memory (row = expert, slot = lane*4: conflict-free LDS.32 via one PRMT), and keeps each
-// token's four placement sums in registers as u16 lanes until the end of the tile.
+// a tile of TPT*blockDim tokens and walks the L layers, keeping each token's four placement sums
+// in registers as u16 lanes.  Each layer's W=1 table is staged in shared memory replicated per
+// lane (row = expert, slot = lane*4: conflict-free LDS.32 via one PRMT); the replicated tables
+// are expanded once into global memory (32 KB per layer, L2-resident) and streamed into a
+// double buffer with cp.async, so layer l+1's table lands while layer l is being gathered and
+// each layer costs one barrier.
 #include "common.cuh"
 
 namespace mp {
 
-constexpr int kTokThreads = 256;
-constexpr int kTPT = 8;  // tokens per thread per tile
+constexpr int kTokThreads = 512;
+constexpr int kTPT = 8;                   // tokens per thread per tile -> 4096-token tiles
+constexpr int kRowBytes = 128;            // 32 lanes x 4 B
+constexpr int kTabBytes = 256 * kRowBytes;  // 32 KB per layer
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// replicated[l][e][r] = tables[l][e] for r < 32 (one-time expansion, 32 KB per layer)
+__global__ void replicate_kernel(const uint32_t* __restrict__ tables, int L, uint32_t* __restrict__ rep) {
+  const int64_t n = (int64_t)L * 256 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    rep[i] = tables[i >> 5];
+}
 
 template <bool K8, bool SMALLP>
 __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* __restrict__ planes, int64_t stride,
                                                                  int64_t t0, int64_t n, int L, int K,
-                                                                 const uint32_t* __restrict__ tables,
+                                                                 const uint32_t* __restrict__ rep,
                                                                  uint32_t* __restrict__ hops) {
-  extern __shared__ __align__(128) uint8_t sm[];  // 256 rows x 128 B
-  uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
+  extern __shared__ __align__(128) uint8_t sm[];  // 2 x (256 rows x 128 B)
   const int lane = threadIdx.x & 31;
-  const uint32_t base = smem_addr(sm);
-  const uint32_t slot8 = (uint32_t)(lane << 3);  // PRMT yields (e << 8) | (lane << 3); >> 1 -> row e*128 + lane*4
+  const uint32_t base0 = smem_addr(sm);
+  const uint32_t slot8 = (uint32_t)(lane << 3);  // PRMT -> (e << 8) | (lane << 3); >> 1 -> e*128 + lane*4
   const uint32_t slot = (uint32_t)(lane << 2);
   const int64_t tile = (int64_t)kTPT * blockDim.x;
+  auto fetch = [&](int l, int buf) {  // async copy of layer l's replicated table into buffer buf
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(rep) + (int64_t)l * kTabBytes;
+    for (int i = threadIdx.x; i < kTabBytes / 16; i += blockDim.x)
+      cp_async16(base0 + buf * kTabBytes + i * 16, src + i * 16);
+    cp_async_commit();
+  };
   for (int64_t ta = (int64_t)blockIdx.x * tile; ta < n; ta += (int64_t)gridDim.x * tile) {
     uint32_t acc[kTPT][2];  // per token: u16 lanes {q0, q2} and {q1, q3}
 #pragma unroll
     for (int j = 0; j < kTPT; ++j) acc[j][0] = acc[j][1] = 0;
+    __syncthreads();  // previous tile done with both buffers
+    fetch(0, 0);
     for (int l = 0; l < L; ++l) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x)
-        smw[(i >> 5) * 32 + (i & 31)] = __ldg(tables + (int64_t)l * 256 + (i >> 5));
-      __syncthreads();
+      cp_async_wait_all();
+      __syncthreads();  // layer l's table visible; buffer (l+1)&1 free
+      if (l + 1 < L) fetch(l + 1, (l + 1) & 1);
+      const uint32_t base = base0 + (l & 1) * kTabBytes;
       const uint8_t* plane = planes + (int64_t)l * stride + (t0 + ta) * K;
+      if constexpr (K8) {
+        uint2 v[kTPT];
 #pragma unroll
-      for (int j = 0; j < kTPT; ++j) {
-        const int64_t i = (int64_t)j * blockDim.x + threadIdx.x;  // token within tile (coalesced per j)
-        if (ta + i >= n) continue;
-        uint32_t s8 = 0;
-        if constexpr (K8) {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(plane + i * 8));
-          const uint32_t wv[2] = {v.x, v.y};
+        for (int j = 0; j < kTPT; ++j) {
+          const int64_t i = (int64_t)j * blockDim.x + threadIdx.x;
+          v[j] = (ta + i < n) ? __ldg(reinterpret_cast<const uint2*>(plane + i * 8)) : make_uint2(0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < kTPT; ++j) {
+          const uint32_t wv[2] = {v[j].x, v[j].y};
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            uint32_t s8 = 0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               const uint32_t w = lds32(base + (prmt(wv[h], slot8, sel_row(b)) >> 1));
@@ -56,13 +84,17 @@ __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* 
             if constexpr (SMALLP) {
               acc[j][0] += s8 & 0x00ff00ffu;
               acc[j][1] += (s8 >> 8) & 0x00ff00ffu;
-              s8 = 0;
             }
           }
-        } else {
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kTPT; ++j) {
+          const int64_t i = (int64_t)j * blockDim.x + threadIdx.x;
+          if (ta + i >= n) continue;
           for (int k = 0; k < K; ++k) {
             const uint32_t e = plane[i * K + k];
-            const uint32_t w = lds32(base + e * 128 + slot);
+            const uint32_t w = lds32(base + e * kRowBytes + slot);
             acc[j][0] += w & 0x00ff00ffu;
             acc[j][1] += (w >> 8) & 0x00ff00ffu;
           }
@@ -84,26 +116,29 @@ __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* 
 
 template <bool K8, bool SMALLP>
 static void run_token_hops(int64_t tiles, int nsm, const uint8_t* planes, int64_t stride, int64_t t0, int64_t n,
-                           int L, int K, const uint32_t* tables, uint32_t* hops, cudaStream_t s) {
-  const int smem = 256 * 128;
+                           int L, int K, const uint32_t* rep, uint32_t* hops, cudaStream_t s) {
+  const int smem = 2 * kTabBytes;
   int per_sm = 0;
   cudaFuncSetAttribute(token_hops_kernel<K8, SMALLP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, token_hops_kernel<K8, SMALLP>, kTokThreads, smem);
   const int64_t grid = max((int64_t)1, min(tiles, (int64_t)nsm * max(1, per_sm)));
-  token_hops_kernel<K8, SMALLP><<<(unsigned)grid, kTokThreads, smem, s>>>(planes, stride, t0, n, L, K, tables, hops);
+  token_hops_kernel<K8, SMALLP><<<(unsigned)grid, kTokThreads, smem, s>>>(planes, stride, t0, n, L, K, rep, hops);
 }
 
 cudaError_t launch_token_hops(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
-                              const uint32_t* tables, int max_p, uint32_t* hops, cudaStream_t s) {
+                              const uint32_t* tables, int max_p, uint32_t* replicated, uint32_t* hops,
+                              cudaStream_t s) {
   const int64_t n = t1 - t0;
   if (n <= 0) return cudaSuccess;
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nrep = (int64_t)L * 256 * 32;
+  replicate_kernel<<<(unsigned)min((nrep + 255) / 256, (int64_t)4096), 256, 0, s>>>(tables, L, replicated);
   const int64_t tiles = (n + (int64_t)kTPT * kTokThreads - 1) / ((int64_t)kTPT * kTokThreads);
-  if (K == 8 && max_p <= 63) run_token_hops<true, true>(tiles, nsm, planes, stride, t0, n, L, K, tables, hops, s);
-  else if (K == 8) run_token_hops<true, false>(tiles, nsm, planes, stride, t0, n, L, K, tables, hops, s);
-  else run_token_hops<false, false>(tiles, nsm, planes, stride, t0, n, L, K, tables, hops, s);
+  if (K == 8 && max_p <= 63) run_token_hops<true, true>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
+  else if (K == 8) run_token_hops<true, false>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
+  else run_token_hops<false, false>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
   return cudaGetLastError();
 }
 

@@ -372,8 +372,9 @@ def token_hops_all(trace: ActivationTrace, placements: Sequence[Placement], cost
         grp = placements[g0:g0 + 4]
         tables, max_p = _group_tables(grp, costs[g0:g0 + 4], m, 1)
         hops = t.empty((4, n), dtype=t.int32, device=planes.device)
+        scratch = t.empty((m.L, 256, 32), dtype=t.int32, device=planes.device)
         _lib.call("mp_token_hops_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
-                  _lib.ptr(tables), max_p, _lib.ptr(hops), _lib.stream_handle())
+                  _lib.ptr(tables), max_p, _lib.ptr(scratch), _lib.ptr(hops), _lib.stream_handle())
         out[g0:g0 + len(grp)] = hops[:len(grp)].cpu().numpy().astype(np.int64)
     return out
 

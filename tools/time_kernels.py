@@ -55,21 +55,68 @@ def run(w):
                   _lib.ptr(s), sh)
 
 
+hops_out = torch.empty((4, a.tokens), dtype=torch.int32, device="cuda")
+rep_scratch = torch.empty((L, 256, 32), dtype=torch.int32, device="cuda")
+cc = torch.zeros((C, L * E), dtype=torch.int64, device="cuda")
+srv_t = torch.empty((L, 256), dtype=torch.int32, device="cuda")
+_lib.call("mp_pack_server_tables", _lib.ptr(_lib.to_dev(g.device_server[None].astype("int32"), torch.int32)), 1,
+          _lib.ptr(_lib.to_dev(__import__("numpy").stack([p.assign for p in pls[:4]]), torch.int32)),
+          _lib.ptr(torch.zeros(4, dtype=torch.int32, device="cuda")), 4, L, E, g.n_devices, _lib.ptr(srv_t),
+          _lib.ptr(err), sh)
+src = _lib.to_dev(__import__("numpy").tile(g.device_server[attn.dispatch].astype("uint8"), (4, 1)), torch.uint8)
+dd = torch.zeros((3, 4, C), dtype=torch.int64, device="cuda")
+
+
+def run_ext(w):
+    t1_, mp1_ = tabs[1]
+    if w == "token_hops":
+        _lib.call("mp_token_hops_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(t1_), mp1_, _lib.ptr(rep_scratch),
+                  _lib.ptr(hops_out), sh)
+    elif w == "hist_chunks":
+        _lib.call("mp_hist_chunks_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(cc),
+                  _lib.ptr(err), sh)
+    elif w == "dedup":
+        _lib.call("mp_score_dedup_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t1_),
+                  _lib.ptr(srv_t), _lib.ptr(src), _lib.ptr(dd[0]), _lib.ptr(dd[1]), _lib.ptr(dd[2]), sh)
+
+
 res = {}
 bytes_ = a.tokens * L * K
-for w in ("hist", "score1", "score2", "score4", "fused"):
+for w in ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup"):
+    fn = run if w in ("hist", "score1", "score2", "score4", "fused") else run_ext
     for _ in range(3):
-        run(w)
+        fn(w)
     ts = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        run(w)
+        fn(w)
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = float(np.mean(ts))
     res[w] = {"ms": ms, "min_ms": float(min(ts)), "GBps": bytes_ / ms / 1e6, "frac_6548": bytes_ / ms / 1e6 / 6548.2}
     print(f"{w:8s} {ms:7.3f} ms (min {min(ts):.3f})  {bytes_ / ms / 1e6:8.1f} GB/s  {100 * bytes_ / ms / 1e6 / 6548.2:5.1f}%")
+# device text IO at 1M tokens (text ~2.1 KB per R1 token)
+import tempfile, time  # noqa: E401,E402
+sub = tr.view(0, 15)  # first 15 chunks (~1M tokens)
+with tempfile.TemporaryDirectory() as d:
+    f = os.path.join(d, "t.txt")
+    mt.write_trace(sub, f, engine="cuda")
+    torch.cuda.synchronize()
+    t_a = time.perf_counter()
+    mt.write_trace(sub, f, engine="cuda")
+    t_w = time.perf_counter() - t_a
+    size = os.path.getsize(f)
+    mt.parse_trace(f)
+    torch.cuda.synchronize()
+    t_a = time.perf_counter()
+    back = mt.parse_trace(f)
+    torch.cuda.synchronize()
+    t_p = time.perf_counter() - t_a
+    ok = bool((back.tokens()[:1000] == sub.tokens()[:1000]).all())
+res["io"] = {"tokens": sub.n_tokens, "text_bytes": size, "write_s": t_w, "parse_s": t_p, "roundtrip_ok": ok,
+             "write_GBps": size / t_w / 1e9, "parse_GBps": size / t_p / 1e9}
+print("io", res["io"])
 if a.out:
     json.dump(res, open(a.out, "w"), indent=1)
