@@ -38,15 +38,28 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every kernel for sm_100a (-lineinfo) plus the host solver into one .so."""
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path = None) -> Path:
+    """Compile every kernel for sm_100a (-lineinfo) plus the host solver into one .so.
+    ``defines``/``out`` build an experimental variant (e.g. MP_PF_AHEAD=0) next to the product lib."""
+    global LIB
+    product = LIB
+    if out is not None:
+        LIB = Path(out)
+    try:
+        return _build(force or out is not None, verbose, list(defines))
+    finally:
+        LIB = product
+
+
+def _build(force: bool, verbose: bool, defines: list) -> Path:
     if not force and not _stale():
         return LIB
     nvcc = _nvcc()
     LIBDIR.mkdir(exist_ok=True)
-    objdir = LIBDIR / "obj"
+    objdir = LIBDIR / ("obj" if not defines else "obj_" + "_".join(d.replace("=", "") for d in defines))
     objdir.mkdir(exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
+    common += ["-D" + d for d in defines]
     objs = []
     jobs = []
     for src in CU_SOURCES:

@@ -59,6 +59,12 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
+// Bulk L2 prefetch of [p, p + bytes) (bytes a multiple of 16, p 16-byte aligned): raises the
+// number of DRAM requests in flight without spending registers on them.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Warp reduce-scatter of P per-lane values (P = 4, 8, 16): after log2(P) halving exchanges at
 // offsets 16, 8, ... every lane holds one value index q, then the remaining offsets finish the
 // warp sum.  Cost: P - 1 + log2(32 / P) SHFLs instead of P * 5.  Lanes with

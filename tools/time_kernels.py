@@ -20,7 +20,12 @@ ap.add_argument("--tokens", type=int, default=10_000_000)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--s", type=float, default=1.2)
 ap.add_argument("--out")
+ap.add_argument("--lib", help="load this libmoeplace_cuda.so variant instead of the product build")
+ap.add_argument("--only", default="")
 a = ap.parse_args()
+if a.lib:
+    from pathlib import Path
+    _lib.LIB_PATH = Path(a.lib)
 L, E, K = 58, 256, 8
 m = mt.ModelSpec(L, E, K)
 g = topo.build_topology(topo.TopologySpec("FatTree", 8, 4, 8, {"spines": 4}))
@@ -82,7 +87,7 @@ def run_ext(w):
 
 res = {}
 bytes_ = a.tokens * L * K
-for w in ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup"):
+for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup")):
     fn = run if w in ("hist", "score1", "score2", "score4", "fused") else run_ext
     for _ in range(3):
         fn(w)
@@ -97,6 +102,10 @@ for w in ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chu
     ms = float(np.mean(ts))
     res[w] = {"ms": ms, "min_ms": float(min(ts)), "GBps": bytes_ / ms / 1e6, "frac_6548": bytes_ / ms / 1e6 / 6548.2}
     print(f"{w:8s} {ms:7.3f} ms (min {min(ts):.3f})  {bytes_ / ms / 1e6:8.1f} GB/s  {100 * bytes_ / ms / 1e6 / 6548.2:5.1f}%")
+if a.only:
+    if a.out:
+        json.dump(res, open(a.out, "w"), indent=1)
+    sys.exit(0)
 # device text IO at 1M tokens (text ~2.1 KB per R1 token)
 import tempfile, time  # noqa: E401,E402
 sub = tr.view(0, 15)  # first 15 chunks (~1M tokens)
