@@ -422,6 +422,31 @@ def main():
         wf = lookups / 32 * 4 * 4 / 4 + n * L * K / 512 * 4  # per launch group of 16 placements
         roofline["smem_bound_ms_per_launch"] = wf / 148 / (mhz * 1e6) * 1e3
 
+    # ---------------- each streaming kernel alone on the same trace (context for the roofline) ----------
+    kernels_alone = None
+    if wl in (2, 5) and rank == 0:
+        scratch = torch.zeros_like(buf)
+        alone = {
+            "mp_score_u8 (W=1, 4 placements)": lambda: _lib.call(
+                "mp_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C,
+                _lib.ptr(groups[0][1]), 1, groups[0][2], _lib.ptr(scratch[L * E:]), sh),
+            "mp_hist_u8": lambda: _lib.call(
+                "mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(scratch[:L * E]), _lib.ptr(err), sh),
+        }
+        kernels_alone = {}
+        for nm, fn in alone.items():
+            for _ in range(3):
+                fn()
+            xa, xb = _events()
+            xa.record(stream)
+            for _ in range(10):
+                fn()
+            xb.record(stream)
+            torch.cuda.synchronize()
+            kms_ = xa.elapsed_time(xb) / 10
+            gbs = n * L * K / (kms_ / 1e3) / 1e9
+            kernels_alone[nm] = {"ms": kms_, "GBps": gbs, "frac": gbs / peak}
+
     # ---------------- config 4: the factorized evaluator beside the measured gather ----------------
     factorized = None
     if wl == 4:
@@ -541,6 +566,7 @@ def main():
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
                 "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "factorized": factorized,
+                "kernels_alone": kernels_alone,
                 "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
         emit(line)
     if world > 1:

@@ -1,0 +1,111 @@
+"""Property tests of the device path (SPEC.md invariants) over random shapes with
+hypothesis: every property is checked on the GPU engine's integers/floats."""
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+import moeplace.eval as ev
+import moeplace.model_trace as mt
+import moeplace.placement as mpl
+
+from helpers import random_assign
+
+pytestmark = pytest.mark.gpu
+
+SETTINGS = dict(max_examples=12, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+
+
+@st.composite
+def case(draw):
+    L = draw(st.integers(1, 6))
+    E = draw(st.sampled_from([2, 5, 16, 64, 256]))
+    K = draw(st.integers(1, min(E, 9)))
+    N = draw(st.integers(1, 700))
+    C = draw(st.integers(1, 12))
+    seed = draw(st.integers(0, 2 ** 31))
+    s = draw(st.sampled_from([0.0, 1.2, 2.0]))
+    return L, E, K, N, C, seed, s
+
+
+def _cost(rng, L, S, hi=9):
+    import torch
+    p = rng.integers(0, hi + 1, (L, S)).astype(np.uint8)
+    return mpl.CostMatrix(torch.as_tensor(p, device="cuda")), p
+
+
+@settings(**SETTINGS)
+@given(case())
+def test_permutation_within_chunks_and_duplication(c):
+    """SPEC.md:382 (permutation within chunks) and SPEC.md:352 (duplicating every token)."""
+    L, E, K, N, C, seed, s = c
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, s, N, C, seed)
+    sel = tr.tokens()
+    lab = tr.token_chunk_ids()
+    rng = np.random.default_rng(seed % 1000)
+    cost, p = _cost(rng, L, 8)
+    pl = mpl.Placement(random_assign(rng, L, E, 8))
+    base = ev.evaluate(tr, pl, cost)
+    perm = rng.permutation(N)  # from_tokens regroups stably by chunk: a within-chunk shuffle
+    shuffled = mt.ActivationTrace.from_tokens(m, sel[perm], lab[perm])
+    r2 = ev.evaluate(shuffled, pl, cost)
+    nonempty = [x for x, n in zip(base.chunk_hop_sums, tr.chunk_token_counts()) if n > 0]
+    assert r2.chunk_hop_sums == nonempty
+    assert r2.mean_hops_per_token == base.mean_hops_per_token
+    dup = mt.ActivationTrace.from_tokens(m, np.concatenate([sel, sel]), np.concatenate([lab, lab]))
+    r3 = ev.evaluate(dup, pl, cost)
+    assert r3.mean_hops_per_token == base.mean_hops_per_token
+    assert r3.chunk_hop_sums == [2 * x for x in nonempty]
+
+
+@settings(**SETTINGS)
+@given(case())
+def test_frequency_invariants(c):
+    """rows sum to 1; estimate of a concatenation = count-weighted average."""
+    L, E, K, N, C, seed, s = c
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, s, N, C, seed)
+    f = mt.estimate_frequencies(tr, m)
+    assert np.allclose(f.f.sum(axis=1), 1.0, atol=1e-9)
+    if C >= 2 and tr.chunk_bounds[1] > 0 and tr.chunk_bounds[1] < N:
+        a, b = tr.view(0, 1), tr.view(1, C)
+        fa, fb = mt.estimate_frequencies(a, m), mt.estimate_frequencies(b, m)
+        w = (fa.f * a.n_tokens + fb.f * b.n_tokens) / N
+        assert np.allclose(w, f.f, rtol=0, atol=1e-12)
+        assert np.array_equal(fa.counts + fb.counts, f.counts)
+
+
+@settings(**SETTINGS)
+@given(case())
+def test_metric_objective_identity(c):
+    """SPEC.md:383 / acceptance #2: evaluate(train).mean == K * objective_value(f_train) (1e-6),
+    and the integer form sum(counts * pe) == hop_sum exactly."""
+    L, E, K, N, C, seed, s = c
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, s, N, C, seed)
+    rng = np.random.default_rng(seed % 977)
+    cost, p = _cost(rng, L, 16, hi=30)
+    pl = mpl.Placement(random_assign(rng, L, E, 16))
+    rep = ev.evaluate(tr, pl, cost)
+    f = mt.estimate_frequencies(tr, m)
+    obj = ev.objective_value(pl, f, cost)
+    assert abs(rep.mean_hops_per_token - K * obj) <= 1e-6 * max(1.0, rep.mean_hops_per_token)
+    pe = p.astype(np.int64)[np.arange(L)[:, None], pl.assign]
+    assert int((f.counts * pe).sum()) == rep.hop_sum
+    assert np.array_equal(ev.token_hops_all(tr, [pl], cost)[0].sum(), rep.hop_sum)
+
+
+@settings(max_examples=6, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(0, 2 ** 31), st.sampled_from(["FatTree", "FatTreeHier", "Dragonfly", "DragonflySparse"]))
+def test_commmap_mass_equals_mean(seed, kind):
+    """CommMap total mass == evaluate mean; symmetric, zero diagonal."""
+    from helpers import setup_topology
+    m = mt.ModelSpec(5, 32, 3)
+    g, dist, order, attn, cost = setup_topology(kind, 4, 2, 2, m)
+    tr = mt.generate_trace(m, 1.2, 900, 6, seed)
+    pl = mpl.Placement(random_assign(np.random.default_rng(seed % 101), 5, 32, g.n_devices))
+    cm = ev.communication_map(tr, pl, cost)
+    rep = ev.evaluate(tr, pl, cost)
+    assert abs(cm.traffic.sum() - rep.mean_hops_per_token) <= 1e-9 * max(1.0, rep.mean_hops_per_token)
+    assert np.allclose(cm.traffic, cm.traffic.T) and (np.diag(cm.traffic) == 0).all()
