@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 from .errors import ConfigError, InfeasibleError, MoeplaceError, exit_code
-from .eval import communication_map, evaluate_many, evaluate_with_stats, gain, objective_value
+from .eval import communication_map, evaluate_many, gain, objective_value, report_from_sums, score_sums
 from .model_trace import (ModelSpec, default_attention_placement, estimate_frequencies, generate_trace,
                           parse_trace, split_trace, trace_stats, write_trace)
 from .placement import (Constraints, cost_matrix, place_greedy, place_round_robin, read_placement, validate,
@@ -180,8 +180,13 @@ def run_experiment(cfg: ExperimentConfig) -> dict:
         _atomic_write(d / "topology.json", lambda p: Path(p).write_text(json.dumps(g.to_json())))
         _atomic_write(d / "distance.csv", dist.to_csv)
         methods = list(placements)
-        reports = evaluate_many(test, [placements[m] for m in methods], cost)
-        train_reports = evaluate_many(train, [placements[m] for m in methods], cost)
+        # one pass over train + test chunks (they are contiguous): per-chunk sums, split after
+        n_tr, n_te = int(cfg.values["train_chunks"]), int(cfg.values["test_chunks"])
+        both = trace.view(0, n_tr + n_te)
+        sums = score_sums(both, [placements[m] for m in methods], cost)
+        tok = both.chunk_token_counts()
+        reports = [report_from_sums(sums[i, n_tr:], tok[n_tr:], m) for i, m in enumerate(methods)]
+        train_reports = [report_from_sums(sums[i, :n_tr], tok[:n_tr], m) for i, m in enumerate(methods)]
         res = {}
         for m, rep, trep in zip(methods, reports, train_reports):
             rep.label = m

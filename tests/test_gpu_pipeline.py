@@ -179,3 +179,22 @@ def test_placement_search_improves_and_keeps_constraints():
     assert ev.evaluate(tr, ilp, cost).mean_hops_per_token <= res.objective + 1e-9
     r2 = se.improve_placement(tr, ilp, cost, "mean+std", lam=2.0, iters=10, batch=256, seed=2)
     assert r2.history[-1] <= r2.history[0]
+
+
+def test_table2_setup_all_topologies(tmp_path):
+    """PAPER Table 2 / SPEC.md:415: 64 devices, 1 GPU per server, 1 server per leaf, 16B shape,
+    c_layer = 1, c_exp = 54, all 4 topologies and 4 methods in one run."""
+    cfg = {"model": "16b", "L": 27, "E": 64, "K": 6, "c_exp": 54, "c_layer": 1,
+           "topologies": ["FatTree", "FatTreeHier", "Dragonfly", "DragonflySparse"],
+           "num_leaf_switches": 64, "num_nodes_per_leaf": 1, "num_gpus_per_server": 1,
+           "zipf_s": 1.2, "n_tokens": 20000, "n_chunks": 150, "seed": 0, "train_chunks": 100, "test_chunks": 50,
+           "output_dir": str(tmp_path / "t2")}
+    res = cli.run_experiment(cfg)
+    rows = (tmp_path / "t2" / "comparison.csv").read_text().splitlines()
+    assert len(rows) == 1 + 16
+    for kind, per in res["results"].items():
+        assert (tmp_path / "t2" / kind / "distance.csv").exists()
+        for m, d in per.items():
+            tr, obj = d["train"].mean_hops_per_token, d["test"].objective_train
+            assert abs(tr - 6 * obj) <= 1e-6 * tr, (kind, m)  # acceptance #2 per topology
+        assert per["ilpload"]["test"].objective_train <= min(d["test"].objective_train for d in per.values()) + 1e-12
