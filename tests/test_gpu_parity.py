@@ -547,3 +547,33 @@ def test_wide_k_and_degenerate_shapes(tmp_path, shape):
     assert np.array_equal(ev.score_sums_factorized(tr, pls, cost), got)
     mt.write_trace(tr, tmp_path / "t.txt")
     assert np.array_equal(mt.parse_trace(tmp_path / "t.txt").tokens(), sel)
+
+
+@pytest.mark.parametrize("shape", [R1, B16, (3, 64, 5)])
+def test_poisoned_padding_is_never_read(shape):
+    """Guard band (compute-sanitizer is unavailable on this pool): plane bytes beyond the valid
+    tokens are filled with an out-of-range id; every kernel must ignore them (the histogram
+    range check would raise, sums would change)."""
+    import torch
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    N, C = 2001, 9
+    tr = mt.generate_trace(m, 1.2, N, C, 4)
+    stride = ((N * K + 15) // 16) * 16 + 4096
+    planes = torch.full((L, stride), 255 if E < 256 else 0, dtype=torch.uint8, device="cuda")
+    planes[:, :N * K] = tr.planes[:, :N * K]
+    poisoned = mt.ActivationTrace(m, planes, 0, N, tr.chunk_ids.copy(), tr.chunk_bounds.copy(), _validated=True)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 4)
+    assert np.array_equal(mt.estimate_frequencies(poisoned, m).counts, ost.counts(sel, E))
+    rng = np.random.default_rng(1)
+    S = 8
+    p = rng.integers(1, 9, (L, S)).astype(np.uint8)
+    cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(9)]
+    want = np.stack([oracle_sums(sel, p, pl.assign, bounds) for pl in pls])
+    assert np.array_equal(ev.score_sums(poisoned, pls, cost), want)
+    assert np.array_equal(ev.score_sums_factorized(poisoned, pls, cost), want)
+    f, reps = ev.evaluate_with_stats(poisoned, pls[:4], cost)
+    assert [r.chunk_hop_sums for r in reps] == want[:4].tolist()
+    th = ev.token_hops_all(poisoned, pls[:1], cost)[0]
+    assert np.array_equal(th, oe.per_token_hops(sel, oe.pe_table(p, pls[0].assign)))
