@@ -144,6 +144,33 @@ class ActivationTrace:
                                self.source_is_file, self._validated)
 
     @classmethod
+    def from_router_topk(cls, model: ModelSpec, topk_ids, chunk_bounds: Optional[Sequence[int]] = None,
+                         chunk_ids: Optional[Sequence[int]] = None) -> "ActivationTrace":
+        """Ingest router top-k indices that are already on the GPU (e.g. captured from a running
+        MoE model): ``topk_ids`` int tensor [N, L, K] in token order; tokens are grouped by chunk
+        via ``chunk_bounds`` (default: one chunk).  Narrowed to u8 and transposed to layer planes on
+        the device, then validated by ``mp_validate_u8`` (ids < E, K distinct per record)."""
+        t = _lib.torch()
+        dev = _lib.require_cuda()
+        if not isinstance(topk_ids, t.Tensor) or topk_ids.dim() != 3 or tuple(topk_ids.shape[1:]) != (model.L, model.K):
+            raise ConfigError(f"topk_ids must be a tensor [N, {model.L}, {model.K}]")
+        if model.E > MAX_EXPERTS:
+            raise ConfigError(f"E = {model.E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
+        ids = topk_ids.to(dev)
+        N = int(ids.shape[0])
+        if N and (int(ids.min()) < 0 or int(ids.max()) >= model.E):
+            raise MoeplaceError(f"router ids outside [0, {model.E})")
+        planes = t.zeros((model.L, _plane_stride(N, model.K)), dtype=t.uint8, device=dev)
+        planes[:, :N * model.K] = ids.to(t.uint8).permute(1, 0, 2).reshape(model.L, N * model.K)
+        b = np.array([0, N] if chunk_bounds is None else list(chunk_bounds), dtype=np.int64)
+        if b[0] != 0 or b[-1] != N or (np.diff(b) < 0).any():
+            raise ConfigError("chunk_bounds must ascend from 0 to N")
+        cid = np.arange(len(b) - 1, dtype=np.int64) if chunk_ids is None else np.asarray(chunk_ids, dtype=np.int64)
+        tr = cls(model, planes, 0, N, cid, b)
+        validate_trace(tr)
+        return tr
+
+    @classmethod
     def from_tokens(cls, model: ModelSpec, selections, chunk_of_token: Optional[Sequence[int]] = None,
                     device=None) -> "ActivationTrace":
         """Build a trace from token-major selections [N, L, K] and per-token chunk labels.

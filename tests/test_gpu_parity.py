@@ -577,3 +577,19 @@ def test_poisoned_padding_is_never_read(shape):
     assert [r.chunk_hop_sums for r in reps] == want[:4].tolist()
     th = ev.token_hops_all(poisoned, pls[:1], cost)[0]
     assert np.array_equal(th, oe.per_token_hops(sel, oe.pe_table(p, pls[0].assign)))
+
+
+def test_from_router_topk_device_ingestion():
+    import torch
+    m = mt.ModelSpec(5, 64, 6)
+    sel, bounds = og.generate(5, 64, 6, 1.2, 3000, 7, 5)
+    ids = torch.as_tensor(sel.astype(np.int64), device="cuda")
+    tr = mt.ActivationTrace.from_router_topk(m, ids, bounds)
+    assert np.array_equal(tr.tokens(), sel)
+    assert np.array_equal(mt.estimate_frequencies(tr, m).counts, ost.counts(sel, 64))
+    bad = ids.clone()
+    bad[7, 2, 1] = bad[7, 2, 0]  # duplicate id in one record
+    with pytest.raises(MoeplaceError):
+        mt.ActivationTrace.from_router_topk(m, bad, bounds)
+    with pytest.raises(MoeplaceError):
+        mt.ActivationTrace.from_router_topk(m, ids + 64, bounds)
