@@ -593,3 +593,19 @@ def test_from_router_topk_device_ingestion():
         mt.ActivationTrace.from_router_topk(m, bad, bounds)
     with pytest.raises(MoeplaceError):
         mt.ActivationTrace.from_router_topk(m, ids + 64, bounds)
+
+
+def test_binary_sidecar_roundtrip(tmp_path):
+    m = mt.ModelSpec(27, 64, 6)
+    tr = mt.generate_trace(m, 1.2, 5001, 13, 2)
+    v = tr.view(2, 11)
+    mt.write_trace_binary(v, tmp_path / "t.mptrace")
+    for dev in ("pinned", "cuda"):
+        b = mt.read_trace_binary(tmp_path / "t.mptrace", device=dev)
+        assert np.array_equal(b.tokens(), v.tokens())
+        assert np.array_equal(b.chunk_ids, v.chunk_ids)
+        assert np.array_equal(b.chunk_bounds, v.chunk_bounds - v.tok_begin)
+        assert np.array_equal(mt.estimate_frequencies(b, m).counts, mt.estimate_frequencies(v, m).counts)
+    (tmp_path / "bad").write_bytes(b"NOTATRACE" * 4)
+    with pytest.raises(TraceParseError):
+        mt.read_trace_binary(tmp_path / "bad")
