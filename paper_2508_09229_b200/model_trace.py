@@ -599,6 +599,8 @@ def sweep(trace: ActivationTrace, launch) -> None:
     kernel output is additive over token ranges).  Other host planes are uploaded once and cached.
     """
     t = _lib.torch()
+    if trace.n_tokens == 0:
+        return
     planes = trace.planes
     if planes.is_cuda or not planes.is_pinned():
         planes = trace.device_planes()
