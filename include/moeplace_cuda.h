@@ -178,7 +178,9 @@ int mp_cost_matrix(const uint8_t* dsrv, int n_srv, const int32_t* dev_server, in
  * f[l][e] = counts[l*E+e] / denom (float64; counts == NULL means uniform f = 1/E), then
  *   w[l][e][s] = f[l][e] * p[l][s]              (float64, nullable output)
  *   w_int[l][e][s] = rint(w[l][e][s] * scale)   (int64 round-half-even, nullable output)
- * in exactly numpy's operation order, so results are bit-identical to the host formula.      */
+ * in exactly numpy's operation order, so results are bit-identical to the host formula.
+ * scale == 0 selects exact integer costs w_int = counts[l][e] * p[l][s] (1 * p when uniform):
+ * the same argmin (f is a positive multiple of counts) without the 1e9 rounding.   */
 int mp_coeffs(const int64_t* counts, int64_t denom, const uint8_t* p, int L, int E, int S, double scale,
               double* w, int64_t* w_int, void* stream);
 

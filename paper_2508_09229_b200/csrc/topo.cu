@@ -133,7 +133,11 @@ __global__ void coeffs_kernel(const int64_t* __restrict__ counts, int64_t denom,
     const double f = counts ? __ddiv_rn((double)counts[le], (double)denom) : inv_uniform;
     const double v = __dmul_rn(f, (double)p[(int64_t)l * S + s]);
     if (w) w[i] = v;
-    if (w_int) w_int[i] = (int64_t)rint(__dmul_rn(v, scale));
+    if (w_int) {
+      // scale > 0: SPEC.md:308 integerisation rint(w * scale); scale == 0: exact count * p
+      w_int[i] = scale > 0.0 ? (int64_t)rint(__dmul_rn(v, scale))
+                             : (counts ? counts[le] : 1) * (int64_t)p[(int64_t)l * S + s];
+    }
   }
 }
 

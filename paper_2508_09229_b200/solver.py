@@ -93,18 +93,21 @@ class UniformFrequencies:
 
 
 def build_instance(cost: CostMatrix, freq: Union[FrequencyTable, UniformFrequencies, str, None], c: Constraints,
-                   E: Optional[int] = None) -> PlacementInstance:
+                   E: Optional[int] = None, exact: bool = False) -> PlacementInstance:
     """w[l,e,s] = f[l,e] * p[l,s].  ``freq`` may be a FrequencyTable (ILPLoad),
     ``UniformFrequencies(E)`` or "uniform" with ``E=`` (ILP).  Computed on the GPU; when the
-    table carries its integer counts the device derives f itself, bit-identical to numpy."""
+    table carries its integer counts the device derives f itself, bit-identical to numpy.
+    ``exact=True`` makes the flow costs the exact integers count*p (p for uniform) instead of
+    rint(w * 1e9): same optimal placements, no resolution loss beyond 1e7 tokens."""
     p = cost.p
     L, S = int(p.shape[0]), int(p.shape[1])
+    scale = 0.0 if exact else SCALE
     if isinstance(freq, UniformFrequencies):
-        return _instance(cost, None, 0, freq.E, c, None, "ilp")
+        return _instance(cost, None, 0, freq.E, c, None, "ilp", scale)
     if freq is None or (isinstance(freq, str) and freq == Uniform):
         if E is None:
             raise ConfigError("uniform build_instance needs the expert count E")
-        return _instance(cost, None, 0, int(E), c, None, "ilp")
+        return _instance(cost, None, 0, int(E), c, None, "ilp", scale)
     if not isinstance(freq, FrequencyTable):
         raise ConfigError("freq must be a FrequencyTable, UniformFrequencies or 'uniform'")
     f = np.asarray(freq.f, dtype=np.float64)
@@ -114,11 +117,14 @@ def build_instance(cost: CostMatrix, freq: Union[FrequencyTable, UniformFrequenc
         raise MoeplaceError("build_instance: negative or non-finite frequency")
     counts, denom = freq.counts, freq.topk * freq.n_tokens
     if counts is not None and denom > 0 and np.array_equal(np.asarray(counts) / denom, f):
-        return _instance(cost, counts, denom, f.shape[1], c, None, "ilpload")
+        return _instance(cost, counts, denom, f.shape[1], c, None, "ilpload", scale)
+    if exact:
+        raise ConfigError("exact costs need a FrequencyTable that carries its integer counts")
     return _instance(cost, None, 0, f.shape[1], c, f, "ilpload")
 
 
-def _instance(cost: CostMatrix, counts, denom: int, E: int, c: Constraints, f_float, label: str) -> PlacementInstance:
+def _instance(cost: CostMatrix, counts, denom: int, E: int, c: Constraints, f_float, label: str,
+              scale: float = SCALE) -> PlacementInstance:
     t = _lib.torch()
     p = cost.p
     L, S = int(p.shape[0]), int(p.shape[1])
@@ -132,9 +138,9 @@ def _instance(cost: CostMatrix, counts, denom: int, E: int, c: Constraints, f_fl
         w_int.copy_(t.round(w * SCALE).to(t.int64))
     else:
         cnt = None if counts is None else _lib.to_dev(counts, t.int64)
-        _lib.call("mp_coeffs", _lib.ptr(cnt), int(denom), _lib.ptr(p), L, E, S, SCALE, _lib.ptr(w), _lib.ptr(w_int),
-                  _lib.stream_handle())
-    return PlacementInstance(w, w_int, c, L, E, S, p.cpu().numpy(), SCALE, label)
+        _lib.call("mp_coeffs", _lib.ptr(cnt), int(denom), _lib.ptr(p), L, E, S, float(scale), _lib.ptr(w),
+                  _lib.ptr(w_int), _lib.stream_handle())
+    return PlacementInstance(w, w_int, c, L, E, S, p.cpu().numpy(), scale if scale > 0 else 1.0, label)
 
 
 def solve_exact(inst: PlacementInstance) -> tuple[Placement, float]:

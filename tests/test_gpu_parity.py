@@ -609,3 +609,21 @@ def test_binary_sidecar_roundtrip(tmp_path):
     (tmp_path / "bad").write_bytes(b"NOTATRACE" * 4)
     with pytest.raises(TraceParseError):
         mt.read_trace_binary(tmp_path / "bad")
+
+
+def test_exact_integer_coefficients_same_optimum():
+    """exact count*p flow costs give the same optimal objective as the 1e9-scaled
+    SPEC costs (positive scaling) — and are exactly counts * p."""
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("Dragonfly", 2, 2, 8, m)
+    tr = mt.generate_trace(m, 1.2, 20000, 10, 3)
+    freq = mt.estimate_frequencies(tr, m)
+    c = mpl.Constraints(54, 2)
+    a = sv.build_instance(cost, freq, c)
+    b = sv.build_instance(cost, freq, c, exact=True)
+    assert np.array_equal(b.w_int_numpy(), freq.counts[:, :, None] * cost.numpy().astype(np.int64)[:, None, :])
+    pa, oa = sv.solve_exact(a)
+    pb, ob = sv.solve_exact(b)
+    assert abs(oa - ob) <= 1e-12 * max(1.0, oa)
+    assert ev.objective_value(pa, freq, cost) == pytest.approx(ev.objective_value(pb, freq, cost), rel=1e-12)

@@ -198,3 +198,29 @@ def test_table2_setup_all_topologies(tmp_path):
             tr, obj = d["train"].mean_hops_per_token, d["test"].objective_train
             assert abs(tr - 6 * obj) <= 1e-6 * tr, (kind, m)  # acceptance #2 per topology
         assert per["ilpload"]["test"].objective_train <= min(d["test"].objective_train for d in per.values()) + 1e-12
+
+
+def test_config1_comparison_csv_equals_cpu_oracle(tmp_path):
+    """BASELINE config 1 (16B shape, 4 servers x 8 GPUs FatTree, c_layer 2, Zipf 1.2, 150 chunks,
+    100/50 split): the comparison CSV written by the GPU pipeline is byte-identical to one rebuilt
+    from the CPU oracle (generator, per-chunk sums, report floats, gains) on the same placements."""
+    cfg = dict(CFG1, output_dir=str(tmp_path / "c1"), n_tokens=60000)
+    cli.run_experiment(cfg)
+    out = tmp_path / "c1"
+    model = mt.ModelSpec(27, 64, 6)
+    sel, bounds = og.generate(27, 64, 6, 1.2, 60000, 150, 0)
+    g, dist, order, attn, cost = setup_topology("FatTree", 2, 2, 8, model, {"spines": 4})
+    from oracle import topology as ot
+    dsrv = ot.server_hops(g.n_nodes, g.links.tolist(), g.n_servers)
+    p = ot.cost_matrix(dsrv, g.device_server, attn.dispatch, attn.collect)
+    tok = np.diff(bounds)
+    rows, base = [], None
+    for m in ("rr", "greedy", "ilp", "ilpload"):
+        asg = mpl.read_placement(out / f"placement_{m}.csv", model).assign
+        sums = oe.chunk_sums(sel, oe.pe_table(p, asg), bounds)
+        r = oe.report(sums[100:150], tok[100:150])
+        if m == "rr":
+            base = r["mean"]
+        rows.append(f"FatTree,{m},{r['mean']!r},{r['std']!r},{oe.gain(base, r['mean'])!r}\n")
+    want = "network,placement,hops_mean,hops_std,gain_pct\n" + "".join(rows)
+    assert (out / "comparison.csv").read_text() == want
