@@ -49,15 +49,18 @@ class Packed:
 
 
 def sharded_evaluate(model, zipf_s: float, n_tokens: int, n_chunks: int, seed: int,
-                     placements: Sequence, cost, group=None, rank: Optional[int] = None,
+                     placements: Sequence, costs, group=None, rank: Optional[int] = None,
                      world: Optional[int] = None):
-    """Generate this rank's shard on its GPU, run the fused pass, all-reduce, and return the
-    global (FrequencyTable, [EvalReport]) — identical on every rank and to one-GPU results."""
+    """Generate this rank's shard on its GPU, build the load counts and the per-chunk hop sums of
+    every placement (``costs``: one CostMatrix or one per placement — several topologies can be
+    mixed), all-reduce ONE packed int64 buffer, and return the global
+    (FrequencyTable, [EvalReport]) — identical on every rank and to a one-GPU run.
+    Placements 0..3 ride the fused statistics pass; further ones are scored 16 per gather pass."""
     import torch
     import torch.distributed as dist
 
     from . import _lib
-    from .eval import _group_tables, report_from_sums
+    from .eval import MAX_LANES, _as_costs, _group_tables, _lanes_for, report_from_sums
     from .model_trace import chunk_bounds_even, frequencies_from_counts, generate_trace
 
     if rank is None or world is None:
@@ -66,22 +69,34 @@ def sharded_evaluate(model, zipf_s: float, n_tokens: int, n_chunks: int, seed: i
         else:
             rank, world = 0, 1
     placements = list(placements)
-    if not 1 <= len(placements) <= 4:
-        raise ConfigError("sharded_evaluate scores 1..4 placements per pass")
+    if not placements:
+        raise ConfigError("sharded_evaluate needs at least one placement")
+    costs = _as_costs(costs, len(placements))
     a, b = shard_range(n_tokens, rank, world)
     tr = generate_trace(model, zipf_s, n_tokens, n_chunks, seed, tok_range=(a, b))
     dev = tr.planes.device
-    pk = Packed(model.L, model.E, 4, n_chunks, dev)
+    P = len(placements)
+    pk = Packed(model.L, model.E, P, n_chunks, dev)
     if b > a:
-        tables, max_p = _group_tables(placements, [cost] * len(placements), model, 1)
+        planes, stride = tr.planes, tr.planes.shape[1]
         bounds = _lib.to_dev(tr.chunk_bounds, torch.int64)
         err = _lib.new_err()
+        sh = _lib.stream_handle()
+        head = placements[:4]
+        tables, max_p = _group_tables(head, costs[:4], model, 1)
         sums = torch.zeros((4, n_chunks), dtype=torch.int64, device=dev)
-        _lib.call("mp_hist_score_u8", _lib.ptr(tr.planes), tr.planes.shape[1], 0, b - a, model.L, model.K,
-                  model.E, _lib.ptr(bounds), n_chunks, _lib.ptr(tables), max_p, _lib.ptr(pk.counts),
-                  _lib.ptr(sums), _lib.ptr(err), _lib.stream_handle())
+        _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, 0, b - a, model.L, model.K, model.E, _lib.ptr(bounds),
+                  n_chunks, _lib.ptr(tables), max_p, _lib.ptr(pk.counts), _lib.ptr(sums), _lib.ptr(err), sh)
         _lib.check_err(err, "sharded_evaluate")
-        pk.sums.copy_(sums)
+        pk.sums[:len(head)].copy_(sums[:len(head)])
+        for g0 in range(4, P, MAX_LANES):
+            grp = placements[g0:g0 + MAX_LANES]
+            W = _lanes_for(len(grp))
+            tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], model, W)
+            gs = torch.zeros((4 * W, n_chunks), dtype=torch.int64, device=dev)
+            _lib.call("mp_score_u8", _lib.ptr(planes), stride, 0, b - a, model.L, model.K, _lib.ptr(bounds), n_chunks,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(gs), sh)
+            pk.sums[g0:g0 + len(grp)].copy_(gs[:len(grp)])
     pk.allreduce(group)
     counts = pk.counts.cpu().numpy()
     sums = pk.sums.cpu().numpy()

@@ -224,3 +224,18 @@ def test_config1_comparison_csv_equals_cpu_oracle(tmp_path):
         rows.append(f"FatTree,{m},{r['mean']!r},{r['std']!r},{oe.gain(base, r['mean'])!r}\n")
     want = "network,placement,hops_mean,hops_std,gain_pct\n" + "".join(rows)
     assert (out / "comparison.csv").read_text() == want
+
+
+def test_sharded_evaluate_many_placements_world1():
+    from paper_2508_09229_b200.shard import sharded_evaluate
+    m = mt.ModelSpec(27, 64, 6)
+    g, dist, order, attn, cost = setup_topology("FatTree", 4, 2, 4, m)
+    g2, _, _, _, cost2 = setup_topology("Dragonfly", 4, 2, 4, m)
+    rng = np.random.default_rng(1)
+    pls = [mpl.Placement(np.stack([rng.permutation(32)[:64 % 32 or 32].repeat(2)[:64] for _ in range(27)]))
+           for _ in range(23)]
+    costs = [cost if i % 3 else cost2 for i in range(23)]
+    freq, reps = sharded_evaluate(m, 1.2, 40_000, 30, 5, pls, costs)
+    tr = mt.generate_trace(m, 1.2, 40_000, 30, 5)
+    assert np.array_equal(freq.counts, mt.estimate_frequencies(tr, m).counts)
+    assert [r.chunk_hop_sums for r in reps] == ev.score_sums(tr, pls, costs).tolist()

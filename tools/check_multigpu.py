@@ -29,6 +29,14 @@ c = mpl.Constraints(64, 1)
 pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c)]
 N, C = 2_000_003, 150
 freq, reps = sharded_evaluate(m, 1.2, N, C, 11, pls, cost)
+# many placements over two topologies in one sharded evaluation (fused pass + gather passes)
+g2 = topo.build_topology(topo.TopologySpec("FatTree", 16, 4, 4))
+d2 = topo.all_pairs_hops(g2)
+cost2 = mpl.cost_matrix(d2, mt.default_attention_placement(m, topo.locality_order(g2, d2)))
+rng = np.random.default_rng(0)
+many = [mpl.Placement(np.stack([rng.permutation(256) for _ in range(58)])) for _ in range(21)]
+mcost = [cost if i % 2 else cost2 for i in range(21)]
+_, many_reps = sharded_evaluate(m, 1.2, N, C, 11, many, mcost)
 sig = torch.tensor([int(freq.counts.sum()), sum(r.hop_sum for r in reps)], dtype=torch.int64, device="cuda")
 allsig = [torch.zeros_like(sig) for _ in range(world)]
 dist.all_gather(allsig, sig)
@@ -38,6 +46,8 @@ if rank == 0:
     assert np.array_equal(f1.counts, freq.counts), "counts differ"
     assert [r.chunk_hop_sums for r in r1] == [r.chunk_hop_sums for r in reps], "hop sums differ"
     assert all(torch.equal(s, allsig[0]) for s in allsig), "ranks disagree"
+    want_many = ev.score_sums(tr, many, mcost)
+    assert [r.chunk_hop_sums for r in many_reps] == want_many.tolist(), "many-placement sums differ"
     print(f"multigpu ok: world={world} counts and per-chunk hop sums bit-identical to 1 GPU; "
           f"RR {reps[0].mean_hops_per_token:.4f} greedy {reps[1].mean_hops_per_token:.4f}")
 dist.barrier()
