@@ -353,6 +353,37 @@ def main():
         if world > 1:
             dist.all_reduce(buf)
 
+    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        default_ns = {2: 1_000_000, 3: 250_000, 4: 2_000, 5: 1_000_000}[wl]
+        ns = min(args.cpu_tokens or default_ns, n)
+        sel = cpu_sample(trace, ns)
+        bnd = np.minimum(np.asarray(trace.chunk_bounds, dtype=np.int64), ns)
+        from oracle import evaluate as oe
+        pes = []
+        cache = {}
+        for pl, cs in zip(placements, costs):
+            key = id(cs)
+            if key not in cache:
+                cache[key] = cs.numpy()
+            pes.append(oe.pe_table(cache[key], pl.assign))
+        oe.fused_pass(sel[:16], pes, bnd, E)
+        t_cpu = float("inf")
+        for _ in range(5):
+            t_a = time.perf_counter()
+            oe.fused_pass(sel, pes, bnd, E)
+            t_cpu = min(t_cpu, time.perf_counter() - t_a)
+        thr = cpu_threads()
+        cpu = {"value": ns * L * P_ / t_cpu, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P_} "
+                         f"placements in one pass, oracle/ numba parallel, best of 5, measured before any GPU timing",
+               "ms_per_sample": t_cpu * 1e3}
+        try:
+            cpu["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+        except Exception:
+            pass
+
     launches_per_step = (1 if fused else len(groups) + (1 if with_hist else 0))
     for _ in range(args.warmup):
         step(False)
@@ -513,37 +544,6 @@ def main():
                "h2d_bytes_per_step": int(n * L * K * world),
                "d2h_bytes_per_step": int(((L * E if with_hist else 0) + P_ * C) * 8 * world), "api": api}
         del host
-
-    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        default_ns = {2: 1_000_000, 3: 250_000, 4: 2_000, 5: 1_000_000}[wl]
-        ns = min(args.cpu_tokens or default_ns, n)
-        sel = cpu_sample(trace, ns)
-        bnd = np.minimum(np.asarray(trace.chunk_bounds, dtype=np.int64), ns)
-        from oracle import evaluate as oe
-        pes = []
-        cache = {}
-        for pl, cs in zip(placements, costs):
-            key = id(cs)
-            if key not in cache:
-                cache[key] = cs.numpy()
-            pes.append(oe.pe_table(cache[key], pl.assign))
-        oe.fused_pass(sel[:16], pes, bnd, E)
-        t_cpu = float("inf")
-        for _ in range(3):
-            t_a = time.perf_counter()
-            oe.fused_pass(sel, pes, bnd, E)
-            t_cpu = min(t_cpu, time.perf_counter() - t_a)
-        thr = cpu_threads()
-        cpu = {"value": ns * L * P_ / t_cpu, "unit": UNIT, "cores": thr, "kind": "port",
-               "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P_} "
-                         f"placements in one pass, oracle/ numba parallel, best of 3",
-               "ms_per_sample": t_cpu * 1e3}
-        try:
-            cpu["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
-        except Exception:
-            pass
 
     if rank == 0:
         cfg = workload(world, n, "fused" if fused else "separate")
