@@ -40,11 +40,12 @@ __device__ __forceinline__ void table_load(uint32_t a, uint32_t (&t)[W]) {
   }
 }
 
-// L2 bulk-prefetch lookahead in main-loop iterations (0 = off).  Measured on B200 (R1, 10M
-// tokens): helps the ATOMS-bound histogram kernels (hist 0.902 -> 0.878 ms, fused 1.370 -> 1.354
-// ms at 2 iterations) and hurts the LDS-bound gather (0.799 -> 0.903 ms), so only HIST uses it.
+// L2 bulk-prefetch lookahead in main-loop iterations (0 = off, the default).  Measured on B200
+// (R1, 10M tokens): at 2 iterations it speeds the ATOMS-bound histogram kernels by 1-3 % (hist
+// 0.902 -> 0.878 ms, fused 1.370 -> 1.354 ms) but raises their DRAM traffic to 1.09-1.13x the
+// algorithmic bytes (ncu), and slows the gather (0.799 -> 0.903 ms); kept as a build option only.
 #ifndef MP_PF_AHEAD
-#define MP_PF_AHEAD 2
+#define MP_PF_AHEAD 0
 #endif
 
 template <bool HIST, int W, int WIDEN, int UNROLL>
