@@ -627,3 +627,18 @@ def test_exact_integer_coefficients_same_optimum():
     pb, ob = sv.solve_exact(b)
     assert abs(oa - ob) <= 1e-12 * max(1.0, oa)
     assert ev.objective_value(pa, freq, cost) == pytest.approx(ev.objective_value(pb, freq, cost), rel=1e-12)
+
+
+def test_single_chunk_std_zero_and_p_sweep():
+    """C = 1 gives std = 0 exactly; P in {1, 4, 16} on E = 64 / 256."""
+    import torch
+    for (L, E, K) in [(4, 64, 6), (3, 256, 8)]:
+        m = mt.ModelSpec(L, E, K)
+        tr = mt.generate_trace(m, 1.2, 1237, 1, 2)
+        rng = np.random.default_rng(E)
+        p = rng.integers(0, 9, (L, 8)).astype(np.uint8)
+        cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+        for P in (1, 4, 16):
+            pls = [mpl.Placement(random_assign(rng, L, E, 8)) for _ in range(P)]
+            reps = ev.evaluate_many(tr, pls, cost)
+            assert all(r.std_hops == 0.0 and r.n_chunks == 1 for r in reps)
