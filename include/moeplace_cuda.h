@@ -117,16 +117,6 @@ int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, i
 int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P,
                    int L, int E, int S, uint32_t* tables, int W, int64_t* err, void* stream);
 
-/* ---- 4-bit-lane tables (every hop cost <= 15, true at the paper's topology sizes) ------------
- * mp_pack_tables_nib: W = 1 or 2 words of 8 nibbles per (l, e): nibble 2j+h of word w is
- * pe of placement 8w + 4h + j (P <= 8W); a cost > 15 raises MP_DATA_HOPS_RANGE in err.
- * mp_score_nib_u8: mp_score_u8 on such tables — hop_sums is int64 [8W][C] — with half the
- * shared-memory traffic per placement (16 placements per LDS.64).                             */
-int mp_pack_tables_nib(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
-                       int S, uint32_t* tables, int W, int64_t* err, void* stream);
-int mp_score_nib_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
-                    const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int64_t* hop_sums, void* stream);
-
 /* ---- traffic evaluator: token_hops / evaluate -----------------
  * For placement q and chunk c:
  *   hop_sums[q*C + c] += sum_{t in chunk c, t in [tok_begin,tok_end)} sum_l sum_k pe_q[l][planes[l][t*K+k]]

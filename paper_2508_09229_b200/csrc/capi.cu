@@ -41,10 +41,6 @@ cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int
                             cudaStream_t s);
 cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
                           const int64_t* cids, int64_t* lens_or_offsets, uint8_t* out, cudaStream_t s);
-cudaError_t launch_pack_nib(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L,
-                            int E, int S, uint32_t* tables, int W, int64_t* err, cudaStream_t s);
-cudaError_t launch_score_nib(int W, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
-                             const int64_t* bounds, int C, const uint32_t* tables, int64_t* hop_sums, cudaStream_t s);
 }  // namespace mp
 
 namespace {
@@ -126,24 +122,6 @@ int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int3
   if (!cost || !assign || !topo_of || !tables || T <= 0 || P <= 0 || L <= 0 || E <= 0 || S_ <= 0) return MP_ERR_ARG;
   if (!(W == 1 || W == 2 || W == 4) || P > 4 * W) return MP_ERR_ARG;
   return status(mp::launch_pack(cost, T, assign, topo_of, P, L, E, S_, tables, W, err, S(stream)));
-}
-
-int mp_pack_tables_nib(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
-                       int S_, uint32_t* tables, int W, int64_t* err, void* stream) {
-  if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
-  if (!cost || !assign || !topo_of || !tables || T <= 0 || P <= 0 || L <= 0 || E <= 0 || S_ <= 0) return MP_ERR_ARG;
-  if (!(W == 1 || W == 2) || P > 8 * W) return MP_ERR_ARG;
-  return status(mp::launch_pack_nib(cost, T, assign, topo_of, P, L, E, S_, tables, W, err, S(stream)));
-}
-
-int mp_score_nib_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
-                    const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int64_t* hop_sums, void* stream) {
-  int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
-  if (r) return r;
-  if (!chunk_bounds || C <= 0 || !tables || !hop_sums || !(W == 1 || W == 2)) return MP_ERR_ARG;
-  if (tok_end == tok_begin) return MP_OK;
-  return status(mp::launch_score_nib(W, planes, plane_stride, tok_begin, tok_end, L, K, chunk_bounds, C, tables,
-                                     hop_sums, S(stream)));
 }
 
 int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,

@@ -16,8 +16,9 @@
 
 namespace mp {
 
-template <int P>
+template <int W>
 struct ScoreAcc {
+  static constexpr int P = 4 * W;
   uint32_t tot[P];
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -47,44 +48,33 @@ __device__ __forceinline__ void table_load(uint32_t a, uint32_t (&t)[W]) {
 #define MP_PF_AHEAD 0
 #endif
 
-// NIB: placement costs packed as 4-bit lanes (max_p <= 15): a table word carries 8 placements,
-// split into two byte-lane words with one mask and one shift+mask.  Halves the shared traffic
-// per placement of the gather (LDS.64 serves 16 placements).  Nibble position 2j+h of word w holds
-// placement 8w + 4h + j, so byte-lane word 2w+h, byte j is placement 8w + 4h + j.
-template <bool HIST, int W, int WIDEN, int UNROLL, bool NIB = false>
+template <bool HIST, int W, int WIDEN, int UNROLL>
 struct Stream {
-  static constexpr int WW = W > 0 ? W : 1;
-  static constexpr int BW = WW * (NIB ? 2 : 1);  // byte-lane words per lookup
-  static constexpr int P = 4 * BW;
+  static constexpr int P = 4 * W;
   uint32_t base;   // shared address of row 0
   uint32_t slot;   // lane's score slot (byte 0 of the row offset)
   uint32_t hslot;  // lane's histogram slot
 
   // single byte (heads/tails of ranges; rare)
-  __device__ __forceinline__ void one(uint32_t e, ScoreAcc<P>& acc) {
+  __device__ __forceinline__ void one(uint32_t e, ScoreAcc<(W > 0 ? W : 1)>& acc) {
     if constexpr (HIST) atoms_inc(base + ((e << 8) | hslot) + 128);
     if constexpr (W > 0) {
       uint32_t t[W];
       table_load<W>(base + ((e << 8) | slot), t);
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if constexpr (NIB) {
+      for (int w = 0; w < W; ++w)
 #pragma unroll
-          for (int n = 0; n < 8; ++n) acc.tot[8 * w + 4 * (n & 1) + (n >> 1)] += (t[w] >> (4 * n)) & 0xfu;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc.tot[4 * w + j] += (t[w] >> (8 * j)) & 0xffu;
-        }
-      }
+        for (int j = 0; j < 4; ++j) acc.tot[4 * w + j] += (t[w] >> (8 * j)) & 0xffu;
     }
   }
 
   // 16 bytes -> lookups; u8-lane sums widened into u16-lane accumulators every WIDEN lookups
-  __device__ __forceinline__ void vec(const int4& x, uint32_t (&acc16)[2 * BW]) {
+  __device__ __forceinline__ void vec(const int4& x, uint32_t (&acc16)[2 * (W > 0 ? W : 1)]) {
     const uint32_t wd[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
-    uint32_t acc8[BW];
+    constexpr int WW = W > 0 ? W : 1;
+    uint32_t acc8[WW];
 #pragma unroll
-    for (int i = 0; i < BW; ++i) acc8[i] = 0;
+    for (int w = 0; w < WW; ++w) acc8[w] = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
@@ -94,24 +84,17 @@ struct Stream {
           uint32_t t[W];
           table_load<W>(base + off, t);
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            if constexpr (NIB) {
-              acc8[2 * w] += t[w] & 0x0f0f0f0fu;
-              acc8[2 * w + 1] += (t[w] >> 4) & 0x0f0f0f0fu;
-            } else {
-              acc8[w] += t[w];
-            }
-          }
+          for (int w = 0; w < W; ++w) acc8[w] += t[w];
           if constexpr (HIST) {
             const uint32_t hoff = (W == 1) ? off : prmt(wd[q], hslot, sel_row(b));
             atoms_inc(base + hoff + 128);
           }
           if (((q * 4 + b + 1) % WIDEN) == 0) {
 #pragma unroll
-            for (int i = 0; i < BW; ++i) {
-              acc16[2 * i] += acc8[i] & 0x00ff00ffu;
-              acc16[2 * i + 1] += (acc8[i] >> 8) & 0x00ff00ffu;
-              acc8[i] = 0;
+            for (int w = 0; w < W; ++w) {
+              acc16[2 * w] += acc8[w] & 0x00ff00ffu;
+              acc16[2 * w + 1] += (acc8[w] >> 8) & 0x00ff00ffu;
+              acc8[w] = 0;
             }
           }
         } else {
@@ -122,23 +105,24 @@ struct Stream {
     }
   }
 
-  __device__ __forceinline__ void widen(uint32_t (&acc16)[2 * BW], ScoreAcc<P>& acc) {
+  __device__ __forceinline__ void widen(uint32_t (&acc16)[2 * (W > 0 ? W : 1)], ScoreAcc<(W > 0 ? W : 1)>& acc) {
     if constexpr (W > 0) {
 #pragma unroll
-      for (int i = 0; i < BW; ++i) {
-        acc.tot[4 * i + 0] += acc16[2 * i] & 0xffffu;
-        acc.tot[4 * i + 2] += acc16[2 * i] >> 16;
-        acc.tot[4 * i + 1] += acc16[2 * i + 1] & 0xffffu;
-        acc.tot[4 * i + 3] += acc16[2 * i + 1] >> 16;
-        acc16[2 * i] = 0;
-        acc16[2 * i + 1] = 0;
+      for (int w = 0; w < W; ++w) {
+        acc.tot[4 * w + 0] += acc16[2 * w] & 0xffffu;
+        acc.tot[4 * w + 2] += acc16[2 * w] >> 16;
+        acc.tot[4 * w + 1] += acc16[2 * w + 1] & 0xffffu;
+        acc.tot[4 * w + 3] += acc16[2 * w + 1] >> 16;
+        acc16[2 * w] = 0;
+        acc16[2 * w + 1] = 0;
       }
     }
   }
 
   // all bytes [xa, xb) of one plane (xb - xa <= kMaxPiece, so vector offsets fit in 32 bits)
   __device__ __forceinline__ void range(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb,
-                                        ScoreAcc<P>& acc) {
+                                        ScoreAcc<(W > 0 ? W : 1)>& acc) {
+    constexpr int WW = W > 0 ? W : 1;
     const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
     const int64_t tb = max(ha, xb & ~(int64_t)15);
     for (int64_t x = xa + threadIdx.x; x < ha; x += blockDim.x) one(plane[x], acc);
@@ -146,9 +130,9 @@ struct Stream {
     const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
     const uint32_t nv = (uint32_t)((tb - ha) >> 4);
     const uint32_t T = blockDim.x;
-    uint32_t acc16[2 * BW];
+    uint32_t acc16[2 * WW];
 #pragma unroll
-    for (int i = 0; i < 2 * BW; ++i) acc16[i] = 0;
+    for (int i = 0; i < 2 * WW; ++i) acc16[i] = 0;
     uint32_t v = threadIdx.x;
     // main loop: UNROLL vectors in flight per thread, no bounds checks; one thread keeps the
     // CTA's trace region PF_AHEAD iterations ahead prefetched into L2
@@ -189,16 +173,16 @@ __device__ __forceinline__ int chunk_of(const int64_t* __restrict__ bounds, int 
 // which lets the per-piece flush reduce-scatter u32 values.
 constexpr int64_t kMaxPiece = (int64_t)1 << 26;
 
-template <bool HIST, int W, int WIDEN, int UNROLL, bool CHUNKED = false, bool NIB = false>
+template <bool HIST, int W, int WIDEN, int UNROLL, bool CHUNKED = false>
 __global__ void __launch_bounds__(kThreads, (W == 4 || W == 2) ? 2 : 3)
 stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
               const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
               int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
   extern __shared__ __align__(128) uint8_t sm[];  // 256 rows x 256 B
-  using St = Stream<HIST, W, WIDEN, UNROLL, NIB>;
-  constexpr int P = St::P;
+  constexpr int WW = W > 0 ? W : 1;
+  constexpr int P = 4 * WW;
   const int lane = threadIdx.x & 31;
-  St st;
+  Stream<HIST, W, WIDEN, UNROLL> st;
   st.base = smem_addr(sm);
   st.slot = W == 4 ? (uint32_t)((lane & 7) << 4) : W == 2 ? (uint32_t)(lane << 3) : (uint32_t)(lane << 2);
   st.hslot = (uint32_t)(lane << 2);
@@ -252,7 +236,7 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
       for (int64_t x = x0; x < x1;) {
         while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
         const int64_t xe = min(min(x1, cend), x + kMaxPiece);
-        ScoreAcc<P> acc;
+        ScoreAcc<WW> acc;
         acc.zero();
         st.range(plane, x, xe, acc);
         if constexpr (W > 0) {
@@ -268,7 +252,7 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
         x = xe;
       }
     } else {
-      ScoreAcc<P> dummy;
+      ScoreAcc<1> dummy;
       st.range(plane, x0, x1, dummy);
     }
 
@@ -282,12 +266,12 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 
 constexpr int kSmemBytes = 256 * 256;
 
-template <bool HIST, int W, int WIDEN, bool CHUNKED = false, bool NIB = false>
+template <bool HIST, int W, int WIDEN, bool CHUNKED = false>
 static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                             const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                             int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   constexpr int UNROLL = 4;
-  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED, NIB>;
+  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -304,18 +288,6 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
   kern<<<(unsigned)grid, kThreads, kSmemBytes, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
                                                      hop_sums, err);
   return cudaGetLastError();
-}
-
-// nibble-lane gather: W = 1 (8 placements, LDS.32) or W = 2 (16 placements, LDS.64), max_p <= 15
-cudaError_t launch_score_nib(int W, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
-                             const int64_t* bounds, int C, const uint32_t* tables, int64_t* hop_sums, cudaStream_t s) {
-  if (W == 1)
-    return launch_t<false, 1, 16, false, true>(planes, stride, t0, t1, L, K, 256, bounds, C, tables, nullptr, hop_sums,
-                                               nullptr, s);
-  if (W == 2)
-    return launch_t<false, 2, 16, false, true>(planes, stride, t0, t1, L, K, 256, bounds, C, tables, nullptr, hop_sums,
-                                               nullptr, s);
-  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,

@@ -112,40 +112,6 @@ __global__ void pack_kernel(const uint8_t* __restrict__ cost, int T, const int32
   }
 }
 
-// nibble tables: word w, nibble 2j+h = pe of placement 8w + 4h + j (values must be <= 15)
-__global__ void pack_nib_kernel(const uint8_t* __restrict__ cost, int T, const int32_t* __restrict__ assign,
-                                const int32_t* __restrict__ topo_of, int P, int L, int E, int S,
-                                uint32_t* __restrict__ tables, int W, int64_t* err) {
-  const int64_t n = (int64_t)L * 256 * W;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int w = (int)(i % W);
-    const int e = (int)((i / W) % 256);
-    const int l = (int)(i / ((int64_t)W * 256));
-    uint32_t word = 0;
-    if (e < E) {
-      for (int nb = 0; nb < 8; ++nb) {
-        const int q = 8 * w + 4 * (nb & 1) + (nb >> 1);
-        if (q >= P) continue;
-        const int32_t s = assign[((int64_t)q * L + l) * E + e];
-        const int32_t tp = topo_of[q];
-        if (s < 0 || s >= S || tp < 0 || tp >= T) { report_err(err, MP_DATA_UNPLACED, l, e); continue; }
-        const uint32_t v = cost[((int64_t)tp * L + l) * S + s];
-        if (v > 15) { report_err(err, MP_DATA_HOPS_RANGE, l, e); continue; }
-        word |= v << (4 * nb);
-      }
-    }
-    tables[i] = word;
-  }
-}
-
-cudaError_t launch_pack_nib(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L,
-                            int E, int S, uint32_t* tables, int W, int64_t* err, cudaStream_t s) {
-  const int64_t n = (int64_t)L * 256 * W;
-  pack_nib_kernel<<<(unsigned)min((n + 255) / 256, (int64_t)4096), 256, 0, s>>>(cost, T, assign, topo_of, P, L, E, S,
-                                                                                tables, W, err);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_pack(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
                         int S, uint32_t* tables, int W, int64_t* err, cudaStream_t s) {
   const int64_t n = (int64_t)L * 256 * W;

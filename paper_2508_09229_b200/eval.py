@@ -103,10 +103,8 @@ def _unique_costs(costs: Sequence[CostMatrix]):
     return uniq, topo_of
 
 
-def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec, W: int,
-                  nib: bool = False):
-    """Pack one group into device tables uint32 [L, 256, W]: u8 lanes (<= 4W placements) or,
-    with ``nib``, 4-bit lanes (<= 8W placements, every cost <= 15)."""
+def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec, W: int):
+    """Pack one group (<= 4W placements) into device tables uint32 [L, 256, W]."""
     t = _lib.torch()
     dev = _lib.require_cuda()
     uniq, topo_of = _unique_costs(costs)
@@ -122,9 +120,8 @@ def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], 
     d_topo = _lib.to_dev(np.asarray(topo_of, dtype=np.int32), t.int32)
     tables = t.empty((model.L, 256, W), dtype=t.int32, device=dev)
     err = _lib.new_err()
-    _lib.call("mp_pack_tables_nib" if nib else "mp_pack_tables", _lib.ptr(cost), len(uniq), _lib.ptr(d_assign),
-              _lib.ptr(d_topo), len(placements), model.L, model.E, S, _lib.ptr(tables), W, _lib.ptr(err),
-              _lib.stream_handle())
+    _lib.call("mp_pack_tables", _lib.ptr(cost), len(uniq), _lib.ptr(d_assign), _lib.ptr(d_topo), len(placements),
+              model.L, model.E, S, _lib.ptr(tables), W, _lib.ptr(err), _lib.stream_handle())
     _lib.check_err(err, "evaluate: unplaced expert")
     max_p = max(c.max_p for c in uniq)
     return tables, max_p
@@ -134,19 +131,8 @@ def _lanes_for(n: int) -> int:
     return 1 if n <= 4 else 2 if n <= 8 else 4
 
 
-def _nib_words(n: int, costs) -> int:
-    """Table words for a group in 4-bit-lane mode, or 0 when u8 lanes are better/required:
-    4-bit lanes pay off from 5 placements on (8 per LDS.32, 16 per LDS.64) and need every
-    hop cost <= 15 (true at the paper's topology sizes)."""
-    if n <= 4 or any(c.max_p > 15 for c in costs):
-        return 0
-    return 1 if n <= 8 else 2
-
-
-def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, nibble: bool = True) -> np.ndarray:
-    """Exact per-chunk hop sums, int64 [P, C], computed on the GPU: groups of up to 16 placements
-    per pass, in 4-bit lanes when every cost is <= 15 (``mp_score_nib_u8``), else u8 lanes
-    (``mp_score_u8``)."""
+def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs) -> np.ndarray:
+    """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_u8``)."""
     t = _lib.torch()
     m = trace.model
     if m is None or trace.n_tokens == 0:
@@ -158,27 +144,18 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, n
     groups = []
     for g0 in range(0, len(placements), MAX_LANES):
         grp = placements[g0:g0 + MAX_LANES]
-        gc = costs[g0:g0 + MAX_LANES]
-        nw = _nib_words(len(grp), gc) if nibble else 0
-        if nw:
-            tables, max_p = _group_tables(grp, gc, m, nw, nib=True)
-            groups.append((g0, len(grp), nw, tables, max_p, t.zeros((8 * nw, C), dtype=t.int64, device=dev), True))
-        else:
-            W = _lanes_for(len(grp))
-            tables, max_p = _group_tables(grp, gc, m, W)
-            groups.append((g0, len(grp), W, tables, max_p, t.zeros((4 * W, C), dtype=t.int64, device=dev), False))
+        W = _lanes_for(len(grp))
+        tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], m, W)
+        groups.append((g0, len(grp), W, tables, max_p, t.zeros((4 * W, C), dtype=t.int64, device=dev)))
 
     def launch(planes, stride, t0, t1, bounds):
-        for _, _, W, tables, max_p, sums, nib in groups:
-            if nib:
-                _lib.call("mp_score_nib_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
-                          _lib.ptr(tables), W, _lib.ptr(sums), _lib.stream_handle())
-            else:
-                _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
-                          _lib.ptr(tables), W, max_p, _lib.ptr(sums), _lib.stream_handle())
+        for _, _, W, tables, max_p, sums in groups:
+            _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(sums), _lib.stream_handle())
+
     sweep(trace, launch)
     out = np.zeros((len(placements), C), dtype=np.int64)
-    for g0, n, _, _, _, sums, _ in groups:
+    for g0, n, _, _, _, sums in groups:
         out[g0:g0 + n] = sums[:n].cpu().numpy()
     return out
 

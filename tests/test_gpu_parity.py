@@ -642,27 +642,3 @@ def test_single_chunk_std_zero_and_p_sweep():
             pls = [mpl.Placement(random_assign(rng, L, E, 8)) for _ in range(P)]
             reps = ev.evaluate_many(tr, pls, cost)
             assert all(r.std_hops == 0.0 and r.n_chunks == 1 for r in reps)
-
-
-@pytest.mark.parametrize("P", [5, 8, 9, 16, 21])
-def test_nibble_lanes_match_u8_lanes(P):
-    """4-bit-lane tables (max_p <= 15) give the same per-chunk sums as u8 lanes and the oracle,
-    including heads/tails of unaligned views and several topologies in one group."""
-    L, E, K = R1
-    m = mt.ModelSpec(L, E, K)
-    tr = mt.generate_trace(m, 1.2, 7013, 19, 9)
-    sel, bounds = og.generate(L, E, K, 1.2, 7013, 19, 9)
-    costs = []
-    for kind in ("FatTree", "Dragonfly", "DragonflySparse"):
-        costs.append(setup_topology(kind, 16, 4, 4, m)[4])
-    assert all(c.max_p <= 15 for c in costs)
-    rng = np.random.default_rng(P)
-    pls = [mpl.Placement(random_assign(rng, L, E, 256)) for _ in range(P)]
-    cs = [costs[i % 3] for i in range(P)]
-    a = ev.score_sums(tr, pls, cs)
-    b = ev.score_sums(tr, pls, cs, nibble=False)
-    assert np.array_equal(a, b)
-    for i in (0, P - 1):
-        assert np.array_equal(a[i], oracle_sums(sel, cs[i].numpy(), pls[i].assign, bounds))
-    v = tr.view(3, 17)
-    assert np.array_equal(ev.score_sums(v, pls, cs), ev.score_sums(v, pls, cs, nibble=False))
