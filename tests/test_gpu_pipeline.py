@@ -239,3 +239,17 @@ def test_sharded_evaluate_many_placements_world1():
     tr = mt.generate_trace(m, 1.2, 40_000, 30, 5)
     assert np.array_equal(freq.counts, mt.estimate_frequencies(tr, m).counts)
     assert [r.chunk_hop_sums for r in reps] == ev.score_sums(tr, pls, costs).tolist()
+
+
+def test_plain_c_client_of_the_abi(tmp_path):
+    """The C-ABI works from plain C (cudart only): examples/capi_client.c."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    exe = tmp_path / "capi_client"
+    subprocess.run(["nvcc", "-o", str(exe), str(root / "examples" / "capi_client.c"), "-I", str(root / "include"),
+                    "-L", str(root / "paper_2508_09229_b200" / "lib"), "-lmoeplace_cuda"], check=True,
+                   capture_output=True)
+    env = dict(__import__("os").environ, LD_LIBRARY_PATH=str(root / "paper_2508_09229_b200" / "lib"))
+    r = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 0 and "capi_client ok" in r.stdout, r.stdout + r.stderr
