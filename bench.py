@@ -477,6 +477,19 @@ def main():
             kms_ = xa.elapsed_time(xb) / 10
             gbs = n * L * K / (kms_ / 1e3) / 1e9
             kernels_alone[nm] = {"ms": kms_, "GBps": gbs, "frac": gbs / peak}
+        # L1TEX model of the fused pass: per 512 B of trace one LDG.128 (4 wavefronts), 16 LDS.32 gathers
+        # (1 each) and 16 ATOMS (a each, a fitted live from mp_hist_u8 alone = 4 + 16a wavefronts per 512 B);
+        # one wavefront per SM per clock.
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        blocks = n * L * K / 512 / 148  # 512-byte blocks per SM
+        clk = mhz * 1e6
+        a = (kernels_alone["mp_hist_u8"]["ms"] / 1e3 * clk / blocks - 4) / 16
+        if fused:
+            roofline["l1tex_model"] = {
+                "wavefronts_per_512B": {"LDG.128": 4, "LDS.32": 16, "ATOMS": 16 * a},
+                "atoms_wavefronts_per_instr": a, "sm_mhz": mhz,
+                "bound_ms": (4 + 16 + 16 * a) * blocks / clk * 1e3,
+                "frac_of_l1tex_bound": (4 + 16 + 16 * a) * blocks / clk * 1e3 / per_launch_ms}
 
     # ------- configs 2/4: the factorized evaluator beside the measured gather (not the headline) -------
     factorized = None
