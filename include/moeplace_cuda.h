@@ -19,7 +19,9 @@
  *   - Return value: MP_OK, or an MP_ERR_* code describing a synchronous argument/launch
  *     failure (the Python layer maps MP_ERR_ARG/MP_ERR_UNSUPPORTED to ConfigError,
  *     MP_ERR_CUDA to RuntimeError).  Data errors found by a kernel are written to a caller
- *     owned device `err` block (int64[4] = {code, layer, value, count}; code 0 = clean).
+ *     owned device `err` block (int64[4] = {code, layer, value, count}; code 0 = clean).  Every
+ *     entry point that takes `err` requires it (NULL -> MP_ERR_ARG); argument checks run before
+ *     any CUDA call, so a rejected call never touches the device.
  *
  * Trace layout ("layer planes"): uint8 planes[L][plane_stride]; byte t*K+k of plane l is the
  * k-th expert selected by token t in MoE layer l.  plane_stride and the

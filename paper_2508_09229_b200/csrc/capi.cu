@@ -73,7 +73,7 @@ const char* mp_status_string(int st) {
 int mp_gen_trace(uint64_t seed, int64_t tok_begin, int64_t tok_end, int L, int K, int E, const uint32_t* cdf,
                  const uint8_t* perm, uint8_t* planes, int64_t plane_stride, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
-  if (E <= 0 || K > E || !cdf || !perm || tok_begin < 0) return MP_ERR_ARG;
+  if (E <= 0 || K > E || !cdf || !perm || tok_begin < 0 || L > 65535) return MP_ERR_ARG;
   int r = check_trace(planes, plane_stride, 0, tok_end - tok_begin, L, K);
   if (r) return r;
   return status(mp::launch_gen(seed, tok_begin, tok_end, L, K, E, cdf, perm, planes, plane_stride, S(stream)));
@@ -91,7 +91,7 @@ int mp_validate_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begi
 int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K, int E,
                int64_t* counts, int64_t* err, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
-  if (E <= 0 || !counts) return MP_ERR_ARG;
+  if (E <= 0 || !counts || !err) return MP_ERR_ARG;
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
   if (tok_end == tok_begin) return MP_OK;
@@ -104,7 +104,7 @@ int mp_hist_chunks_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_b
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
-  if (E <= 0 || !counts || !chunk_bounds || C <= 0) return MP_ERR_ARG;
+  if (E <= 0 || !counts || !err || !chunk_bounds || C <= 0) return MP_ERR_ARG;
   if (tok_end == tok_begin) return MP_OK;
   return status(mp::launch_hist_chunks(planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C, counts, err,
                                        S(stream)));
@@ -119,7 +119,7 @@ int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, i
 int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
                    int S_, uint32_t* tables, int W, int64_t* err, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
-  if (!cost || !assign || !topo_of || !tables || T <= 0 || P <= 0 || L <= 0 || E <= 0 || S_ <= 0) return MP_ERR_ARG;
+  if (!cost || !assign || !topo_of || !tables || !err || T <= 0 || P <= 0 || L <= 0 || E <= 0 || S_ <= 0) return MP_ERR_ARG;
   if (!(W == 1 || W == 2 || W == 4) || P > 4 * W) return MP_ERR_ARG;
   return status(mp::launch_pack(cost, T, assign, topo_of, P, L, E, S_, tables, W, err, S(stream)));
 }
@@ -154,7 +154,7 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
-  if (E <= 0 || !counts || !chunk_bounds || C <= 0 || !tables || !hop_sums || max_p < 0) return MP_ERR_ARG;
+  if (E <= 0 || !counts || !err || !chunk_bounds || C <= 0 || !tables || !hop_sums || max_p < 0) return MP_ERR_ARG;
   if (max_p > 255) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;
   return status(mp::launch_stream(true, 1, max_p, planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C,
@@ -163,7 +163,7 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
 
 int mp_apsp_bfs(const int32_t* row_ptr, const int32_t* col, int n_nodes, const int32_t* src_nodes, int n_src,
                 const int32_t* dst_nodes, int n_dst, uint8_t* dist, int64_t* err, void* stream) {
-  if (!row_ptr || !col || !src_nodes || !dst_nodes || !dist || n_nodes <= 0 || n_src < 0 || n_dst < 0)
+  if (!row_ptr || !col || !src_nodes || !dst_nodes || !dist || !err || n_nodes <= 0 || n_src < 0 || n_dst < 0)
     return MP_ERR_ARG;
   if (n_nodes > 8192) return MP_ERR_UNSUPPORTED;
   return status(mp::launch_bfs(row_ptr, col, n_nodes, src_nodes, n_src, dst_nodes, n_dst, dist, err, S(stream)));
@@ -190,7 +190,7 @@ int mp_coeffs(const int64_t* counts, int64_t denom, const uint8_t* p, int L, int
 int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev_server, const uint8_t* dsrv, int n_srv,
                 const int32_t* dispatch, const int32_t* collect, int L, int E, int S_, int64_t* traffic, int64_t* err,
                 void* stream) {
-  if (!counts || !assign || !dev_server || !dsrv || !dispatch || !collect || !traffic || n_srv <= 0 || L <= 0 ||
+  if (!counts || !assign || !dev_server || !dsrv || !dispatch || !collect || !traffic || !err || n_srv <= 0 || L <= 0 ||
       E <= 0 || S_ <= 0)
     return MP_ERR_ARG;
   return status(mp::launch_comm(counts, assign, dev_server, dsrv, n_srv, dispatch, collect, L, E, S_, traffic, err,
@@ -214,7 +214,7 @@ int mp_score_dedup_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_b
 int mp_pack_server_tables(const int32_t* server_of, int T, const int32_t* assign, const int32_t* topo_of, int P, int L,
                           int E, int S_, uint32_t* srv_tables, int64_t* err, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
-  if (!server_of || !assign || !topo_of || !srv_tables || T <= 0 || P <= 0 || P > 4 || L <= 0 || E <= 0 || S_ <= 0)
+  if (!server_of || !assign || !topo_of || !srv_tables || !err || T <= 0 || P <= 0 || P > 4 || L <= 0 || E <= 0 || S_ <= 0)
     return MP_ERR_ARG;
   return status(mp::launch_pack_srv(server_of, T, assign, topo_of, P, L, E, S_, srv_tables, err, S(stream)));
 }

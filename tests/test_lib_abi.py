@@ -43,6 +43,49 @@ def test_status_strings_and_arg_checks():
     assert L.mp_gen_trace(0, 0, 1, 1, 1, 300, None, None, None, 16, None) == 3  # E > 256 unsupported
 
 
+def test_argument_validation_matrix():
+    """Every rejection is synchronous and happens before any CUDA call (fake pointers are never
+    dereferenced), with the status the wrappers map to ConfigError (1/3)."""
+    L = _lib.load()
+    P = 0x10000  # 16-byte aligned fake device pointer
+    ARG, UNS = 1, 3
+    N, K, Lr, E = 100, 8, 4, 256
+    st = 800  # >= N*K, multiple of 16
+    cases = [
+        (L.mp_hist_u8(P, st, 0, N, Lr, K, E, P, None, None), ARG),          # err required
+        (L.mp_hist_u8(P + 1, st, 0, N, Lr, K, E, P, P, None), ARG),         # misaligned planes
+        (L.mp_hist_u8(P, st + 8, 0, N, Lr, K, E, P, P, None), ARG),         # stride % 16
+        (L.mp_hist_u8(P, 784, 0, N, Lr, K, E, P, P, None), ARG),            # stride < N*K
+        (L.mp_hist_u8(P, st, 5, 4, Lr, K, E, P, P, None), ARG),             # t1 < t0
+        (L.mp_hist_u8(P, st, 0, N, Lr, K, 0, P, P, None), ARG),             # E = 0
+        (L.mp_hist_u8(P, st, 0, N, Lr, K, 257, P, P, None), UNS),           # E > 256
+        (L.mp_hist_u8(P, st, 0, N, 0, K, E, P, P, None), ARG),              # L = 0
+        (L.mp_hist_chunks_u8(P, st, 0, N, Lr, K, E, P, 0, P, P, None), ARG),  # C = 0
+        (L.mp_hist_score_u8(P, st, 0, N, Lr, K, E, P, 1, P, 8, P, P, None, None), ARG),
+        (L.mp_hist_score_u8(P, st, 0, N, Lr, K, E, P, 1, P, 256, P, P, P, None), UNS),
+        (L.mp_score_u8(P, st, 0, N, Lr, K, P, 1, P, 3, 8, P, None), ARG),   # W not 1/2/4
+        (L.mp_score_u8(P, st, 0, N, Lr, K, P, 1, P, 1, -1, P, None), ARG),
+        (L.mp_score_u8(P, st, 0, N, Lr, K, P, 1, P, 1, 300, P, None), UNS),
+        (L.mp_pack_tables(P, 1, P, P, 5, Lr, E, 8, P, 1, P, None), ARG),     # P > 4*W
+        (L.mp_pack_tables(P, 1, P, P, 4, Lr, E, 8, P, 1, None, None), ARG),  # err required
+        (L.mp_token_hops_u8(P, st, 0, N, 58, 8, P, 200, P, P, None), UNS),   # L*K*max_p > 65535
+        (L.mp_apsp_bfs(P, P, 9000, P, 1, P, 1, P, P, None), UNS),
+        (L.mp_apsp_bfs(P, P, 10, P, 1, P, 1, P, None, None), ARG),
+        (L.mp_gen_trace(0, 0, N, 70000, K, E, P, P, P, st, None), ARG),     # grid.y limit
+        (L.mp_gen_trace(0, 0, N, Lr, 9, 8, P, P, P, st, None), ARG),        # K > E
+        (L.mp_score_dedup_u8(P, 33 * N + 12, 0, N, Lr, 33, P, 1, P, P, P, P, P, P, None), UNS),
+        (L.mp_comm_map(P, P, P, P, 4, P, P, Lr, E, 8, P, None, None), ARG),
+        (L.mp_pack_server_tables(P, 1, P, P, 5, Lr, E, 8, P, P, None), ARG),
+        (L.mp_contract_counts(P, 65535 * 16 + 1, P, 1, 10, P, None), UNS),
+        (L.mp_coeffs(P, 0, P, Lr, E, 8, 1e9, P, None, None), ARG),          # denom 0 with counts
+        (L.mp_copy_planes_h2d(P, 8, P, 16, 16, 1, None), ARG),               # dst stride < width
+        (L.mp_copy_planes_h2d(P, 16, P, 16, 0, 4, None), 0),                 # empty copy is a no-op
+        (L.mp_hist_u8(P, st, 7, 7, Lr, K, E, P, P, None), 0),                # empty range is a no-op
+    ]
+    for i, (got, want) in enumerate(cases):
+        assert got == want, (i, got, want)
+
+
 def test_host_solver_through_abi():
     w = np.array([[[3, 1]]], dtype=np.int64)
     a = np.zeros((1, 1), np.int32)
