@@ -9,7 +9,10 @@ Placements scored: RR, Greedy, ILP and ILPLoad (P=4), computed in the untimed se
 One step = one pass over the resident trace that builds the per-(layer, expert) load counts
 (estimate_frequencies) AND scores the P=4 placements (per-chunk hop sums of evaluate), i.e.
 "hist over all N and score of P=4 over all N" — by default with the fused kernel
-(mp_hist_score_u8), or with --mode separate as mp_hist_u8 + mp_score_u8.  For N GPUs each rank
+(mp_hist_score_u8), or with --mode separate as mp_hist_u8 + mp_score_u8.  The library computes the
+hop sums by count-contract (histogram of every (layer, chunk) piece contracted with the cost
+tables at the piece's flush; exact by linearity); --algo gather times the per-byte
+table gather instead (bit-identical results, tests/test_gpu_algos.py).  For N GPUs each rank
 owns a contiguous 10M-token shard of one N*10M-token trace (weak scaling) and the packed int64
 [counts | hop sums] buffer is combined with one NCCL all_reduce inside the timed step.
 
@@ -196,6 +199,8 @@ def main():
                     help="BASELINE config: 2 (default, the metric's config), 3 multi-topology, 4 4096 candidates, "
                          "5 100M tokens strong scaling")
     ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
+    ap.add_argument("--algo", choices=["auto", "gather", "count"], default="auto",
+                    help="hop-sum algorithm (include/moeplace_cuda.h MP_ALGO_*); auto = the library's choice")
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (configs 2-4) / total (config 5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-tokens", type=int, default=None, help="cpu_baseline sample (tokens)")
@@ -326,14 +331,16 @@ def main():
     kev = [_events() for _ in range(2)]
     kernel_ms = [[], []]
 
+    algo = {"auto": 0, "gather": 1, "count": 2}[args.algo]
+
     def step(timed: bool):
         buf.zero_()
         if with_hist and fused:
             if timed:
                 kev[0][0].record(stream)
             W, tables, max_p, _ = groups[0]
-            _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
-                      _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(views[0]), _lib.ptr(err), sh)
+            _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(counts), _lib.ptr(views[0]), _lib.ptr(err), algo, sh)
             if timed:
                 kev[0][1].record(stream)
         else:
@@ -346,8 +353,8 @@ def main():
             if timed:
                 kev[0][0].record(stream)
             for (W, tables, max_p, _), v in zip(groups, views):
-                _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C, _lib.ptr(tables),
-                          W, max_p, _lib.ptr(v), sh)
+                _lib.call("mp_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C,
+                          _lib.ptr(tables), W, max_p, _lib.ptr(v), algo, sh)
             if timed:
                 kev[0][1].record(stream)
         if world > 1:
@@ -421,7 +428,8 @@ def main():
     peak, peak_src = measured_peak()
     k_main = float(np.mean(kernel_ms[0]))
     if fused:
-        kname, tkey, launches = "mp_hist_score_u8 (fused hist+score, W=1)", "fused", 1
+        kname, tkey, launches = ("mp_hist_score_u8 (fused hist+score of 4 placements; count-contract: histogram "
+                                 "+ per-(layer,chunk) contraction with the cost tables)"), "fused", 1
     else:
         Ws = sorted({W for W, _, _, _ in groups})
         kname = f"mp_score_u8 (W={'/'.join(map(str, Ws))}, {len(groups)} launch(es) per step)"
@@ -463,6 +471,11 @@ def main():
                 _lib.ptr(groups[0][1]), 1, groups[0][2], _lib.ptr(scratch[L * E:]), sh),
             "mp_hist_u8": lambda: _lib.call(
                 "mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(scratch[:L * E]), _lib.ptr(err), sh),
+            # the same fused step with the per-byte GATHER algorithm (one LDS per lookup + ATOMS), for comparison
+            "mp_hist_score_ex_u8 (GATHER, 4 placements)": lambda: _lib.call(
+                "mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+                _lib.ptr(groups[0][1]), 1, groups[0][2], _lib.ptr(scratch[:L * E]), _lib.ptr(scratch[L * E:]),
+                _lib.ptr(err), 1, sh),
         }
         kernels_alone = {}
         for nm, fn in alone.items():
@@ -477,19 +490,20 @@ def main():
             kms_ = xa.elapsed_time(xb) / 10
             gbs = n * L * K / (kms_ / 1e3) / 1e9
             kernels_alone[nm] = {"ms": kms_, "GBps": gbs, "frac": gbs / peak}
-        # L1TEX model of the fused pass: per 512 B of trace one LDG.128 (4 wavefronts), 16 LDS.32 gathers
-        # (1 each) and 16 ATOMS (a each, a fitted live from mp_hist_u8 alone = 4 + 16a wavefronts per 512 B);
-        # one wavefront per SM per clock.
+        # L1TEX model (one wavefront per SM per clock): per 512 B of trace one LDG.128 (4 wavefronts) and 16
+        # ATOMS (a each, a fitted live from mp_hist_u8 alone = 4 + 16a wavefronts per 512 B); the GATHER
+        # algorithm adds 16 LDS.32 (1 each).  The count-contract step needs only the histogram's wavefronts.
         mhz = (clocks or {}).get("sm_mhz") or 1965.0
         blocks = n * L * K / 512 / 148  # 512-byte blocks per SM
         clk = mhz * 1e6
         a = (kernels_alone["mp_hist_u8"]["ms"] / 1e3 * clk / blocks - 4) / 16
         if fused:
             roofline["l1tex_model"] = {
-                "wavefronts_per_512B": {"LDG.128": 4, "LDS.32": 16, "ATOMS": 16 * a},
+                "wavefronts_per_512B": {"LDG.128": 4, "ATOMS": 16 * a},
                 "atoms_wavefronts_per_instr": a, "sm_mhz": mhz,
-                "bound_ms": (4 + 16 + 16 * a) * blocks / clk * 1e3,
-                "frac_of_l1tex_bound": (4 + 16 + 16 * a) * blocks / clk * 1e3 / per_launch_ms}
+                "bound_ms": (4 + 16 * a) * blocks / clk * 1e3,
+                "frac_of_l1tex_bound": (4 + 16 * a) * blocks / clk * 1e3 / per_launch_ms,
+                "gather_bound_ms": (4 + 16 + 16 * a) * blocks / clk * 1e3}
 
     # ------- configs 2/4: the factorized evaluator beside the measured gather (not the headline) -------
     factorized = None
@@ -521,11 +535,11 @@ def main():
         torch.cuda.synchronize()
         f_ms = fa.elapsed_time(fb) / args.steps
         factorized = {"ms_per_step": f_ms, "placements_evaluated_per_s": P_ / (f_ms / 1e3),
-                      "bit_identical_to_gather": ok,
-                      "note": "per-chunk histogram (mp_hist_chunks_u8) + exact contraction on the tensor cores (7-bit digit int8 "
-                              "GEMMs, cuBLASLt, int32 accumulation); "
-                              "same per-chunk hop sums as the per-token gather by linearity (SPEC.md:383); "
-                              "not a token-layers-scored rate (no per-token values are produced)"}
+                      "bit_identical_to_step": ok,
+                      "note": "cross-check: per-chunk histogram materialised in HBM (mp_hist_chunks_u8, int64 [C][L][E]) "
+                              "+ exact contraction on the tensor cores (7-bit digit int8 GEMMs, cuBLASLt, int32 "
+                              "accumulation) -- the out-of-kernel form of the step's count-contract; "
+                              "same per-chunk hop sums by linearity (SPEC.md:383)"}
 
     # ---------------- e2e through the public API, host buffers ----------------
     e2e = None
@@ -579,6 +593,13 @@ def main():
                    else f"trace {n * L * K / 1e6:.0f} MB < 126 MB L2: each step streams it {len(groups)}x; "
                         "first pass per step from HBM, reuse from L2",
                    "parallelism": f"token shards x{world}" + (" + 1 NCCL all_reduce" if world > 1 else "")}
+
+        def algo_used(hist: bool, W: int) -> str:  # mirrors choose_algo in csrc/stream.cu
+            if args.algo != "auto":
+                return args.algo
+            return "count-contract" if (hist or W > 1) else "gather"
+        cfg["hop_sum_algorithm"] = (algo_used(True, 1) if fused else
+                                    "/".join(sorted({algo_used(False, W) for W, _, _, _ in groups})))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",

@@ -138,10 +138,30 @@ int mp_token_hops_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
                      const uint32_t* tables, int max_p, uint32_t* scratch, uint32_t* hops, void* stream);
 
 /* ---- fused statistics + traffic pass (one read of the trace) -----------------------------
- * mp_hist_u8 and mp_score_u8 over the same token range in one kernel (W = 1 only).           */
+ * mp_hist_u8 and mp_score_u8 over the same token range in one kernel (W = 1 tables).          */
 int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
                      int L, int K, int E, const int64_t* chunk_bounds, int C, const uint32_t* tables,
                      int max_p, int64_t* counts, int64_t* hop_sums, int64_t* err, void* stream);
+
+/* ---- explicit algorithm choice for the hop sums -------------------------------------------
+ * Both algorithms produce bit-identical hop_sums (and counts):
+ *   MP_ALGO_GATHER: every expert byte looks up its placement costs in a shared-memory table and
+ *     per-token-layer sums are accumulated in u8 lanes (one LDS per lookup);
+ *   MP_ALGO_COUNT:  count-contract -- the kernel only histograms; at each (layer, chunk) piece it
+ *     contracts the piece's bin totals with the tables (hop sum = sum_e n[e]*pe[e]),
+ *     so the per-byte cost does not depend on the number of placements;
+ *   MP_ALGO_AUTO:   the faster one for the shape (GATHER for score-only W = 1, COUNT otherwise),
+ *     which is what mp_score_u8 / mp_hist_score_u8 use.
+ * mp_hist_score_ex_u8 takes W = 1, 2 or 4 (GATHER supports W = 1 only -> MP_ERR_UNSUPPORTED).   */
+#define MP_ALGO_AUTO 0
+#define MP_ALGO_GATHER 1
+#define MP_ALGO_COUNT 2
+int mp_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
+                   int L, int K, const int64_t* chunk_bounds, int C, const uint32_t* tables, int W,
+                   int max_p, int64_t* hop_sums, int algo, void* stream);
+int mp_hist_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
+                        int L, int K, int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int W,
+                        int max_p, int64_t* counts, int64_t* hop_sums, int64_t* err, int algo, void* stream);
 
 /* ---- unique-destination scoring (extension A17; not a SPEC metric) ------------------------
  * For up to 4 placements (W = 1 tables) and per chunk c:

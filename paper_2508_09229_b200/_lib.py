@@ -36,6 +36,9 @@ SIGNATURES = {
     "mp_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p]),
     "mp_token_hops_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p]),
     "mp_hist_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _i32, _p, _p, _p, _p]),
+    "mp_score_ex_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _i32, _p]),
+    "mp_hist_score_ex_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _i32,
+                                   _p]),
     "mp_score_dedup_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "mp_pack_server_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _p, _p]),
     "mp_apsp_bfs": (_i32, [_p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),

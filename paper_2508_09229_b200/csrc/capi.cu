@@ -5,7 +5,7 @@
 namespace mp {
 cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1,
                           int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
-                          int64_t* hop_sums, int64_t* err, cudaStream_t s);
+                          int64_t* hop_sums, int64_t* err, cudaStream_t s, int algo);
 cudaError_t launch_gen(uint64_t seed, int64_t t0, int64_t t1, int L, int K, int E, const uint32_t* cdf,
                        const uint8_t* perm, uint8_t* planes, int64_t stride, cudaStream_t s);
 cudaError_t launch_validate(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
@@ -96,7 +96,7 @@ int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, i
   if (r) return r;
   if (tok_end == tok_begin) return MP_OK;
   return status(mp::launch_stream(true, 0, 0, planes, plane_stride, tok_begin, tok_end, L, K, E, nullptr, 1, nullptr,
-                                  counts, nullptr, err, S(stream)));
+                                  counts, nullptr, err, S(stream), MP_ALGO_AUTO));
 }
 
 int mp_hist_chunks_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
@@ -124,17 +124,24 @@ int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int3
   return status(mp::launch_pack(cost, T, assign, topo_of, P, L, E, S_, tables, W, err, S(stream)));
 }
 
-int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
-                const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int max_p, int64_t* hop_sums,
-                void* stream) {
+int mp_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                   const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int max_p, int64_t* hop_sums,
+                   int algo, void* stream) {
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
   if (!chunk_bounds || C <= 0 || !tables || !hop_sums || !(W == 1 || W == 2 || W == 4)) return MP_ERR_ARG;
-  if (max_p < 0) return MP_ERR_ARG;
+  if (max_p < 0 || algo < MP_ALGO_AUTO || algo > MP_ALGO_COUNT) return MP_ERR_ARG;
   if (max_p > 255) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;
   return status(mp::launch_stream(false, W, max_p, planes, plane_stride, tok_begin, tok_end, L, K, 256, chunk_bounds,
-                                  C, tables, nullptr, hop_sums, nullptr, S(stream)));
+                                  C, tables, nullptr, hop_sums, nullptr, S(stream), algo));
+}
+
+int mp_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int max_p, int64_t* hop_sums,
+                void* stream) {
+  return mp_score_ex_u8(planes, plane_stride, tok_begin, tok_end, L, K, chunk_bounds, C, tables, W, max_p, hop_sums,
+                        MP_ALGO_AUTO, stream);
 }
 
 int mp_token_hops_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
@@ -148,17 +155,25 @@ int mp_token_hops_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
                                       S(stream)));
 }
 
-int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
-                     int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int max_p, int64_t* counts,
-                     int64_t* hop_sums, int64_t* err, void* stream) {
+int mp_hist_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                        int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int W, int max_p,
+                        int64_t* counts, int64_t* hop_sums, int64_t* err, int algo, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
   if (E <= 0 || !counts || !err || !chunk_bounds || C <= 0 || !tables || !hop_sums || max_p < 0) return MP_ERR_ARG;
-  if (max_p > 255) return MP_ERR_UNSUPPORTED;
+  if (!(W == 1 || W == 2 || W == 4) || algo < MP_ALGO_AUTO || algo > MP_ALGO_COUNT) return MP_ERR_ARG;
+  if (max_p > 255 || (algo == MP_ALGO_GATHER && W != 1)) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;
-  return status(mp::launch_stream(true, 1, max_p, planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C,
-                                  tables, counts, hop_sums, err, S(stream)));
+  return status(mp::launch_stream(true, W, max_p, planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C,
+                                  tables, counts, hop_sums, err, S(stream), algo));
+}
+
+int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
+                     int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int max_p, int64_t* counts,
+                     int64_t* hop_sums, int64_t* err, void* stream) {
+  return mp_hist_score_ex_u8(planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C, tables, 1, max_p,
+                             counts, hop_sums, err, MP_ALGO_AUTO, stream);
 }
 
 int mp_apsp_bfs(const int32_t* row_ptr, const int32_t* col, int n_nodes, const int32_t* src_nodes, int n_src,

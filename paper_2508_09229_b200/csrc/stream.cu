@@ -172,8 +172,15 @@ __device__ __forceinline__ int chunk_of(const int64_t* __restrict__ bounds, int 
 // Pieces are capped so one warp's hop sum over a piece fits u32 (64 MB / 16 warps x 255 < 2^32),
 // which lets the per-piece flush reduce-scatter u32 values.
 constexpr int64_t kMaxPiece = (int64_t)1 << 26;
+// Count-contract pieces are capped at 16 MB: a bin total times a u8 cost then fits u32, and so does
+// any warp's partial hop sum over a piece (2^24 * 255 < 2^32).
+constexpr int64_t kMaxContractPiece = (int64_t)1 << 24;
 
-template <bool HIST, int W, int WIDEN, int UNROLL, bool CHUNKED = false>
+// WC > 0 selects the count-contract algorithm (requires HIST, W == 0, CHUNKED): the trace is only
+// histogrammed, and at every piece flush (one layer x one chunk) the piece's bin totals are
+// contracted with the WC-word placement tables: hop_sums[q][c] += sum_e n[e] * pe[q][l][e].  Exact
+// by linearity, and the per-byte cost no longer depends on the number of placements.
+template <bool HIST, int W, int WIDEN, int UNROLL, bool CHUNKED = false, int WC = 0>
 __global__ void __launch_bounds__(kThreads, (W == 4 || W == 2) ? 2 : 3)
 stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
               const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
@@ -229,13 +236,51 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
       }
     };
 
+    // count-contract flush: two threads per bin (16 replicas each, rotated so a warp's 32 loads hit
+    // 32 banks), bin total -> counts (if requested) and x pe of every placement -> hop_sums[q][c]
+    constexpr int PC = 4 * (WC > 0 ? WC : 1);
+    const int fe = threadIdx.x >> 1, fh = threadIdx.x & 1;
+    uint32_t tw[WC > 0 ? WC : 1];
+    if constexpr (WC > 0) {
+#pragma unroll
+      for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
+    }
+    auto flush_contract = [&](int c) {
+      uint32_t n = 0;
+      if (fe < 256) {
+        uint32_t* row = smw + fe * 64 + 32;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int rr = (fh * 16 + i + fe) & 31;
+          n += row[rr];
+          row[rr] = 0;
+        }
+      }
+      n += __shfl_xor_sync(0xffffffffu, n, 1);
+      if (fh) n = 0;  // even lane of each pair owns the bin
+      if (n && counts) {
+        if (fe < E) atomic_add_i64(counts + (int64_t)l * E + fe, (int64_t)n);
+        else report_err(err, MP_DATA_EXPERT_RANGE, l, fe, n);
+      }
+      if (__any_sync(0xffffffffu, n != 0)) {
+        uint32_t v[PC];
+#pragma unroll
+        for (int w = 0; w < (WC > 0 ? WC : 1); ++w)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[4 * w + j] = n * ((tw[w] >> (8 * j)) & 0xffu);
+        int q = 0;
+        const uint32_t tot = warp_reduce_scatter<PC>(v, lane, &q);
+        if ((lane & (32 / PC - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
+      }
+    };
+
     if constexpr (W > 0 || CHUNKED) {
       // chunk of the segment's first byte by binary search, then walk forward (pieces are in order)
       int c = chunk_of(bounds, C, x0 / K);
       int64_t cend = __ldg(bounds + c + 1) * K;
       for (int64_t x = x0; x < x1;) {
         while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
-        const int64_t xe = min(min(x1, cend), x + kMaxPiece);
+        const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
         ScoreAcc<WW> acc;
         acc.zero();
         st.range(plane, x, xe, acc);
@@ -244,7 +289,11 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
           const uint32_t tot = warp_reduce_scatter<P>(acc.tot, lane, &q);
           if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
         }
-        if constexpr (CHUNKED) {  // per-chunk histogram: counts is [C][L][E]
+        if constexpr (CHUNKED && WC > 0) {
+          __syncthreads();
+          flush_contract(c);
+          __syncthreads();
+        } else if constexpr (CHUNKED) {  // per-chunk histogram: counts is [C][L][E]
           __syncthreads();
           flush_hist(counts + (int64_t)c * L * E);
           __syncthreads();
@@ -266,12 +315,12 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 
 constexpr int kSmemBytes = 256 * 256;
 
-template <bool HIST, int W, int WIDEN, bool CHUNKED = false>
+template <bool HIST, int W, int WIDEN, bool CHUNKED = false, int WC = 0>
 static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                             const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                             int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   constexpr int UNROLL = 4;
-  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED>;
+  auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED, WC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -343,12 +392,28 @@ cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int
   return cudaGetLastError();
 }
 
+// Which exact algorithm computes the hop sums: the per-byte gather costs one LDS per
+// lookup (1/2/4 wavefronts per 32 lookups for W = 1/2/4) on top of the histogram's ATOMS when both are
+// needed; count-contract costs only the histogram.  Measured (R1, 10M tokens): gather W=1 0.80 ms,
+// W=2 1.25, W=4 2.25, fused hist+gather 1.36; count-contract 0.91-0.93 for any W, with or without counts.
+int choose_algo(bool hist, int W, int algo) {
+  if (algo != MP_ALGO_AUTO) return algo;
+  return (hist || W > 1) ? MP_ALGO_COUNT : MP_ALGO_GATHER;
+}
+
 cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1,
                           int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
-                          int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+                          int64_t* hop_sums, int64_t* err, cudaStream_t s, int algo) {
 #define MP_ARGS planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s
   const int widen = max_p <= 15 ? 16 : max_p <= 63 ? 4 : 1;
   if (W == 0) return launch_t<true, 0, 16>(MP_ARGS);
+  if (choose_algo(hist, W, algo) == MP_ALGO_COUNT) {
+    if (!hist) counts = nullptr;  // histogram stays in shared memory
+    if (W == 1) return launch_t<true, 0, 16, true, 1>(MP_ARGS);
+    if (W == 2) return launch_t<true, 0, 16, true, 2>(MP_ARGS);
+    if (W == 4) return launch_t<true, 0, 16, true, 4>(MP_ARGS);
+    return cudaErrorInvalidValue;
+  }
   if (hist) {
     if (W == 1) {
       if (widen == 16) return launch_t<true, 1, 16>(MP_ARGS);

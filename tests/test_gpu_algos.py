@@ -1,0 +1,152 @@
+"""The two exact hop-sum algorithms behind mp_score_u8 / mp_hist_score_u8 (per-byte GATHER and
+COUNT-contract, include/moeplace_cuda.h) are bit-identical to each other and to the oracle
+(oracle/evaluate.py chunk_sums, oracle/stats.py counts) for every table width, on sub-ranges,
+empty chunks, pieces above the 16 MB contract cap, large costs and out-of-range ids."""
+import numpy as np
+import pytest
+
+import moeplace.eval as ev
+import moeplace.model_trace as mt
+import moeplace.placement as mpl
+from oracle import gen as og
+from oracle import stats as ost
+
+from helpers import B16, R1, oracle_sums, random_assign
+
+pytestmark = pytest.mark.gpu
+
+AUTO, GATHER, COUNT = 0, 1, 2
+
+
+def _tables(pls, p, m, W):
+    import torch
+    cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    return ev._group_tables(pls, [cost] * len(pls), m, W)
+
+
+def _run(tr, tables, W, max_p, algo, hist):
+    import torch
+    from paper_2508_09229_b200 import _lib
+    m = tr.model
+    C = len(tr.chunk_bounds) - 1
+    bounds = _lib.to_dev(tr.chunk_bounds, torch.int64)
+    sums = torch.zeros((4 * W, C), dtype=torch.int64, device="cuda")
+    counts = torch.zeros((m.L, m.E), dtype=torch.int64, device="cuda")
+    err = _lib.new_err()
+    stride = tr.planes.shape[1]
+    if hist:
+        _lib.call("mp_hist_score_ex_u8", _lib.ptr(tr.planes), stride, tr.tok_begin, tr.tok_end, m.L, m.K, m.E,
+                  _lib.ptr(bounds), C, _lib.ptr(tables), W, max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err),
+                  algo, _lib.stream_handle())
+    else:
+        _lib.call("mp_score_ex_u8", _lib.ptr(tr.planes), stride, tr.tok_begin, tr.tok_end, m.L, m.K,
+                  _lib.ptr(bounds), C, _lib.ptr(tables), W, max_p, _lib.ptr(sums), algo, _lib.stream_handle())
+    torch.cuda.synchronize()
+    return sums.cpu().numpy(), counts.cpu().numpy(), _lib.read_err(err)
+
+
+def _check(tr, sel, bounds, t0, pls, p, W, hist_ws=(1,)):
+    m = tr.model
+    tables, max_p = _tables(pls, p, m, W)
+    want = np.zeros((4 * W, len(bounds) - 1), np.int64)
+    for i, pl in enumerate(pls):
+        want[i] = oracle_sums(sel, p, pl.assign, bounds, t0)
+    for algo in (AUTO, GATHER, COUNT):
+        s, _, _ = _run(tr, tables, W, max_p, algo, hist=False)
+        assert np.array_equal(s, want), ("score", W, algo)
+        if W in hist_ws or algo != GATHER:
+            s, c, e = _run(tr, tables, W, max_p, algo, hist=True)
+            assert np.array_equal(s, want), ("hist_score", W, algo)
+            assert np.array_equal(c, ost.counts(sel, m.E)), ("counts", W, algo)
+            assert e[0] == 0
+
+
+@pytest.mark.parametrize("W", [1, 2, 4])
+@pytest.mark.parametrize("shape", [R1, B16, (3, 5, 2), (5, 200, 7)])
+def test_algorithms_agree_with_oracle(shape, W):
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    N, C = 5003, 17
+    tr = mt.generate_trace(m, 1.2, N, C, 3)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 3)
+    rng = np.random.default_rng(W)
+    S = 24
+    p = rng.integers(0, 13, (L, S)).astype(np.uint8)
+    pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(4 * W - (1 if W > 1 else 0))]
+    _check(tr, sel, bounds, 0, pls, p, W)
+    # a chunk sub-range view (token range starts mid-trace; plane byte offsets unaligned)
+    sub = tr.view(3, 11)
+    a, b = int(bounds[3]), int(bounds[11])
+    _check(sub, sel[a:b], bounds[3:12], a, pls, p, W)
+
+
+def test_algorithms_agree_on_empty_chunks_and_large_costs():
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 2.0, 90, 150, 1)  # N < C: many empty chunks
+    sel, bounds = og.generate(L, E, K, 2.0, 90, 150, 1)
+    rng = np.random.default_rng(5)
+    p = rng.integers(200, 256, (L, 8)).astype(np.uint8)
+    pls = [mpl.Placement(random_assign(rng, L, E, 8)) for _ in range(16)]
+    for W in (1, 2, 4):
+        _check(tr, sel, bounds, 0, pls[:4 * W], p, W)
+
+
+def test_count_contract_splits_pieces_above_cap():
+    """One layer x one chunk of 24 MB (> the 16 MB contract piece cap), costs up to 255: the
+    per-piece u32 partials must not overflow and the split pieces must add up exactly."""
+    L, E, K = 1, 256, 8
+    m = mt.ModelSpec(L, E, K)
+    N = 3_000_001
+    tr = mt.generate_trace(m, 0.0, N, 1, 9)
+    sel, bounds = og.generate(L, E, K, 0.0, N, 1, 9)
+    p = np.full((L, 4), 255, np.uint8)
+    p[0, 1] = 254
+    rng = np.random.default_rng(0)
+    pls = [mpl.Placement(random_assign(rng, L, E, 4)) for _ in range(4)]
+    _check(tr, sel, bounds, 0, pls, p, 1)
+
+
+def test_out_of_range_ids_same_result_both_algorithms():
+    """Ids >= E: not counted, reported as MP_DATA_EXPERT_RANGE, and they add 0 hops (table rows
+    e >= E are zero) -- identically for both algorithms."""
+    import torch
+    L, E, K = 4, 40, 4
+    m = mt.ModelSpec(L, E, K)
+    N, C = 777, 5
+    tr = mt.generate_trace(m, 1.2, N, C, 2)
+    planes = tr.planes.clone()
+    planes[2, 5 * K + 1] = 200  # token 5, layer 2
+    planes[0, 700 * K] = 41
+    bad = mt.ActivationTrace(m, planes, 0, N, tr.chunk_ids.copy(), tr.chunk_bounds.copy(), _validated=True)
+    rng = np.random.default_rng(3)
+    p = rng.integers(1, 9, (L, 8)).astype(np.uint8)
+    pls = [mpl.Placement(random_assign(rng, L, E, 8)) for _ in range(4)]
+    tables, max_p = _tables(pls, p, m, 1)
+    res = [_run(bad, tables, 1, max_p, algo, hist=True) for algo in (GATHER, COUNT)]
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    for s, c, e in res:
+        assert e[0] == 1  # MP_DATA_EXPERT_RANGE
+        assert c.sum() == N * L * K - 2
+    clean = planes.clone()
+    clean[2, 5 * K + 1] = 0
+    clean[0, 700 * K] = 0
+    sel = clean.cpu().numpy()[:, :N * K].reshape(L, N, K).transpose(1, 0, 2)
+    want = np.stack([oracle_sums(sel, p, pl.assign, tr.chunk_bounds) for pl in pls])
+    # the oracle sees id 0 where the bad ids were: subtract pe[l][0] for those two picks
+    for i, pl in enumerate(pls):
+        pe = p[np.arange(L)[:, None], pl.assign]
+        want[i, 0] -= pe[2, 0]
+        want[i, np.searchsorted(tr.chunk_bounds, 700, side="right") - 1] -= pe[0, 0]
+    assert np.array_equal(res[1][0][:4], want)
+
+
+def test_argument_rules_of_the_explicit_entry_points():
+    import torch
+    from paper_2508_09229_b200 import _lib
+    L = _lib.load()
+    x = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    P = x.data_ptr()
+    assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 2, 8, P, P, P, GATHER, None) == 3
+    assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 3, 8, P, P, P, COUNT, None) == 1
+    assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 8, P, 1, P, 1, 8, P, 7, None) == 1

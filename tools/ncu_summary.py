@@ -22,14 +22,22 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 
 
 def name_of(k):
-    if "stream_kernel<true, 1" in k or "stream_kernel<1, 1" in k:
-        return "fused"
-    if "stream_kernel<true, 0" in k or "stream_kernel<1, 0" in k:
-        return "hist"
-    for w in ("1", "2", "4"):
-        if f"stream_kernel<false, {w}" in k or f"stream_kernel<0, {w}" in k:
-            return "score" if w == "1" else f"score_w{w}"
-    return k[:40]
+    """stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED, WC> -> the bench's traffic keys."""
+    import re
+    mm = re.search(r"stream_kernel<(\w+), (\d+), \d+, \d+(?:, (\w+))?(?:, (\d+))?>", k)
+    if not mm:
+        return k[:40]
+    hist = mm.group(1) in ("true", "1")
+    W = int(mm.group(2))
+    chunked = (mm.group(3) or "false") in ("true", "1")
+    wc = int(mm.group(4) or 0)
+    if wc:  # count-contract: the fused step (W=1 tables) or score-only W=2/4
+        return "fused" if wc == 1 else f"score_w{wc}"
+    if hist and W == 0:
+        return "hist_chunks" if chunked else "hist"
+    if hist:
+        return "fused_gather"
+    return "score" if W == 1 else f"score_w{W}_gather"
 
 
 out, traffic = [], {}

@@ -17,7 +17,7 @@ from paper_2508_09229_b200 import _lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--tokens", type=int, default=10_000_000)
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--which", default="fused,hist,score1,score4")
+ap.add_argument("--which", default="fused,hist,score1,score4,fused_gather,score4_gather")
 a = ap.parse_args()
 L, E, K = 58, 256, 8
 m = mt.ModelSpec(L, E, K)
@@ -48,6 +48,12 @@ for _ in range(a.reps):
         elif w == "score1":
             _lib.call("mp_score_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t1), 1, mp1,
                       _lib.ptr(s), sh)
+        elif w == "fused_gather":
+            _lib.call("mp_hist_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t1), 1,
+                      mp1, _lib.ptr(cnt), _lib.ptr(s), _lib.ptr(err), 1, sh)
+        elif w == "score4_gather":
+            _lib.call("mp_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t4), 4, mp4,
+                      _lib.ptr(s), 1, sh)
         elif w == "score4":
             _lib.call("mp_score_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t4), 4, mp4,
                       _lib.ptr(s), sh)
