@@ -131,8 +131,16 @@ def _lanes_for(n: int) -> int:
     return 1 if n <= 4 else 2 if n <= 8 else 4
 
 
-def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs) -> np.ndarray:
-    """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_u8``)."""
+ALGOS = {"auto": 0, "gather": 1, "count": 2}  # include/moeplace_cuda.h MP_ALGO_*
+
+
+def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, algo: str = "auto") -> np.ndarray:
+    """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_ex_u8``), up to 16
+    placements per pass.  ``algo``: "gather" (per-byte table lookups), "count" (count-contract:
+    per-(layer, chunk) histograms contracted with the tables) or "auto" (the library's faster
+    choice); all three give the same integers."""
+    if algo not in ALGOS:
+        raise ConfigError(f"unknown score algorithm {algo!r}")
     t = _lib.torch()
     m = trace.model
     if m is None or trace.n_tokens == 0:
@@ -150,8 +158,8 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs) -
 
     def launch(planes, stride, t0, t1, bounds):
         for _, _, W, tables, max_p, sums in groups:
-            _lib.call("mp_score_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
-                      _lib.ptr(tables), W, max_p, _lib.ptr(sums), _lib.stream_handle())
+            _lib.call("mp_score_ex_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(sums), ALGOS[algo], _lib.stream_handle())
 
     sweep(trace, launch)
     out = np.zeros((len(placements), C), dtype=np.int64)
@@ -238,13 +246,17 @@ def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement
 
 
 def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs,
-                  method: str = "gather") -> list[EvalReport]:
-    """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies):
-    up to 16 placements per pass over the trace (extension A18).  ``method="factorized"`` uses
-    the per-chunk-histogram evaluator instead (identical integers)."""
+                  method: str = "auto") -> list[EvalReport]:
+    """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies),
+    extension A18.  ``method``: "gather" / "count" — streaming passes of up to 16 placements with
+    that algorithm; "factorized" — one per-chunk histogram pass + tensor-core contraction for any
+    number of placements; "auto" — one streaming pass when P <= 16, factorized above.  All give
+    identical integers."""
     placements = list(placements)
-    if method == "gather":
-        sums = score_sums(trace, placements, costs)
+    if method == "auto":
+        method = "pass" if len(placements) <= MAX_LANES else "factorized"
+    if method in ("gather", "count", "pass"):
+        sums = score_sums(trace, placements, costs, algo="auto" if method == "pass" else method)
     elif method == "factorized":
         sums = score_sums_factorized(trace, placements, costs)
     else:
@@ -259,27 +271,32 @@ def evaluate(trace: ActivationTrace, placement: Placement, cost: CostMatrix) -> 
     return evaluate_many(trace, [placement], cost)[0]
 
 
-def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement], cost: CostMatrix):
-    """One fused pass (``mp_hist_score_u8``): the trace's FrequencyTable plus the EvalReports of
-    up to 4 placements on one cost matrix.  Used for the train split, where the ILPLoad
-    frequencies and the train-side metric come from the same tokens."""
+def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement], cost, algo: str = "auto"):
+    """One fused pass (``mp_hist_score_ex_u8``): the trace's FrequencyTable plus the EvalReports of
+    up to 16 placements (``cost``: one CostMatrix or one per placement).  Used for the train
+    split, where the ILPLoad frequencies and the train-side metric come from the same tokens.
+    ``algo`` as in ``score_sums`` ("gather" takes at most 4 placements)."""
     t = _lib.torch()
     m = trace.model
     placements = list(placements)
     if m is None or trace.n_tokens == 0:
         raise MoeplaceError("evaluate: empty trace")
-    if not 1 <= len(placements) <= 4:
-        raise ConfigError("evaluate_with_stats takes 1..4 placements")
+    if algo not in ALGOS:
+        raise ConfigError(f"unknown score algorithm {algo!r}")
+    if not 1 <= len(placements) <= (4 if algo == "gather" else MAX_LANES):
+        raise ConfigError(f"evaluate_with_stats takes 1..{4 if algo == 'gather' else MAX_LANES} placements")
     dev = _lib.require_cuda()
-    tables, max_p = _group_tables(placements, [cost] * len(placements), m, 1)
+    W = _lanes_for(len(placements))
+    tables, max_p = _group_tables(placements, _as_costs(cost, len(placements)), m, W)
     C = trace.n_chunks
     counts = t.zeros((m.L, m.E), dtype=t.int64, device=dev)
-    sums = t.zeros((4, C), dtype=t.int64, device=dev)
+    sums = t.zeros((4 * W, C), dtype=t.int64, device=dev)
     err = _lib.new_err()
 
     def launch(planes, stride, t0, t1, bounds):
-        _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, m.E, _lib.ptr(bounds), C,
-                  _lib.ptr(tables), max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err), _lib.stream_handle())
+        _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, m.E, _lib.ptr(bounds), C,
+                  _lib.ptr(tables), W, max_p, _lib.ptr(counts), _lib.ptr(sums), _lib.ptr(err), ALGOS[algo],
+                  _lib.stream_handle())
 
     sweep(trace, launch)
     _lib.check_err(err, "evaluate_with_stats")

@@ -55,7 +55,7 @@ def sharded_evaluate(model, zipf_s: float, n_tokens: int, n_chunks: int, seed: i
     every placement (``costs``: one CostMatrix or one per placement — several topologies can be
     mixed), all-reduce ONE packed int64 buffer, and return the global
     (FrequencyTable, [EvalReport]) — identical on every rank and to a one-GPU run.
-    Placements 0..3 ride the fused statistics pass; further ones are scored 16 per gather pass."""
+    Placements 0..15 ride the fused statistics pass; further ones are scored 16 per pass."""
     import torch
     import torch.distributed as dist
 
@@ -82,14 +82,16 @@ def sharded_evaluate(model, zipf_s: float, n_tokens: int, n_chunks: int, seed: i
         bounds = _lib.to_dev(tr.chunk_bounds, torch.int64)
         err = _lib.new_err()
         sh = _lib.stream_handle()
-        head = placements[:4]
-        tables, max_p = _group_tables(head, costs[:4], model, 1)
-        sums = torch.zeros((4, n_chunks), dtype=torch.int64, device=dev)
-        _lib.call("mp_hist_score_u8", _lib.ptr(planes), stride, 0, b - a, model.L, model.K, model.E, _lib.ptr(bounds),
-                  n_chunks, _lib.ptr(tables), max_p, _lib.ptr(pk.counts), _lib.ptr(sums), _lib.ptr(err), sh)
+        head = placements[:MAX_LANES]
+        W = _lanes_for(len(head))
+        tables, max_p = _group_tables(head, costs[:MAX_LANES], model, W)
+        sums = torch.zeros((4 * W, n_chunks), dtype=torch.int64, device=dev)
+        _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, 0, b - a, model.L, model.K, model.E,
+                  _lib.ptr(bounds), n_chunks, _lib.ptr(tables), W, max_p, _lib.ptr(pk.counts), _lib.ptr(sums),
+                  _lib.ptr(err), 0, sh)
         _lib.check_err(err, "sharded_evaluate")
         pk.sums[:len(head)].copy_(sums[:len(head)])
-        for g0 in range(4, P, MAX_LANES):
+        for g0 in range(MAX_LANES, P, MAX_LANES):
             grp = placements[g0:g0 + MAX_LANES]
             W = _lanes_for(len(grp))
             tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], model, W)

@@ -150,3 +150,36 @@ def test_argument_rules_of_the_explicit_entry_points():
     assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 2, 8, P, P, P, GATHER, None) == 3
     assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 3, 8, P, P, P, COUNT, None) == 1
     assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 8, P, 1, P, 1, 8, P, 7, None) == 1
+
+
+def test_public_api_algorithms_and_wide_stats_pass():
+    """evaluate_many(method=auto|gather|count|factorized) and evaluate_with_stats with up to 16
+    placements over mixed topologies: identical integers, equal to the oracle."""
+    from moeplace.errors import ConfigError
+    from helpers import oracle_cost, setup_topology
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 3001, 12, 6)
+    sel, bounds = og.generate(L, E, K, 1.2, 3001, 12, 6)
+    costs, ps, pls = [], [], []
+    for i, kind in enumerate(["FatTree", "Dragonfly", "DragonflySparse", "FatTreeHier"]):
+        g, dist, order, attn, cost = setup_topology(kind, 4, 2, 4, m)
+        _, p = oracle_cost(g, attn)
+        for j in range(5):
+            pls.append(mpl.Placement(random_assign(np.random.default_rng(10 * i + j), L, E, g.n_devices)))
+            costs.append(cost)
+            ps.append(p)
+    want = np.stack([oracle_sums(sel, p, pl.assign, bounds) for p, pl in zip(ps, pls)])
+    for n in (5, 16, 20):
+        for method in ("auto", "gather", "count", "factorized"):
+            reps = ev.evaluate_many(tr, pls[:n], costs[:n], method=method)
+            assert [r.chunk_hop_sums for r in reps] == want[:n].tolist(), (n, method)
+    for n in (1, 4, 9, 16):
+        for algo in (("auto", "count", "gather") if n <= 4 else ("auto", "count")):
+            f, reps = ev.evaluate_with_stats(tr, pls[:n], costs[:n], algo=algo)
+            assert np.array_equal(f.counts, ost.counts(sel, E))
+            assert [r.chunk_hop_sums for r in reps] == want[:n].tolist(), (n, algo)
+    with pytest.raises(ConfigError):
+        ev.evaluate_with_stats(tr, pls[:5], costs[:5], algo="gather")
+    with pytest.raises(ConfigError):
+        ev.evaluate_with_stats(tr, pls[:17], costs[:17])
