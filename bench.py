@@ -333,6 +333,11 @@ def main():
 
     algo = {"auto": 0, "gather": 1, "count": 2}[args.algo]
 
+    def algo_used(hist: bool, W: int) -> str:  # mirrors choose_algo in csrc/stream.cu
+        if args.algo != "auto":
+            return {"gather": "gather", "count": "count-contract"}[args.algo]
+        return "count-contract" if (hist or W > 1) else "gather"
+
     def step(timed: bool):
         buf.zero_()
         if with_hist and fused:
@@ -453,7 +458,7 @@ def main():
                 "peak_source": peak_src}
     if with_hist and not fused:
         roofline["hist_ms"] = float(np.mean(kernel_ms[1]))
-    if wl == 4 or (wl == 3):
+    if wl in (3, 4) and algo_used(False, 4) == "gather":
         # shared-memory roofline for the W=4 gather: 4 LDS.128 wavefronts per 32 lookups + 4 LDG wavefronts
         # per 512 B, at 1 wavefront / SM / clock (sm_max_mhz)
         mhz = (clocks or {}).get("sm_mhz") or 1965.0
@@ -593,11 +598,6 @@ def main():
                    else f"trace {n * L * K / 1e6:.0f} MB < 126 MB L2: each step streams it {len(groups)}x; "
                         "first pass per step from HBM, reuse from L2",
                    "parallelism": f"token shards x{world}" + (" + 1 NCCL all_reduce" if world > 1 else "")}
-
-        def algo_used(hist: bool, W: int) -> str:  # mirrors choose_algo in csrc/stream.cu
-            if args.algo != "auto":
-                return args.algo
-            return "count-contract" if (hist or W > 1) else "gather"
         cfg["hop_sum_algorithm"] = (algo_used(True, 1) if fused else
                                     "/".join(sorted({algo_used(False, W) for W, _, _, _ in groups})))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
