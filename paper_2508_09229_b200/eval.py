@@ -196,7 +196,9 @@ def contract_tc(cnt, pe):
     """Exact hop sums [P, C] = pe [P, LE] (uint8) @ cnt^T [LE, C] (int64 counts) on the tensor cores:
     both operands are split into 7-bit digits (int8 >= 0), every digit pair is one int8 GEMM with
     int32 accumulation (cuBLASLt; exact since LE * 127^2 < 2^31 for LE <= 133,000), and the
-    partial products are recombined in int64 with weights 128^(a+b)."""
+    partial products are recombined in int64 with weights 128^(a+b).  pe (the large operand for
+    big candidate batches) is split straight from uint8 into at most two digits, without padding
+    copies when P and LE are already GEMM-aligned."""
     t = _lib.torch()
     P, LE = pe.shape
     C = cnt.shape[0]
@@ -204,16 +206,27 @@ def contract_tc(cnt, pe):
         raise ConfigError("contract_tc: L*E too large for exact int32 accumulation")
     Pp, Cp = max(32, -(-P // 32) * 32), max(8, -(-C // 8) * 8)
     LEp = max(16, -(-LE // 16) * 16)  # cuBLASLt int8: K a multiple of 16 (zero padding is exact)
-    pe_w = pe.to(t.int64)
     out = t.zeros((P, C), dtype=t.int64, device=pe.device)
-    da, db = _digits(cnt), _digits(pe_w)
-    A = t.zeros((Pp, LEp), dtype=t.int8, device=pe.device)
+    da = _digits(cnt)
+    db = 1 if int(pe.max().item()) < 128 else 2
+
+    def pe_digit(b):
+        d = pe if db == 1 else ((pe & 127) if b == 0 else (pe >> 7))
+        if (Pp, LEp) == (P, LE):
+            return d.view(t.int8)  # values < 128: the uint8 bits are the int8 value
+        A = t.zeros((Pp, LEp), dtype=t.int8, device=pe.device)
+        A[:P, :LE].copy_(d.view(t.int8))
+        return A
+
     B = t.zeros((Cp, LEp), dtype=t.int8, device=pe.device)  # B^T row-major == B column-major
+    Bd = []
+    for a in range(da):
+        B[:C, :LE].copy_(((cnt >> (7 * a)) & 127).to(t.int8))
+        Bd.append(B.clone() if a + 1 < da else B)
     for b in range(db):
-        A[:P, :LE].copy_(((pe_w >> (7 * b)) & 127).to(t.int8))
+        A = pe_digit(b)
         for a in range(da):
-            B[:C, :LE].copy_(((cnt >> (7 * a)) & 127).to(t.int8))
-            part = t._int_mm(A, B.t())  # int32 [Pp, Cp], exact
+            part = t._int_mm(A, Bd[a].t())  # int32 [Pp, Cp], exact
             out += part[:P, :C].to(t.int64) << (7 * (a + b))
     return out
 

@@ -490,12 +490,14 @@ def test_factorized_evaluator_matches_gather(shape):
     assert [r.chunk_hop_sums for r in ra] == [r.chunk_hop_sums for r in rb]
 
 
-def test_contract_tc_digit_paths():
-    """Exact tensor-core contraction with multi-digit operands (pe up to 255, counts up to 2^20)."""
+@pytest.mark.parametrize("P,LE,C,pe_hi", [(37, 1000, 11, 256), (37, 1000, 11, 128), (64, 1024, 8, 256),
+                                          (64, 1024, 13, 100), (4096, 14848, 150, 13)])
+def test_contract_tc_digit_paths(P, LE, C, pe_hi):
+    """Exact tensor-core contraction with multi-digit operands (pe up to 255, counts up to 2^20),
+    padded and GEMM-aligned (no-copy) operand shapes."""
     import torch
-    rng = np.random.default_rng(0)
-    P, LE, C = 37, 1000, 11
-    pe = torch.as_tensor(rng.integers(0, 256, (P, LE)).astype(np.uint8), device="cuda")
+    rng = np.random.default_rng(P + C)
+    pe = torch.as_tensor(rng.integers(0, pe_hi, (P, LE)).astype(np.uint8), device="cuda")
     cnt = torch.as_tensor(rng.integers(0, 2 ** 20, (C, LE)), device="cuda")
     got = ev.contract_tc(cnt, pe).cpu().numpy()
     want = pe.cpu().numpy().astype(np.int64) @ cnt.cpu().numpy().T
