@@ -183,3 +183,46 @@ def test_public_api_algorithms_and_wide_stats_pass():
         ev.evaluate_with_stats(tr, pls[:5], costs[:5], algo="gather")
     with pytest.raises(ConfigError):
         ev.evaluate_with_stats(tr, pls[:17], costs[:17])
+
+
+def test_plane_offsets_beyond_2_pow_31():
+    """One plane longer than 2^31 bytes (N*K = 2.4e9): 64-bit byte offsets through every piece
+    of both algorithms.  Properties: per-layer counts sum to N*K, constant costs give exactly
+    p*N*L*K, gather == count, the histogram.table identity holds, and a CPU-regenerated window
+    at the far end of the plane matches the oracle."""
+    import torch
+    L, E, K = 2, 256, 8
+    m = mt.ModelSpec(L, E, K)
+    N, C = 300_000_000, 40
+    tr = mt.generate_trace(m, 1.2, N, C, 4)
+    assert tr.planes.shape[1] >= N * K > 2 ** 31
+    rng = np.random.default_rng(2)
+    S = 16
+    p = rng.integers(0, 40, (L, S)).astype(np.uint8)
+    pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(4)]
+    tables, max_p = _tables(pls, p, m, 1)
+    sg, cg, eg = _run(tr, tables, 1, max_p, GATHER, hist=True)
+    sc, cc, ec = _run(tr, tables, 1, max_p, COUNT, hist=True)
+    assert eg[0] == 0 and ec[0] == 0
+    assert np.array_equal(cg, cc) and (cc.sum(axis=1) == N * K).all()
+    assert np.array_equal(sg, sc)
+    for i, pl in enumerate(pls):
+        pe = p[np.arange(L)[:, None], pl.assign]
+        assert int((cc * pe).sum()) == int(sc[i].sum())
+    const = np.full((L, S), 7, np.uint8)
+    t7, _ = _tables(pls[:1], const, m, 1)
+    s7, _, _ = _run(tr, t7, 1, 7, COUNT, hist=False)
+    assert int(s7[0].sum()) == 7 * N * L * K
+    a, b = N - 20_000, N
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 4, tok_range=(a, b))
+    sh = mt.generate_trace(m, 1.2, N, C, 4, tok_range=(a, b))
+    assert np.array_equal(sh.tokens(), sel)
+    want = oracle_sums(sel, p, pls[0].assign, bounds, a)
+    tail = tr.view(C - 1, C)
+    tables0, mp0 = _tables(pls[:1], p, m, 1)
+    # the last chunk of the big trace, restricted to [a, b): equals the oracle window
+    sub = mt.ActivationTrace(m, tail.planes, a, b - a, tail.chunk_ids.copy(),
+                             np.array([a, b], dtype=np.int64), _validated=True)
+    for algo in (GATHER, COUNT):
+        s, _, _ = _run(sub, tables0, 1, mp0, algo, hist=False)
+        assert int(s[0].sum()) == int(want.sum()), algo
