@@ -52,12 +52,13 @@ template <bool HIST, int W, int WIDEN, int UNROLL>
 struct Stream {
   static constexpr int P = 4 * W;
   uint32_t base;   // shared address of row 0
+  uint32_t hbase;  // shared address of row 0's histogram replicas (base + 128, or base for set B)
   uint32_t slot;   // lane's score slot (byte 0 of the row offset)
   uint32_t hslot;  // lane's histogram slot
 
   // single byte (heads/tails of ranges; rare)
   __device__ __forceinline__ void one(uint32_t e, ScoreAcc<(W > 0 ? W : 1)>& acc) {
-    if constexpr (HIST) atoms_inc(base + ((e << 8) | hslot) + 128);
+    if constexpr (HIST) atoms_inc(hbase + ((e << 8) | hslot));
     if constexpr (W > 0) {
       uint32_t t[W];
       table_load<W>(base + ((e << 8) | slot), t);
@@ -87,7 +88,7 @@ struct Stream {
           for (int w = 0; w < W; ++w) acc8[w] += t[w];
           if constexpr (HIST) {
             const uint32_t hoff = (W == 1) ? off : prmt(wd[q], hslot, sel_row(b));
-            atoms_inc(base + hoff + 128);
+            atoms_inc(hbase + hoff);
           }
           if (((q * 4 + b + 1) % WIDEN) == 0) {
 #pragma unroll
@@ -99,7 +100,7 @@ struct Stream {
           }
         } else {
           const uint32_t off = prmt(wd[q], hslot, sel_row(b));
-          atoms_inc(base + off + 128);
+          atoms_inc(hbase + off);
         }
       }
     }
@@ -191,10 +192,19 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
   const int lane = threadIdx.x & 31;
   Stream<HIST, W, WIDEN, UNROLL> st;
   st.base = smem_addr(sm);
+  st.hbase = st.base + 128;
   st.slot = W == 4 ? (uint32_t)((lane & 7) << 4) : W == 2 ? (uint32_t)(lane << 3) : (uint32_t)(lane << 2);
   st.hslot = (uint32_t)(lane << 2);
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
 
+  // count-contract alternates pieces between two replica sets (set A = bytes 128..255 of each row,
+  // set B = bytes 0..127, free since there are no gather tables): a piece's flush reads and zeroes
+  // its set while the next piece already counts into the other one, so one barrier per piece
+  // suffices and no per-segment zeroing is needed.
+  int hset = 0;
+  if constexpr (WC > 0) {
+    for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) smw[i] = 0;
+  }
   Flat f(t0 * K, t1 * K, L);
   for (int64_t g = f.g0; g < f.g1;) {
     const int l = (int)(g / f.nb);
@@ -213,7 +223,7 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
         smw[e * 64 + j] = __ldg(tl + e * W + (j % W));
       }
     }
-    if constexpr (HIST) {
+    if constexpr (HIST && WC == 0) {
       for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) smw[(i >> 5) * 64 + 32 + (i & 31)] = 0;
     }
     __syncthreads();
@@ -245,10 +255,10 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 #pragma unroll
       for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
     }
-    auto flush_contract = [&](int c) {
+    auto flush_contract = [&](int c, int set) {
       uint32_t n = 0;
       if (fe < 256) {
-        uint32_t* row = smw + fe * 64 + 32;
+        uint32_t* row = smw + fe * 64 + (set ? 0 : 32);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int rr = (fh * 16 + i + fe) & 31;
@@ -283,6 +293,7 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
         const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
         ScoreAcc<WW> acc;
         acc.zero();
+        if constexpr (WC > 0) st.hbase = st.base + (hset ? 0u : 128u);
         st.range(plane, x, xe, acc);
         if constexpr (W > 0) {
           int q = 0;
@@ -290,9 +301,9 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
           if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
         }
         if constexpr (CHUNKED && WC > 0) {
-          __syncthreads();
-          flush_contract(c);
-          __syncthreads();
+          __syncthreads();  // every warp's ATOMS into set hset are done
+          flush_contract(c, hset);
+          hset ^= 1;        // the next piece counts into the other set; no second barrier
         } else if constexpr (CHUNKED) {  // per-chunk histogram: counts is [C][L][E]
           __syncthreads();
           flush_hist(counts + (int64_t)c * L * E);
