@@ -18,12 +18,14 @@ namespace mp {
 
 constexpr int kDedupMaxK = 32;
 
-// 0x80 in every byte where a == b (exact per byte, no borrow between lanes)
-__device__ __forceinline__ uint32_t bytes_eq(uint32_t a, uint32_t b) {
+// bit 7 of every byte set where a == b (exact per byte, no borrow between lanes); the other bits
+// are garbage -- callers mask with 0x80808080 once, after OR-ing several of these together
+__device__ __forceinline__ uint32_t bytes_eq7(uint32_t a, uint32_t b) {
   const uint32_t x = a ^ b;
   const uint32_t t = (x & 0x7f7f7f7fu) + 0x7f7f7f7fu;
-  return ~(t | x | 0x7f7f7f7fu);
+  return ~(t | x);
 }
+__device__ __forceinline__ uint32_t bytes_eq(uint32_t a, uint32_t b) { return bytes_eq7(a, b) & 0x80808080u; }
 
 // K = 8 record, all 4 placements at once (byte lanes): SPEC hops and dedup hops widened into u16
 // lanes ({q0,q2}, {q1,q3}), unique remote destination servers as u8 lanes (<= 8 per record).
@@ -41,7 +43,7 @@ __device__ __forceinline__ void dedup_record8(uint2 v, uint32_t base, uint32_t s
   for (int k = 0; k < 8; ++k) {
     uint32_t seen = 0;
 #pragma unroll
-    for (int j = 0; j < k; ++j) seen |= bytes_eq(sw[k], sw[j]);
+    for (int j = 0; j < k; ++j) seen |= bytes_eq7(sw[k], sw[j]);
     const uint32_t first = ~seen & 0x80808080u;   // 0x80 where the pick's server is new in the record
     const uint32_t m = pw[k] & ((first >> 7) * 0xffu);
     hop16[0] += pw[k] & 0x00ff00ffu;
@@ -52,7 +54,47 @@ __device__ __forceinline__ void dedup_record8(uint2 v, uint32_t base, uint32_t s
   }
 }
 
-__global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0,
+constexpr int kDedupThreads = 512;
+
+// Fast K = 8 record for pe bytes <= 31 and server ids < 128 (checked per layer by the CTA): with bit
+// 7 of every server byte clear, t = ((a ^ b) | 0x80808080) - 0x01010101 has bit 7 of a byte set iff
+// the bytes differ (each byte of (a^b)|0x80 is >= 0x80, so subtracting 1 never borrows across
+// bytes), so "new server" = AND of t over the earlier picks; a record's hop and dedup sums fit u8
+// lanes (8 * 31 < 256); the dedup mask is PRMT's sign-replicate of the first-occurrence bytes; the
+// source server is removed once per record (distinct servers - [src in set]).
+__device__ __forceinline__ uint32_t bytes_ne7(uint32_t a, uint32_t b) {
+  return ((a ^ b) | 0x80808080u) - 0x01010101u;
+}
+__device__ __forceinline__ void dedup_record8_fast(uint2 v, uint32_t base, uint32_t slot, uint32_t src4,
+                                                   uint32_t (&hop16)[2], uint32_t& uq8, uint32_t (&dd16)[2]) {
+  const uint32_t wv[2] = {v.x, v.y};
+  uint32_t sw[8], pw[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t a = base + prmt(wv[k >> 2], slot, sel_row(k & 3));
+    pw[k] = lds32(a);
+    sw[k] = lds32(a + 128);
+  }
+  uint32_t h8 = 0, d8 = 0, n8 = 0, notsrc = 0xffffffffu;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t nw = 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < k; ++j) nw &= bytes_ne7(sw[k], sw[j]);
+    const uint32_t first = nw & 0x80808080u;
+    h8 += pw[k];
+    d8 += pw[k] & prmt(first, 0u, 0xBA98u);  // 0xff in bytes whose server is new in the record
+    n8 += first >> 7;
+    notsrc &= bytes_ne7(sw[k], src4);
+  }
+  uq8 += n8 - ((~notsrc & 0x80808080u) >> 7);  // distinct remote destination servers per lane
+  hop16[0] += h8 & 0x00ff00ffu;
+  hop16[1] += (h8 >> 8) & 0x00ff00ffu;
+  dd16[0] += d8 & 0x00ff00ffu;
+  dd16[1] += (d8 >> 8) & 0x00ff00ffu;
+}
+
+__global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0,
                                                     int64_t t1, int L, int K, const int64_t* __restrict__ bounds,
                                                     int C, const uint32_t* __restrict__ tables,
                                                     const uint32_t* __restrict__ srv_tables,
@@ -75,17 +117,21 @@ __global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ 
     const int64_t r1 = min(t0 + n, r0 + (g1 - g));
     const uint8_t* plane = planes + (int64_t)l * stride;
     __syncthreads();
+    uint32_t wide = 0;  // any pe byte > 31 or server id >= 128 in this layer -> exact general path
     for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
       const int e = i >> 5, j = i & 31;
-      smw[e * 64 + j] = __ldg(tables + (int64_t)l * 256 + e);
-      smw[e * 64 + 32 + j] = __ldg(srv_tables + (int64_t)l * 256 + e);
+      const uint32_t pw = __ldg(tables + (int64_t)l * 256 + e), sw = __ldg(srv_tables + (int64_t)l * 256 + e);
+      smw[e * 64 + j] = pw;
+      smw[e * 64 + 32 + j] = sw;
+      wide |= (pw & 0xe0e0e0e0u) | (sw & 0x80808080u);
     }
     if (threadIdx.x == 0) {
       uint32_t w = 0;
       for (int q = 0; q < 4; ++q) w |= (uint32_t)src_srv[q * L + l] << (8 * q);
       s_src = w;
+      wide |= w & 0x80808080u;
     }
-    __syncthreads();
+    const bool fast = __syncthreads_or(wide != 0) == 0;
     const uint32_t src = s_src;
     int c = 0;
     {
@@ -103,24 +149,55 @@ __global__ void __launch_bounds__(256) dedup_kernel(const uint8_t* __restrict__ 
       const int64_t te = min(r1, cend);
       uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};
       if (K == 8) {
-        // SIMD-within-a-register path; lane sums are widened every 32 records (u16: 32*8*255 < 2^16)
+        // SIMD-within-a-register path over 16-byte vectors (two records each), 4 vectors in flight
+        // per thread; lane sums are widened every main-loop iteration (8 records, u16 lanes:
+        // 8*8*255 < 2^16) and after every single-record step
         uint32_t h16[2] = {0, 0}, d16[2] = {0, 0}, u8 = 0;
-        int cnt = 0;
-        for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
-          dedup_record8(__ldg(reinterpret_cast<const uint2*>(plane + r * 8)), base, slot, src, h16, u8, d16);
-          if (++cnt == 31) {
-            hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
-            dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
+        auto widen = [&]() {
+          hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
+          dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
-            h16[0] = h16[1] = d16[0] = d16[1] = u8 = 0;
-            cnt = 0;
-          }
+          for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
+          h16[0] = h16[1] = d16[0] = d16[1] = u8 = 0;
+        };
+        auto rec8 = [&](uint2 w, uint32_t b_, uint32_t s_, uint32_t src_, uint32_t (&h_)[2], uint32_t& u_,
+                        uint32_t (&d_)[2]) {
+          if (fast) dedup_record8_fast(w, b_, s_, src_, h_, u_, d_);
+          else dedup_record8(w, b_, s_, src_, h_, u_, d_);
+        };
+        const int64_t va = (t + 1) >> 1, vb = te >> 1;  // full vectors cover records [2va, 2vb)
+        const int T = blockDim.x;
+        if ((t & 1) && threadIdx.x == 0) {  // lone head record
+          rec8(__ldg(reinterpret_cast<const uint2*>(plane + t * 8)), base, slot, src, h16, u8, d16);
+          widen();
         }
-        hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
-        dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
+        if ((te & 1) && te - 1 > t && threadIdx.x == T - 1) {  // lone tail record
+          rec8(__ldg(reinterpret_cast<const uint2*>(plane + (te - 1) * 8)), base, slot, src, h16, u8, d16);
+          widen();
+        }
+        const uint4* __restrict__ pv = reinterpret_cast<const uint4*>(plane);
+        int64_t v = va + threadIdx.x;
+        for (; v + 3 * T < vb; v += 4 * T) {
+          uint4 x[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
+          for (int u = 0; u < 4; ++u) {
+            const int4 r = ldg_stream(pv + v + u * T);
+            x[u] = make_uint4((uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            rec8(make_uint2(x[u].x, x[u].y), base, slot, src, h16, u8, d16);
+            rec8(make_uint2(x[u].z, x[u].w), base, slot, src, h16, u8, d16);
+          }
+          widen();
+        }
+        for (; v < vb; v += T) {
+          const int4 r = ldg_stream(pv + v);
+          const uint4 x = make_uint4((uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w);
+          rec8(make_uint2(x.x, x.y), base, slot, src, h16, u8, d16);
+          rec8(make_uint2(x.z, x.w), base, slot, src, h16, u8, d16);
+          widen();
+        }
       } else
       for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
         uint32_t ids[kDedupMaxK];
@@ -170,11 +247,11 @@ cudaError_t launch_dedup(const uint8_t* planes, int64_t stride, int64_t t0, int6
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dedup_kernel, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dedup_kernel, kDedupThreads, smem);
   const int64_t records = (t1 - t0) * (int64_t)L;
   int64_t grid = (int64_t)nsm * max(1, per_sm);
   grid = max((int64_t)1, min(grid, (records + 4095) / 4096));
-  dedup_kernel<<<(unsigned)grid, 256, smem, s>>>(planes, stride, t0, t1, L, K, bounds, C, tables, srv_tables, src_srv,
+  dedup_kernel<<<(unsigned)grid, kDedupThreads, smem, s>>>(planes, stride, t0, t1, L, K, bounds, C, tables, srv_tables, src_srv,
                                                  hop_sums, uniq_sums, dedup_sums);
   return cudaGetLastError();
 }

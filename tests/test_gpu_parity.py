@@ -345,13 +345,17 @@ def test_host_streaming_matches_device(monkeypatch):
     assert not host.planes.is_cuda  # streamed, not cached on the device
 
 
-@pytest.mark.parametrize("shape,kind", [(R1, "FatTree"), (B16, "Dragonfly"), ((3, 16, 5), "DragonflySparse")])
-def test_dedup_matches_oracle(shape, kind):
+@pytest.mark.parametrize("shape,kind,size", [
+    (R1, "FatTree", (4, 2, 4)), (B16, "Dragonfly", (4, 2, 4)), ((3, 16, 5), "DragonflySparse", (4, 2, 4)),
+    # K = 8 general path: pe bytes up to 36 in some layers (fast and general layers mixed), and
+    # 130 servers (ids >= 128)
+    (R1, "DragonflySparse", (64, 1, 1)), (R1, "FatTree", (65, 2, 1))])
+def test_dedup_matches_oracle(shape, kind, size):
     """Extension A17: unique destination servers and deduplicated hops, bit-exact vs the oracle;
     the SPEC hop sums produced alongside equal mp_score_u8's."""
     L, E, K = shape
     m = mt.ModelSpec(L, E, K)
-    g, dist, order, attn, cost = setup_topology(kind, 4, 2, 4, m)
+    g, dist, order, attn, cost = setup_topology(kind, *size, m)
     _, p = oracle_cost(g, attn)
     tr = mt.generate_trace(m, 1.2, 2345, 9, 6)
     sel, bounds = og.generate(L, E, K, 1.2, 2345, 9, 6)
