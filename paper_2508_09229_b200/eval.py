@@ -103,19 +103,42 @@ def _unique_costs(costs: Sequence[CostMatrix]):
     return uniq, topo_of
 
 
+def _stack_assign(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec) -> np.ndarray:
+    """int32 [P, L, E] assignments; shapes checked, and every expert placed on a device of its own
+    placement's topology (cost matrices of different sizes can share one batch)."""
+    out = np.empty((len(placements), model.L, model.E), dtype=np.int32)
+    for i, (pl, c) in enumerate(zip(placements, costs)):
+        a = np.asarray(pl.assign)
+        if a.shape != (model.L, model.E):
+            raise ConfigError(f"placement shape {a.shape} != model [{model.L}, {model.E}]")
+        if a.size and (int(a.min()) < 0 or int(a.max()) >= c.S):
+            raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {i}, {c.S} devices)")
+        out[i] = a
+    return out
+
+
+def _padded_costs(uniq: Sequence[CostMatrix], model: ModelSpec):
+    """uint8 [T, L, S_max]: the distinct cost matrices, zero-padded to the widest topology."""
+    t = _lib.torch()
+    S = max(c.S for c in uniq)
+    for c in uniq:
+        if c.L != model.L:
+            raise ConfigError(f"cost matrix has {c.L} layers, model has {model.L}")
+    if all(c.S == S for c in uniq):
+        return t.stack([c.p for c in uniq]).contiguous(), S
+    cost = t.zeros((len(uniq), model.L, S), dtype=t.uint8, device=uniq[0].p.device)
+    for i, c in enumerate(uniq):
+        cost[i, :, :c.S] = c.p
+    return cost, S
+
+
 def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec, W: int):
     """Pack one group (<= 4W placements) into device tables uint32 [L, 256, W]."""
     t = _lib.torch()
     dev = _lib.require_cuda()
     uniq, topo_of = _unique_costs(costs)
-    S = uniq[0].S
-    for c in uniq:
-        if c.S != S or c.L != model.L:
-            raise ConfigError(f"cost matrix shape [{c.L}, {c.S}] inconsistent with [{model.L}, {S}]")
-    cost = t.stack([c.p for c in uniq]).contiguous()
-    assign = np.stack([p.assign for p in placements])
-    if assign.shape[1:] != (model.L, model.E):
-        raise ConfigError(f"placement shape {assign.shape[1:]} != model [{model.L}, {model.E}]")
+    cost, S = _padded_costs(uniq, model)
+    assign = _stack_assign(placements, costs, model)
     d_assign = _lib.to_dev(assign, t.int32)
     d_topo = _lib.to_dev(np.asarray(topo_of, dtype=np.int32), t.int32)
     tables = t.empty((model.L, 256, W), dtype=t.int32, device=dev)
@@ -169,17 +192,20 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, a
 
 
 def pe_matrix(placements: Sequence[Placement], costs, model: ModelSpec):
-    """uint8 [P, L*E] per-expert round-trip costs pe_q[l, e] = p_q[l, assign_q[l, e]] on the device."""
+    """uint8 [P, L*E] per-expert round-trip costs pe_q[l, e] = p_q[l, assign_q[l, e]] on the device
+    (one batched gather per distinct cost matrix)."""
     t = _lib.torch()
     placements = list(placements)
     costs = _as_costs(costs, len(placements))
     dev = _lib.require_cuda()
+    assign = _lib.to_dev(_stack_assign(placements, costs, model), t.int64)
+    uniq, topo_of = _unique_costs(costs)
+    topo_of = np.asarray(topo_of)
     out = t.empty((len(placements), model.L * model.E), dtype=t.uint8, device=dev)
-    for i, (pl, c) in enumerate(zip(placements, costs)):
-        a = _lib.to_dev(pl.assign, t.int64)
-        if int(a.min()) < 0 or int(a.max()) >= c.S:
-            raise MoeplaceError("evaluate: expert placed outside the topology")
-        out[i] = t.gather(c.p, 1, a).reshape(-1)
+    for ti, c in enumerate(uniq):
+        idx = t.as_tensor(np.flatnonzero(topo_of == ti), device=dev)
+        sel = assign.index_select(0, idx)
+        out[idx] = t.gather(c.p.unsqueeze(0).expand(len(idx), -1, -1), 2, sel).reshape(len(idx), -1)
     return out
 
 
@@ -354,9 +380,12 @@ def evaluate_dedup(trace: ActivationTrace, placements: Sequence[Placement], cost
                 raise ConfigError("evaluate_dedup needs cost matrices built by cost_matrix(dist, attn)")
         tables, max_p = _group_tables(grp, gcost, m, 1)
         uniq, topo_of = _unique_costs(gcost)
-        S = uniq[0].S
-        server_of = _lib.to_dev(np.stack([c.dist.graph.device_server for c in uniq]).astype(np.int32), t.int32)
-        d_assign = _lib.to_dev(np.stack([p.assign for p in grp]), t.int32)
+        S = max(c.S for c in uniq)
+        srv = np.zeros((len(uniq), S), dtype=np.int32)  # zero-padded to the widest topology
+        for i, c in enumerate(uniq):
+            srv[i, :c.S] = c.dist.graph.device_server
+        server_of = _lib.to_dev(srv, t.int32)
+        d_assign = _lib.to_dev(_stack_assign(grp, gcost, m), t.int32)
         d_topo = _lib.to_dev(np.asarray(topo_of, dtype=np.int32), t.int32)
         srv_tables = t.empty((m.L, 256), dtype=t.int32, device=dev)
         err = _lib.new_err()

@@ -226,3 +226,46 @@ def test_plane_offsets_beyond_2_pow_31():
     for algo in (GATHER, COUNT):
         s, _, _ = _run(sub, tables0, 1, mp0, algo, hist=False)
         assert int(s[0].sum()) == int(want.sum()), algo
+
+
+def test_mixed_topology_sizes_in_one_batch():
+    """Cost matrices of different device counts (256 and 64 devices) share one batch: the tables
+    are zero-padded to the widest topology and every placement is range-checked against its own."""
+    from moeplace.errors import ConfigError, MoeplaceError
+    from helpers import oracle_cost, setup_topology
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 2222, 7, 5)
+    sel, bounds = og.generate(L, E, K, 1.2, 2222, 7, 5)
+    ga, _, _, attn_a, cost_a = setup_topology("FatTree", 8, 4, 8, m)
+    gb, _, _, attn_b, cost_b = setup_topology("Dragonfly", 8, 2, 4, m)
+    assert ga.n_devices == 256 and gb.n_devices == 64
+    pa, pb = oracle_cost(ga, attn_a)[1], oracle_cost(gb, attn_b)[1]
+    rng = np.random.default_rng(4)
+    pls, costs, ps, gs = [], [], [], []
+    for i in range(6):
+        g, c, p = (ga, cost_a, pa) if i % 2 == 0 else (gb, cost_b, pb)
+        pls.append(mpl.Placement(random_assign(rng, L, E, g.n_devices)))
+        costs.append(c)
+        ps.append(p)
+        gs.append(g)
+    want = np.stack([oracle_sums(sel, p, pl.assign, bounds) for p, pl in zip(ps, pls)])
+    for method in ("auto", "gather", "count", "factorized"):
+        reps = ev.evaluate_many(tr, pls, costs, method=method)
+        assert [r.chunk_hop_sums for r in reps] == want.tolist(), method
+    f, reps = ev.evaluate_with_stats(tr, pls, costs)
+    assert [r.chunk_hop_sums for r in reps] == want.tolist()
+    from oracle import evaluate as oe
+    dreps = ev.evaluate_dedup(tr, pls[:4], costs[:4])
+    for i in range(4):
+        g, c = gs[i], costs[i]
+        pe = oe.pe_table(ps[i], pls[i].assign)
+        h, u, d = oe.dedup_sums(sel, pe, g.device_server[pls[i].assign], g.device_server[c.attn.dispatch], bounds)
+        assert dreps[i].spec.chunk_hop_sums == h.tolist()
+        assert dreps[i].chunk_uniq_sums == u.tolist() and dreps[i].chunk_dedup_sums == d.tolist()
+    # a device index valid for the 256-device topology but not for the 64-device one
+    bad = mpl.Placement(np.full((L, E), 100, np.int32))
+    with pytest.raises(MoeplaceError):
+        ev.evaluate_many(tr, [pls[0], bad], [cost_a, cost_b])
+    with pytest.raises(ConfigError):
+        ev.evaluate_many(tr, [mpl.Placement(np.zeros((L, E - 1), np.int32))], cost_a)
