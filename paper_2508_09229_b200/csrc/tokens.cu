@@ -11,6 +11,10 @@
 
 namespace mp {
 
+#ifndef MP_TOK_PF
+#define MP_TOK_PF 1
+#endif
+
 constexpr int kTokThreads = 512;
 constexpr int kTPT = 8;                   // tokens per thread per tile -> 4096-token tiles
 constexpr int kRowBytes = 128;            // 32 lanes x 4 B
@@ -29,21 +33,22 @@ __global__ void replicate_kernel(const uint32_t* __restrict__ tables, int L, uin
     rep[i] = tables[i >> 5];
 }
 
-template <bool K8, bool SMALLP>
-__global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* __restrict__ planes, int64_t stride,
+template <bool K8, int ACC>
+__global__ void __launch_bounds__(kTokThreads, 2) token_hops_kernel(const uint8_t* __restrict__ planes, int64_t stride,
                                                                  int64_t t0, int64_t n, int L, int K,
                                                                  const uint32_t* __restrict__ rep,
                                                                  uint32_t* __restrict__ hops) {
-  extern __shared__ __align__(128) uint8_t sm[];  // 2 x (256 rows x 128 B)
+  // 256 rows x 256 B: row e holds expert e's replicated word of table buffer 0 at bytes [0, 128)
+  // and of buffer 1 at [128, 256), so PRMT's (e << 8) | lane*4 is the address with no shift
+  extern __shared__ __align__(128) uint8_t sm[];
   const int lane = threadIdx.x & 31;
   const uint32_t base0 = smem_addr(sm);
-  const uint32_t slot8 = (uint32_t)(lane << 3);  // PRMT -> (e << 8) | (lane << 3); >> 1 -> e*128 + lane*4
   const uint32_t slot = (uint32_t)(lane << 2);
   const int64_t tile = (int64_t)kTPT * blockDim.x;
   auto fetch = [&](int l, int buf) {  // async copy of layer l's replicated table into buffer buf
     const uint8_t* src = reinterpret_cast<const uint8_t*>(rep) + (int64_t)l * kTabBytes;
-    for (int i = threadIdx.x; i < kTabBytes / 16; i += blockDim.x)
-      cp_async16(base0 + buf * kTabBytes + i * 16, src + i * 16);
+    for (int i = threadIdx.x; i < kTabBytes / 16; i += blockDim.x)  // 8 x 16 B per expert row
+      cp_async16(base0 + (i >> 3) * 256 + buf * kRowBytes + (i & 7) * 16, src + i * 16);
     cp_async_commit();
   };
   for (int64_t ta = (int64_t)blockIdx.x * tile; ta < n; ta += (int64_t)gridDim.x * tile) {
@@ -55,8 +60,19 @@ __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* 
     for (int l = 0; l < L; ++l) {
       cp_async_wait_all();
       __syncthreads();  // layer l's table visible; buffer (l+1)&1 free
-      if (l + 1 < L) fetch(l + 1, (l + 1) & 1);
-      const uint32_t base = base0 + (l & 1) * kTabBytes;
+      if (l + 1 < L) {
+        fetch(l + 1, (l + 1) & 1);
+#if MP_TOK_PF
+        // pull layer l+1's slice of this tile into L2 while layer l is gathered
+        if (threadIdx.x == 0) {
+          const uintptr_t a0 = reinterpret_cast<uintptr_t>(planes + (int64_t)(l + 1) * stride + (t0 + ta) * K);
+          const uintptr_t a1 = reinterpret_cast<uintptr_t>(planes + (int64_t)(l + 1) * stride + (t0 + min(n, ta + tile)) * K);
+          const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;
+          if (hi > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
+        }
+#endif
+      }
+      const uint32_t base = base0 + (l & 1) * kRowBytes;
       const uint8_t* plane = planes + (int64_t)l * stride + (t0 + ta) * K;
       if constexpr (K8) {
         uint2 v[kTPT];
@@ -68,22 +84,25 @@ __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* 
 #pragma unroll
         for (int j = 0; j < kTPT; ++j) {
           const uint32_t wv[2] = {v[j].x, v[j].y};
+          uint32_t w[8];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t s8 = 0;
+          for (int k = 0; k < 8; ++k) w[k] = lds32(base + prmt(wv[k >> 2], slot, sel_row(k & 3)));
+          if constexpr (ACC == 8) {  // max_p <= 31: a token's 8 lookups fit u8 lanes
+            const uint32_t s8 = (w[0] + w[1] + w[2]) + (w[3] + w[4] + w[5]) + (w[6] + w[7]);
+            acc[j][0] += s8 & 0x00ff00ffu;
+            acc[j][1] += (s8 >> 8) & 0x00ff00ffu;
+          } else if constexpr (ACC == 4) {  // max_p <= 63: 4 lookups per u8 lane
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const uint32_t w = lds32(base + (prmt(wv[h], slot8, sel_row(b)) >> 1));
-              if constexpr (SMALLP) {
-                s8 += w;  // 4 lookups x max_p <= 63 fit a u8 lane
-              } else {
-                acc[j][0] += w & 0x00ff00ffu;
-                acc[j][1] += (w >> 8) & 0x00ff00ffu;
-              }
-            }
-            if constexpr (SMALLP) {
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t s8 = (w[4 * h] + w[4 * h + 1] + w[4 * h + 2]) + w[4 * h + 3];
               acc[j][0] += s8 & 0x00ff00ffu;
               acc[j][1] += (s8 >> 8) & 0x00ff00ffu;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              acc[j][0] += w[k] & 0x00ff00ffu;
+              acc[j][1] += (w[k] >> 8) & 0x00ff00ffu;
             }
           }
         }
@@ -94,7 +113,7 @@ __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* 
           if (ta + i >= n) continue;
           for (int k = 0; k < K; ++k) {
             const uint32_t e = plane[i * K + k];
-            const uint32_t w = lds32(base + e * kRowBytes + slot);
+            const uint32_t w = lds32(base + e * 256 + slot);
             acc[j][0] += w & 0x00ff00ffu;
             acc[j][1] += (w >> 8) & 0x00ff00ffu;
           }
@@ -114,15 +133,15 @@ __global__ void __launch_bounds__(kTokThreads) token_hops_kernel(const uint8_t* 
   }
 }
 
-template <bool K8, bool SMALLP>
+template <bool K8, int ACC>
 static void run_token_hops(int64_t tiles, int nsm, const uint8_t* planes, int64_t stride, int64_t t0, int64_t n,
                            int L, int K, const uint32_t* rep, uint32_t* hops, cudaStream_t s) {
-  const int smem = 2 * kTabBytes;
+  const int smem = 256 * 256;  // two interleaved table buffers
   int per_sm = 0;
-  cudaFuncSetAttribute(token_hops_kernel<K8, SMALLP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, token_hops_kernel<K8, SMALLP>, kTokThreads, smem);
+  cudaFuncSetAttribute(token_hops_kernel<K8, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, token_hops_kernel<K8, ACC>, kTokThreads, smem);
   const int64_t grid = max((int64_t)1, min(tiles, (int64_t)nsm * max(1, per_sm)));
-  token_hops_kernel<K8, SMALLP><<<(unsigned)grid, kTokThreads, smem, s>>>(planes, stride, t0, n, L, K, rep, hops);
+  token_hops_kernel<K8, ACC><<<(unsigned)grid, kTokThreads, smem, s>>>(planes, stride, t0, n, L, K, rep, hops);
 }
 
 cudaError_t launch_token_hops(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
@@ -136,9 +155,10 @@ cudaError_t launch_token_hops(const uint8_t* planes, int64_t stride, int64_t t0,
   const int64_t nrep = (int64_t)L * 256 * 32;
   replicate_kernel<<<(unsigned)min((nrep + 255) / 256, (int64_t)4096), 256, 0, s>>>(tables, L, replicated);
   const int64_t tiles = (n + (int64_t)kTPT * kTokThreads - 1) / ((int64_t)kTPT * kTokThreads);
-  if (K == 8 && max_p <= 63) run_token_hops<true, true>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
-  else if (K == 8) run_token_hops<true, false>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
-  else run_token_hops<false, false>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
+  if (K == 8 && max_p <= 31) run_token_hops<true, 8>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
+  else if (K == 8 && max_p <= 63) run_token_hops<true, 4>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
+  else if (K == 8) run_token_hops<true, 1>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
+  else run_token_hops<false, 1>(tiles, nsm, planes, stride, t0, n, L, K, replicated, hops, s);
   return cudaGetLastError();
 }
 

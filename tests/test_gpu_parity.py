@@ -434,7 +434,9 @@ def test_device_parser_R1_scale(tmp_path):
 
 
 @pytest.mark.parametrize("shape,kind,maxp", [(R1, "FatTree", None), (B16, "DragonflySparse", None),
-                                             ((5, 32, 8), None, 200), ((3, 64, 3), None, 100)])
+                                             ((5, 32, 8), None, 200), ((3, 64, 3), None, 100),
+                                             # K = 8 accumulation widths: u8 per token (<= 31), per 4 (<= 63)
+                                             ((4, 64, 8), None, 31), ((4, 64, 8), None, 50), ((4, 64, 8), None, 63)])
 def test_token_hops_all_matches_oracle(shape, kind, maxp):
     """Per-token hops of every token (token-tiled kernel) == the oracle's per-token sums; chunk
     sums of them == the streaming scorer's."""
@@ -452,6 +454,7 @@ def test_token_hops_all_matches_oracle(shape, kind, maxp):
     else:
         S = 16
         p = rng.integers(0, maxp + 1, (L, S)).astype(np.uint8)
+        p[0, 0] = maxp  # pin the accumulation-width boundary
         cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
     pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(6)]
     got = ev.token_hops_all(tr, pls, cost)
