@@ -109,3 +109,26 @@ def test_commmap_mass_equals_mean(seed, kind):
     rep = ev.evaluate(tr, pl, cost)
     assert abs(cm.traffic.sum() - rep.mean_hops_per_token) <= 1e-9 * max(1.0, rep.mean_hops_per_token)
     assert np.allclose(cm.traffic, cm.traffic.T) and (np.diag(cm.traffic) == 0).all()
+
+
+@settings(**SETTINGS)
+@given(case(), st.sampled_from([1, 2, 4]), st.sampled_from([9, 31, 63, 255]), st.integers(1, 40))
+def test_gather_and_count_contract_agree(c, W, hi, S):
+    """The two exact hop-sum algorithms (per-byte gather, count-contract) and the oracle agree on
+    random shapes, table widths and cost ranges, with and without the fused histogram."""
+    from oracle import evaluate as oe
+    from oracle import stats as ost
+    L, E, K, N, C, seed, s = c
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, s, N, C, seed)
+    sel = tr.tokens()
+    rng = np.random.default_rng(seed % 997)
+    cost, p = _cost(rng, L, S, hi)
+    pls = [mpl.Placement(rng.integers(0, S, (L, E)).astype(np.int32)) for _ in range(4 * W)]
+    want = np.stack([oe.chunk_sums(sel, oe.pe_table(p, pl.assign), tr.chunk_bounds) for pl in pls])
+    for algo in ("gather", "count"):
+        assert np.array_equal(ev.score_sums(tr, pls, cost, algo=algo), want), algo
+    n = 4 if W == 1 else 4 * W
+    f, reps = ev.evaluate_with_stats(tr, pls[:n], cost, algo="count")
+    assert np.array_equal(f.counts, ost.counts(sel, E))
+    assert [r.chunk_hop_sums for r in reps] == want[:n].tolist()
