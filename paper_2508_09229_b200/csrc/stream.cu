@@ -325,12 +325,21 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 }
 
 constexpr int kSmemBytes = 256 * 256;
+// Vectors per thread per main-loop iteration (R1, 10M tokens, B200): histogram / count-contract
+// instances 2: 0.894 / 4: 0.895 / 8: 0.846 / 16: 0.840 / 32: 0.843 ms (hist), fused step 0.936 ->
+// 0.886 ms at 16; gather instances 2: 0.963 / 4: 0.795 / 8: 0.770-0.787 / 16: 0.796 ms (score W=1).
+#ifndef MP_COUNT_UNROLL
+#define MP_COUNT_UNROLL 16
+#endif
+#ifndef MP_GATHER_UNROLL
+#define MP_GATHER_UNROLL 8
+#endif
 
 template <bool HIST, int W, int WIDEN, bool CHUNKED = false, int WC = 0>
 static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                             const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                             int64_t* hop_sums, int64_t* err, cudaStream_t s) {
-  constexpr int UNROLL = 4;
+  constexpr int UNROLL = W == 0 ? MP_COUNT_UNROLL : MP_GATHER_UNROLL;  // vectors per thread per iteration
   auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED, WC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;

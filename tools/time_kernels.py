@@ -47,17 +47,20 @@ sh = _lib.stream_handle()
 
 
 def run(w):
+    """fused / hist / scoreW (library's algorithm) and fused_gather / scoreW_gather (forced gather)."""
+    algo = 1 if w.endswith("_gather") else 0
+    w = w.replace("_gather", "")
     if w == "fused":
         t, mp_ = tabs[1]
-        _lib.call("mp_hist_score_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t), mp_,
-                  _lib.ptr(cnt), _lib.ptr(s), _lib.ptr(err), sh)
+        _lib.call("mp_hist_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t), 1, mp_,
+                  _lib.ptr(cnt), _lib.ptr(s), _lib.ptr(err), algo, sh)
     elif w == "hist":
         _lib.call("mp_hist_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(cnt), _lib.ptr(err), sh)
     else:
         W = int(w[-1])
         t, mp_ = tabs[W]
-        _lib.call("mp_score_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t), W, mp_,
-                  _lib.ptr(s), sh)
+        _lib.call("mp_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t), W, mp_,
+                  _lib.ptr(s), algo, sh)
 
 
 hops_out = torch.empty((4, a.tokens), dtype=torch.int32, device="cuda")
@@ -88,7 +91,7 @@ def run_ext(w):
 res = {}
 bytes_ = a.tokens * L * K
 for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup")):
-    fn = run if w in ("hist", "score1", "score2", "score4", "fused") else run_ext
+    fn = run if w.replace("_gather", "") in ("hist", "score1", "score2", "score4", "fused") else run_ext
     for _ in range(3):
         fn(w)
     ts = []
