@@ -15,8 +15,19 @@ namespace mp {
 #define MP_TOK_PF 1
 #endif
 
-constexpr int kTokThreads = 512;
-constexpr int kTPT = 8;                   // tokens per thread per tile -> 4096-token tiles
+// Tile shape (R1, 10M tokens): 512 threads x 8 tokens, 2 CTAs/SM = 1.18 ms; 512 x 16 (1 CTA/SM)
+// 1.26, 256 x 16 (3 CTAs) 1.23, 256 x 8 (3 CTAs) 1.28, 512 x 4 1.46 ms.
+#ifndef MP_TOK_THREADS
+#define MP_TOK_THREADS 512
+#endif
+#ifndef MP_TOK_TPT
+#define MP_TOK_TPT 8
+#endif
+#ifndef MP_TOK_MINB
+#define MP_TOK_MINB 2
+#endif
+constexpr int kTokThreads = MP_TOK_THREADS;
+constexpr int kTPT = MP_TOK_TPT;          // tokens per thread per tile (512 x 8 -> 4096-token tiles)
 constexpr int kRowBytes = 128;            // 32 lanes x 4 B
 constexpr int kTabBytes = 256 * kRowBytes;  // 32 KB per layer
 
@@ -34,7 +45,7 @@ __global__ void replicate_kernel(const uint32_t* __restrict__ tables, int L, uin
 }
 
 template <bool K8, int ACC>
-__global__ void __launch_bounds__(kTokThreads, 2) token_hops_kernel(const uint8_t* __restrict__ planes, int64_t stride,
+__global__ void __launch_bounds__(kTokThreads, MP_TOK_MINB) token_hops_kernel(const uint8_t* __restrict__ planes, int64_t stride,
                                                                  int64_t t0, int64_t n, int L, int K,
                                                                  const uint32_t* __restrict__ rep,
                                                                  uint32_t* __restrict__ hops) {
