@@ -1,4 +1,4 @@
-"""Multi-rank path on CPU: world-size 2 (and 4) gloo process groups.  Each rank computes its
+"""Multi-rank path on CPU: world-size 2, 4 and 8 gloo process groups.  Each rank computes its
 shard's integer partials with the oracle (no GPU here), packs them into the product's single
 int64 buffer and all-reduces; the result must equal the single-process oracle bit for bit."""
 import os
@@ -46,7 +46,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_gloo_sharded_partials_equal_single(world):
     from oracle import evaluate as oe
     from oracle import gen as og
