@@ -119,9 +119,12 @@ class ActivationTrace:
     def to_host(self, pin: bool = True) -> "ActivationTrace":
         """A copy whose planes live in (pinned) host memory: evaluating it streams the trace
         through the device slice by slice (the end-to-end path), without caching it there."""
-        h = self.planes.cpu()
-        if pin:
-            h = h.pin_memory()
+        t = _lib.torch()
+        if pin:  # allocate pinned and copy once (no pageable intermediate: half the peak host memory)
+            h = t.empty(self.planes.shape, dtype=self.planes.dtype, pin_memory=True)
+            h.copy_(self.planes)
+        else:
+            h = self.planes.cpu()
         return ActivationTrace(self.model, h, self.tok_begin, self.n_tokens, self.chunk_ids.copy(),
                                self.chunk_bounds.copy(), self.source_is_file, self._validated)
 
