@@ -47,6 +47,15 @@ __device__ __forceinline__ void table_load(uint32_t a, uint32_t (&t)[W]) {
 #ifndef MP_PF_AHEAD
 #define MP_PF_AHEAD 0
 #endif
+// Vectors per thread per main-loop iteration (R1, 10M tokens, B200): histogram / count-contract
+// instances 2: 0.894 / 4: 0.895 / 8: 0.846 / 16: 0.840 / 32: 0.843 ms (hist), fused step 0.936 ->
+// 0.886 ms at 16; gather instances 2: 0.963 / 4: 0.795 / 8: 0.770-0.787 / 16: 0.796 ms (score W=1).
+#ifndef MP_COUNT_UNROLL
+#define MP_COUNT_UNROLL 16
+#endif
+#ifndef MP_GATHER_UNROLL
+#define MP_GATHER_UNROLL 8
+#endif
 
 template <bool HIST, int W, int WIDEN, int UNROLL>
 struct Stream {
@@ -55,6 +64,8 @@ struct Stream {
   uint32_t hbase;  // shared address of row 0's histogram replicas (base + 128, or base for set B)
   uint32_t slot;   // lane's score slot (byte 0 of the row offset)
   uint32_t hslot;  // lane's histogram slot
+  uint32_t tid;    // this thread's index among the streaming threads
+  uint32_t nth;    // number of streaming threads
 
   // single byte (heads/tails of ranges; rare)
   __device__ __forceinline__ void one(uint32_t e, ScoreAcc<(W > 0 ? W : 1)>& acc) {
@@ -126,15 +137,15 @@ struct Stream {
     constexpr int WW = W > 0 ? W : 1;
     const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
     const int64_t tb = max(ha, xb & ~(int64_t)15);
-    for (int64_t x = xa + threadIdx.x; x < ha; x += blockDim.x) one(plane[x], acc);
-    for (int64_t x = tb + threadIdx.x; x < xb; x += blockDim.x) one(plane[x], acc);
+    for (int64_t x = xa + tid; x < ha; x += nth) one(plane[x], acc);
+    for (int64_t x = tb + tid; x < xb; x += nth) one(plane[x], acc);
     const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
     const uint32_t nv = (uint32_t)((tb - ha) >> 4);
-    const uint32_t T = blockDim.x;
+    const uint32_t T = nth;
     uint32_t acc16[2 * WW];
 #pragma unroll
     for (int i = 0; i < 2 * WW; ++i) acc16[i] = 0;
-    uint32_t v = threadIdx.x;
+    uint32_t v = tid;
     // main loop: UNROLL vectors in flight per thread, no bounds checks; one thread keeps the
     // CTA's trace region PF_AHEAD iterations ahead prefetched into L2
     const uint32_t step_bytes = UNROLL * T * 16u;
@@ -153,7 +164,19 @@ struct Stream {
       for (int u = 0; u < UNROLL; ++u) vec(x[u], acc16);
       widen(acc16, acc);
     }
-    for (; v < nv; v += T) {  // tail: fewer than UNROLL vectors left for this thread
+    // tail: fewer than UNROLL vectors left for this thread -- guard-free batches of 4 first (several
+    // loads per round trip), then single vectors
+    if constexpr (UNROLL > 4) {
+      for (; v + 3 * T < nv; v += 4 * T) {
+        int4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = ldg_stream(pv + v + u * T);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) vec(x[u], acc16);
+        widen(acc16, acc);
+      }
+    }
+    for (; v < nv; v += T) {
       vec(ldg_stream(pv + v), acc16);
       widen(acc16, acc);
     }
@@ -193,6 +216,8 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
   Stream<HIST, W, WIDEN, UNROLL> st;
   st.base = smem_addr(sm);
   st.hbase = st.base + 128;
+  st.tid = threadIdx.x;
+  st.nth = blockDim.x;
   st.slot = W == 4 ? (uint32_t)((lane & 7) << 4) : W == 2 ? (uint32_t)(lane << 3) : (uint32_t)(lane << 2);
   st.hslot = (uint32_t)(lane << 2);
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
@@ -325,15 +350,6 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 }
 
 constexpr int kSmemBytes = 256 * 256;
-// Vectors per thread per main-loop iteration (R1, 10M tokens, B200): histogram / count-contract
-// instances 2: 0.894 / 4: 0.895 / 8: 0.846 / 16: 0.840 / 32: 0.843 ms (hist), fused step 0.936 ->
-// 0.886 ms at 16; gather instances 2: 0.963 / 4: 0.795 / 8: 0.770-0.787 / 16: 0.796 ms (score W=1).
-#ifndef MP_COUNT_UNROLL
-#define MP_COUNT_UNROLL 16
-#endif
-#ifndef MP_GATHER_UNROLL
-#define MP_GATHER_UNROLL 8
-#endif
 
 template <bool HIST, int W, int WIDEN, bool CHUNKED = false, int WC = 0>
 static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,

@@ -22,6 +22,7 @@ ap.add_argument("--s", type=float, default=1.2)
 ap.add_argument("--out")
 ap.add_argument("--lib", help="load this libmoeplace_cuda.so variant instead of the product build")
 ap.add_argument("--only", default="")
+ap.add_argument("--chunks", type=int, default=150)
 a = ap.parse_args()
 if a.lib:
     from pathlib import Path
@@ -35,7 +36,7 @@ attn = mt.default_attention_placement(m, order)
 cost = mpl.cost_matrix(d, attn)
 c = mpl.Constraints(64, 1)
 pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c)] * 8
-tr = mt.generate_trace(m, a.s, a.tokens, 150, 0)
+tr = mt.generate_trace(m, a.s, a.tokens, a.chunks, 0)
 P, st = tr.planes, tr.planes.shape[1]
 C = tr.n_chunks
 b = _lib.to_dev(tr.chunk_bounds, torch.int64)
