@@ -253,3 +253,17 @@ def test_plain_c_client_of_the_abi(tmp_path):
     env = dict(__import__("os").environ, LD_LIBRARY_PATH=str(root / "paper_2508_09229_b200" / "lib"))
     r = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=120)
     assert r.returncode == 0 and "capi_client ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_readme_example_runs():
+    """The README's Python snippet runs as written (the first thing a switching user tries)."""
+    import re
+    from pathlib import Path
+    text = (Path(__file__).resolve().parent.parent / "README.md").read_text()
+    blocks = re.findall(r"```python\n(.*?)```", text, flags=re.S)
+    assert blocks, "README has no python example"
+    ns = {}
+    exec(compile(blocks[0], "README.md", "exec"), ns)
+    reps = ns["reports"]
+    assert len(reps) == 2 and all(r.mean_hops_per_token > 0 for r in reps)
+    assert reps[1].mean_hops_per_token <= reps[0].mean_hops_per_token  # ILPLoad beats round-robin
