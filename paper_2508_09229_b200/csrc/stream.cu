@@ -432,10 +432,15 @@ cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int
 // lookup (1/2/4 wavefronts per 32 lookups for W = 1/2/4) on top of the histogram's ATOMS when both are
 // needed; count-contract costs only the histogram.  Measured (R1, 10M tokens): gather W=1 0.80 ms,
 // W=2 1.25, W=4 2.25, fused hist+gather 1.36; count-contract 0.91-0.93 for any W, with or without counts.
-int choose_algo(bool hist, int W, int algo) {
+int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K, int max_p) {
   if (algo != MP_ALGO_AUTO) return algo;
+  if (tokens < (int64_t)MP_TOKEN_CHUNK_TOKENS * C && (int64_t)L * K * max_p <= 65535) return MP_ALGO_TOKEN;
   return (hist || W > 1) ? MP_ALGO_COUNT : MP_ALGO_GATHER;
 }
+
+cudaError_t launch_score_tok(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
+                             const int64_t* bounds, int C, const uint32_t* tables, int W, int max_p, int64_t* hop_sums,
+                             cudaStream_t s);
 
 cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1,
                           int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
@@ -443,7 +448,16 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
 #define MP_ARGS planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s
   const int widen = max_p <= 15 ? 16 : max_p <= 63 ? 4 : 1;
   if (W == 0) return launch_t<true, 0, 16>(MP_ARGS);
-  if (choose_algo(hist, W, algo) == MP_ALGO_COUNT) {
+  const int chosen = choose_algo(hist, W, algo, t1 - t0, C, L, K, max_p);
+  if (chosen == MP_ALGO_TOKEN) {
+    if (hist) {  // histogram pass (per-layer flushes only) + the token-tiled scorer
+      const cudaError_t e = launch_t<true, 0, 16>(planes, stride, t0, t1, L, K, E, nullptr, 1, nullptr, counts, nullptr,
+                                                   err, s);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_score_tok(planes, stride, t0, t1, L, K, bounds, C, tables, W, max_p, hop_sums, s);
+  }
+  if (chosen == MP_ALGO_COUNT) {
     if (!hist) counts = nullptr;  // histogram stays in shared memory
     if (W == 1) return launch_t<true, 0, 16, true, 1>(MP_ARGS);
     if (W == 2) return launch_t<true, 0, 16, true, 2>(MP_ARGS);

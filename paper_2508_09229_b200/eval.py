@@ -154,14 +154,15 @@ def _lanes_for(n: int) -> int:
     return 1 if n <= 4 else 2 if n <= 8 else 4
 
 
-ALGOS = {"auto": 0, "gather": 1, "count": 2}  # include/moeplace_cuda.h MP_ALGO_*
+ALGOS = {"auto": 0, "gather": 1, "count": 2, "token": 3}  # include/moeplace_cuda.h MP_ALGO_*
 
 
 def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, algo: str = "auto") -> np.ndarray:
     """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_ex_u8``), up to 16
     placements per pass.  ``algo``: "gather" (per-byte table lookups), "count" (count-contract:
-    per-(layer, chunk) histograms contracted with the tables) or "auto" (the library's faster
-    choice); all three give the same integers."""
+    per-(layer, chunk) histograms contracted with the tables), "token" (token-tiled: per-token sums
+    across layers reduced per chunk; cost independent of the chunk count) or "auto" (the library's
+    choice for the shape); all give the same integers."""
     if algo not in ALGOS:
         raise ConfigError(f"unknown score algorithm {algo!r}")
     t = _lib.torch()

@@ -15,7 +15,7 @@ from helpers import B16, R1, oracle_sums, random_assign
 
 pytestmark = pytest.mark.gpu
 
-AUTO, GATHER, COUNT = 0, 1, 2
+AUTO, GATHER, COUNT, TOKEN = 0, 1, 2, 3
 
 
 def _tables(pls, p, m, W):
@@ -51,7 +51,8 @@ def _check(tr, sel, bounds, t0, pls, p, W, hist_ws=(1,)):
     want = np.zeros((4 * W, len(bounds) - 1), np.int64)
     for i, pl in enumerate(pls):
         want[i] = oracle_sums(sel, p, pl.assign, bounds, t0)
-    for algo in (AUTO, GATHER, COUNT):
+    algos = (AUTO, GATHER, COUNT) + ((TOKEN,) if m.L * m.K * max_p <= 65535 else ())
+    for algo in algos:
         s, _, _ = _run(tr, tables, W, max_p, algo, hist=False)
         assert np.array_equal(s, want), ("score", W, algo)
         if W in hist_ws or algo != GATHER:
@@ -123,8 +124,9 @@ def test_out_of_range_ids_same_result_both_algorithms():
     p = rng.integers(1, 9, (L, 8)).astype(np.uint8)
     pls = [mpl.Placement(random_assign(rng, L, E, 8)) for _ in range(4)]
     tables, max_p = _tables(pls, p, m, 1)
-    res = [_run(bad, tables, 1, max_p, algo, hist=True) for algo in (GATHER, COUNT)]
-    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    res = [_run(bad, tables, 1, max_p, algo, hist=True) for algo in (GATHER, COUNT, TOKEN)]
+    for r in res[1:]:
+        assert np.array_equal(res[0][0], r[0]) and np.array_equal(res[0][1], r[1])
     for s, c, e in res:
         assert e[0] == 1  # MP_DATA_EXPERT_RANGE
         assert c.sum() == N * L * K - 2
@@ -223,7 +225,7 @@ def test_plane_offsets_beyond_2_pow_31():
     # the last chunk of the big trace, restricted to [a, b): equals the oracle window
     sub = mt.ActivationTrace(m, tail.planes, a, b - a, tail.chunk_ids.copy(),
                              np.array([a, b], dtype=np.int64), _validated=True)
-    for algo in (GATHER, COUNT):
+    for algo in (GATHER, COUNT, TOKEN):
         s, _, _ = _run(sub, tables0, 1, mp0, algo, hist=False)
         assert int(s[0].sum()) == int(want.sum()), algo
 
@@ -269,3 +271,42 @@ def test_mixed_topology_sizes_in_one_batch():
         ev.evaluate_many(tr, [pls[0], bad], [cost_a, cost_b])
     with pytest.raises(ConfigError):
         ev.evaluate_many(tr, [mpl.Placement(np.zeros((L, E - 1), np.int32))], cost_a)
+
+
+@pytest.mark.parametrize("tokens_per_chunk", [1, 3, 31, 33, 700])
+@pytest.mark.parametrize("W", [1, 4])
+def test_token_algorithm_on_fine_chunks(tokens_per_chunk, W):
+    """Chunks of a few tokens: many 32-token warp groups straddle several chunks (segmented scan),
+    and AUTO picks the token-tiled algorithm; every algorithm equals the oracle."""
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    N = 9001
+    C = max(1, N // tokens_per_chunk)
+    tr = mt.generate_trace(m, 1.2, N, C, 7)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 7)
+    rng = np.random.default_rng(tokens_per_chunk)
+    p = rng.integers(0, 60, (L, 16)).astype(np.uint8)
+    pls = [mpl.Placement(random_assign(rng, L, E, 16)) for _ in range(4 * W)]
+    _check(tr, sel, bounds, 0, pls, p, W)
+    sub = tr.view(C // 3, C - C // 5)
+    a = int(bounds[C // 3])
+    _check(sub, sel[a:int(bounds[C - C // 5])], bounds[C // 3:C - C // 5 + 1], a, pls, p, W)
+
+
+def test_token_algorithm_limit():
+    """Per-token sums must fit u16 lanes: L*K*max_p > 65535 is refused for TOKEN and avoided by AUTO."""
+    import torch
+    from paper_2508_09229_b200 import _lib
+    L, E, K = R1
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 500, 400, 1)  # fine chunks: AUTO would prefer TOKEN
+    sel, bounds = og.generate(L, E, K, 1.2, 500, 400, 1)
+    rng = np.random.default_rng(0)
+    p = rng.integers(100, 256, (L, 8)).astype(np.uint8)  # 58*8*255 > 65535
+    pls = [mpl.Placement(random_assign(rng, L, E, 8)) for _ in range(4)]
+    tables, max_p = _tables(pls, p, m, 1)
+    with pytest.raises(Exception):
+        _run(tr, tables, 1, max_p, TOKEN, hist=False)
+    s, _, _ = _run(tr, tables, 1, max_p, AUTO, hist=False)
+    want = np.stack([oracle_sums(sel, p, pl.assign, bounds) for pl in pls])
+    assert np.array_equal(s, want)

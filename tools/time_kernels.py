@@ -49,8 +49,10 @@ sh = _lib.stream_handle()
 
 def run(w):
     """fused / hist / scoreW (library's algorithm) and fused_gather / scoreW_gather (forced gather)."""
-    algo = 1 if w.endswith("_gather") else 0
-    w = w.replace("_gather", "")
+    algo = 0
+    for suf, code in (("_gather", 1), ("_count", 2), ("_token", 3)):
+        if w.endswith(suf):
+            algo, w = code, w[:-len(suf)]
     if w == "fused":
         t, mp_ = tabs[1]
         _lib.call("mp_hist_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t), 1, mp_,
@@ -92,7 +94,7 @@ def run_ext(w):
 res = {}
 bytes_ = a.tokens * L * K
 for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup")):
-    fn = run if w.replace("_gather", "") in ("hist", "score1", "score2", "score4", "fused") else run_ext
+    fn = run if w.split("_")[0] in ("hist", "score1", "score2", "score4", "fused") else run_ext
     for _ in range(3):
         fn(w)
     ts = []
