@@ -114,8 +114,8 @@ def test_commmap_mass_equals_mean(seed, kind):
 @settings(**SETTINGS)
 @given(case(), st.sampled_from([1, 2, 4]), st.sampled_from([9, 31, 63, 255]), st.integers(1, 40))
 def test_gather_and_count_contract_agree(c, W, hi, S):
-    """The two exact hop-sum algorithms (per-byte gather, count-contract) and the oracle agree on
-    random shapes, table widths and cost ranges, with and without the fused histogram."""
+    """The three exact hop-sum algorithms (per-byte gather, count-contract, token-tiled) and the
+    oracle agree on random shapes, table widths and cost ranges, with and without the histogram."""
     from oracle import evaluate as oe
     from oracle import stats as ost
     L, E, K, N, C, seed, s = c
@@ -126,9 +126,10 @@ def test_gather_and_count_contract_agree(c, W, hi, S):
     cost, p = _cost(rng, L, S, hi)
     pls = [mpl.Placement(rng.integers(0, S, (L, E)).astype(np.int32)) for _ in range(4 * W)]
     want = np.stack([oe.chunk_sums(sel, oe.pe_table(p, pl.assign), tr.chunk_bounds) for pl in pls])
-    for algo in ("gather", "count"):
+    for algo in ("gather", "count", "token"):
         assert np.array_equal(ev.score_sums(tr, pls, cost, algo=algo), want), algo
     n = 4 if W == 1 else 4 * W
-    f, reps = ev.evaluate_with_stats(tr, pls[:n], cost, algo="count")
-    assert np.array_equal(f.counts, ost.counts(sel, E))
-    assert [r.chunk_hop_sums for r in reps] == want[:n].tolist()
+    for algo in ("count", "token"):
+        f, reps = ev.evaluate_with_stats(tr, pls[:n], cost, algo=algo)
+        assert np.array_equal(f.counts, ost.counts(sel, E))
+        assert [r.chunk_hop_sums for r in reps] == want[:n].tolist()
