@@ -94,7 +94,10 @@ def run_ext(w):
 res = {}
 bytes_ = a.tokens * L * K
 for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup")):
-    fn = run if w.split("_")[0] in ("hist", "score1", "score2", "score4", "fused") else run_ext
+    base = w
+    for suf in ("_gather", "_count", "_token"):
+        base = base[:-len(suf)] if base.endswith(suf) else base
+    fn = run if base in ("hist", "score1", "score2", "score4", "fused") else run_ext
     for _ in range(3):
         fn(w)
     ts = []
