@@ -99,3 +99,15 @@ def test_sass_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_integration_stub_matches_the_abi():
+    """The ctypes binding shown in INTEGRATION.md declares the same argument types as the library
+    (so the documented drop-in binding cannot drift from include/moeplace_cuda.h)."""
+    text = (ROOT / "INTEGRATION.md").read_text()
+    names = {"_p": ctypes.c_void_p, "_i32": ctypes.c_int, "_i64": ctypes.c_int64, "C.c_char_p": ctypes.c_char_p}
+    found = re.findall(r"_lib\.(mp_\w+)\.argtypes = \[(.*?)\]", text)
+    assert len(found) >= 3
+    for name, args in found:
+        got = [names[a.strip()] for a in args.split(",")]
+        assert got == list(_lib.SIGNATURES[name][1]), name
