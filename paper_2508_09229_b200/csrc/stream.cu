@@ -1,17 +1,20 @@
 // Streaming kernels over layer-major u8 traces: load statistics (hist), placement traffic
-// (score) and the fused pass.  One kernel template serves all three.
+// (score) and the fused pass.  One kernel template serves all of them, with two of the three
+// exact hop-sum algorithms (gather, count-contract; the token-tiled one is in tokens.cu).
 //
 // Design: the byte space of the L planes is cut into gridDim.x contiguous
-// ranges; a CTA walks its range plane segment by plane segment.  Per segment it stages
-// layer l's state in shared memory as 256 rows of 256 B, one row per expert id e:
-//   * score table: P = 4W placement hop costs (u8 lanes), replicated per lane slot so the
-//     32 lanes of a warp never bank-conflict (slot = lane*4 | lane*8 | (lane&7)*16 for
-//     W = 1 | 2 | 4 -> one LDS.32 | LDS.64 | LDS.128 wavefront per 32 | 16 | 8 lanes);
-//   * histogram: 32 u32 replicas of bin e at bytes 128 + lane*4 (bank = lane), so the
-//     ATOMS of one warp hit 32 distinct banks and no address is shared between lanes.
+// ranges; a CTA walks its range plane segment by plane segment, and chunk boundaries cut a
+// segment into pieces (one layer x one chunk).  Per segment it stages layer l's state in shared
+// memory as 256 rows of 256 B, one row per expert id e:
+//   * gather: P = 4W placement hop costs (u8 lanes), replicated per lane slot so the 32 lanes
+//     of a warp never bank-conflict (slot = lane*4 | lane*8 | (lane&7)*16 for W = 1 | 2 | 4 ->
+//     one LDS.32 | LDS.64 | LDS.128 wavefront per 32 | 16 | 8 lanes);
+//   * histogram: 32 u32 replicas of bin e at bytes 128 + lane*4 (bank = lane), so the ATOMS of
+//     one warp hit 32 distinct banks and no address is shared between lanes; count-contract
+//     alternates pieces between this set and a second one at bytes 0..127.
 // An expert byte b of a loaded word becomes its row offset (e << 8) | slot with a single
-// PRMT, so a lookup costs PRMT + LDS (+ ATOMS for the histogram).
-// The trace is streamed with 128-bit L1-no-allocate loads, UNROLL per thread in flight.
+// PRMT, so a lookup costs PRMT + LDS (gather) and/or PRMT + ATOMS (histogram).  The trace is
+// streamed with 128-bit L1-no-allocate loads, UNROLL vectors per thread per main-loop batch.
 #include "common.cuh"
 
 namespace mp {
