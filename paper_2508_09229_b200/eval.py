@@ -22,6 +22,7 @@ from .model_trace import (ActivationTrace, FrequencyTable, ModelSpec, chunk_coun
 from .placement import CostMatrix, Placement
 
 MAX_LANES = 16  # placements scored per pass (W = 4 words of four u8 lanes)
+FACTORIZED_MAX_BYTES = 4 << 30  # evaluate_many(auto): largest per-chunk count array worth materialising
 
 
 @dataclass
@@ -288,14 +289,20 @@ def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement
 def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs,
                   method: str = "auto") -> list[EvalReport]:
     """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies),
-    extension A18.  ``method``: "gather" / "count" — streaming passes of up to 16 placements with
+    extension A18.  ``method``: "gather" / "count" / "token" — passes of up to 16 placements with
     that algorithm; "factorized" — one per-chunk histogram pass + tensor-core contraction for any
-    number of placements; "auto" — one streaming pass when P <= 16, factorized above.  All give
+    number of placements; "auto" — passes (the library picks the algorithm per pass) when P <= 16
+    or the per-chunk counts would exceed FACTORIZED_MAX_BYTES, factorized otherwise.  All give
     identical integers."""
     placements = list(placements)
     if method == "auto":
-        method = "pass" if len(placements) <= MAX_LANES else "factorized"
-    if method in ("gather", "count", "pass"):
+        # factorized materialises int64 [C, L, E] per-chunk counts: worth it for large batches, but
+        # not when short chunks make that array huge (then the library's own choice per pass --
+        # token-tiled for short chunks -- is the better way)
+        m = trace.model
+        fact_bytes = trace.n_chunks * (m.L * m.E if m else 0) * 8
+        method = "factorized" if len(placements) > MAX_LANES and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
+    if method in ("gather", "count", "token", "pass"):
         sums = score_sums(trace, placements, costs, algo="auto" if method == "pass" else method)
     elif method == "factorized":
         sums = score_sums_factorized(trace, placements, costs)

@@ -310,3 +310,30 @@ def test_token_algorithm_limit():
     s, _, _ = _run(tr, tables, 1, max_p, AUTO, hist=False)
     want = np.stack([oracle_sums(sel, p, pl.assign, bounds) for pl in pls])
     assert np.array_equal(s, want)
+
+
+def test_evaluate_many_auto_bounds_the_factorized_array(monkeypatch):
+    """Above 16 placements AUTO uses the factorized evaluator unless its int64 [C, L, E] count
+    array would exceed FACTORIZED_MAX_BYTES; either way (and with method="token") the integers
+    are the oracle's."""
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    N, C = 4000, 700  # short chunks
+    tr = mt.generate_trace(m, 1.2, N, C, 3)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 3)
+    rng = np.random.default_rng(9)
+    p = rng.integers(0, 20, (L, 12)).astype(np.uint8)
+    import torch
+    cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    pls = [mpl.Placement(random_assign(rng, L, E, 12)) for _ in range(20)]
+    want = [oracle_sums(sel, p, pl.assign, bounds).tolist() for pl in pls]
+    calls = []
+    real = ev.score_sums_factorized
+    monkeypatch.setattr(ev, "score_sums_factorized", lambda *a, **k: calls.append(1) or real(*a, **k))
+    assert [r.chunk_hop_sums for r in ev.evaluate_many(tr, pls, cost)] == want
+    assert calls, "factorized expected within the byte bound"
+    monkeypatch.setattr(ev, "FACTORIZED_MAX_BYTES", 0)
+    calls.clear()
+    assert [r.chunk_hop_sums for r in ev.evaluate_many(tr, pls, cost)] == want
+    assert not calls, "passes expected above the byte bound"
+    assert [r.chunk_hop_sums for r in ev.evaluate_many(tr, pls, cost, method="token")] == want
