@@ -56,38 +56,41 @@ __device__ __forceinline__ void dedup_record8(uint2 v, uint32_t base, uint32_t s
 
 constexpr int kDedupThreads = 512;
 
-// Fast K = 8 record for pe bytes <= 31 and server ids < 128 (checked per layer by the CTA): with bit
-// 7 of every server byte clear, t = ((a ^ b) | 0x80808080) - 0x01010101 has bit 7 of a byte set iff
-// the bytes differ (each byte of (a^b)|0x80 is >= 0x80, so subtracting 1 never borrows across
-// bytes), so "new server" = AND of t over the earlier picks; a record's hop and dedup sums fit u8
-// lanes (8 * 31 < 256); the dedup mask is PRMT's sign-replicate of the first-occurrence bytes; the
-// source server is removed once per record (distinct servers - [src in set]).
+// Fast K = 8 record for pe bytes <= 31 and server ids < 128 (checked per layer by the CTA).  Row
+// layout of the fast path: slot lane*8 holds {pe word, server word} (one LDS.64 per pick), and bit 7
+// of each server byte flags "this is the source server of the layer for that placement".  With the
+// server id in bits 0-6, t = ((a ^ b) | 0x80808080) - 0x01010101 has bit 7 of a byte set iff the
+// ids differ (each byte of (a^b)|0x80 is >= 0x80, so subtracting 1 never borrows across bytes; the
+// flag bit is ignored), so "new server" = AND of t over the earlier picks, read from bit 7 directly
+// (PRMT's sign-replicate turns it into the dedup mask); a record's hop and dedup sums fit u8 lanes
+// (8 * 31 < 256); the source server is removed once per record (distinct servers - [src in set],
+// the latter the OR of the flag bits).
 __device__ __forceinline__ uint32_t bytes_ne7(uint32_t a, uint32_t b) {
   return ((a ^ b) | 0x80808080u) - 0x01010101u;
 }
-__device__ __forceinline__ void dedup_record8_fast(uint2 v, uint32_t base, uint32_t slot, uint32_t src4,
+__device__ __forceinline__ void dedup_record8_fast(uint2 v, uint32_t base, uint32_t slot8,
                                                    uint32_t (&hop16)[2], uint32_t& uq8, uint32_t (&dd16)[2]) {
   const uint32_t wv[2] = {v.x, v.y};
   uint32_t sw[8], pw[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const uint32_t a = base + prmt(wv[k >> 2], slot, sel_row(k & 3));
-    pw[k] = lds32(a);
-    sw[k] = lds32(a + 128);
+    const uint2 r = lds64(base + prmt(wv[k >> 2], slot8, sel_row(k & 3)));
+    pw[k] = r.x;
+    sw[k] = r.y;
   }
-  uint32_t h8 = 0, d8 = 0, n8 = 0, notsrc = 0xffffffffu;
+  uint32_t h8 = pw[0], d8 = pw[0], n8 = 0x01010101u, srcany = sw[0];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    uint32_t nw = 0xffffffffu;
+  for (int k = 1; k < 8; ++k) {
+    uint32_t nw = bytes_ne7(sw[k], sw[0]);
 #pragma unroll
-    for (int j = 0; j < k; ++j) nw &= bytes_ne7(sw[k], sw[j]);
-    const uint32_t first = nw & 0x80808080u;
+    for (int j = 1; j < k; ++j) nw &= bytes_ne7(sw[k], sw[j]);
+    const uint32_t f = (nw >> 7) & 0x01010101u;  // 1 in bytes whose server is new in the record
     h8 += pw[k];
-    d8 += pw[k] & prmt(first, 0u, 0xBA98u);  // 0xff in bytes whose server is new in the record
-    n8 += first >> 7;
-    notsrc &= bytes_ne7(sw[k], src4);
+    d8 += pw[k] & (f * 0xffu);                    // byte mask by IMAD: keeps the ALU pipe free
+    n8 += f;
+    srcany |= sw[k];
   }
-  uq8 += n8 - ((~notsrc & 0x80808080u) >> 7);  // distinct remote destination servers per lane
+  uq8 += n8 - ((srcany >> 7) & 0x01010101u);  // distinct remote destination servers per lane
   hop16[0] += h8 & 0x00ff00ffu;
   hop16[1] += (h8 >> 8) & 0x00ff00ffu;
   dd16[0] += d8 & 0x00ff00ffu;
@@ -106,6 +109,7 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
   const int lane = threadIdx.x & 31;
   const uint32_t base = smem_addr(sm);
   const uint32_t slot = (uint32_t)(lane << 2);
+  const uint32_t slot8 = (uint32_t)(lane << 3);
   const int64_t n = t1 - t0;
   const int64_t total = n * (int64_t)L;
   int64_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -117,22 +121,28 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
     const int64_t r1 = min(t0 + n, r0 + (g1 - g));
     const uint8_t* plane = planes + (int64_t)l * stride;
     __syncthreads();
-    uint32_t wide = 0;  // any pe byte > 31 or server id >= 128 in this layer -> exact general path
-    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
-      const int e = i >> 5, j = i & 31;
-      const uint32_t pw = __ldg(tables + (int64_t)l * 256 + e), sw = __ldg(srv_tables + (int64_t)l * 256 + e);
-      smw[e * 64 + j] = pw;
-      smw[e * 64 + 32 + j] = sw;
-      wide |= (pw & 0xe0e0e0e0u) | (sw & 0x80808080u);
-    }
     if (threadIdx.x == 0) {
       uint32_t w = 0;
       for (int q = 0; q < 4; ++q) w |= (uint32_t)src_srv[q * L + l] << (8 * q);
       s_src = w;
-      wide |= w & 0x80808080u;
     }
-    const bool fast = __syncthreads_or(wide != 0) == 0;
+    uint32_t wide = 0;  // any pe byte > 31 or server id >= 128 in this layer -> exact general path
+    for (int e = threadIdx.x; e < 256; e += blockDim.x)
+      wide |= (__ldg(tables + (int64_t)l * 256 + e) & 0xe0e0e0e0u) | (__ldg(srv_tables + (int64_t)l * 256 + e) & 0x80808080u);
+    const bool fast = __syncthreads_or(wide != 0 || (threadIdx.x == 0 && (s_src & 0x80808080u))) == 0 && K == 8;
     const uint32_t src = s_src;
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int e = i >> 5, j = i & 31;
+      const uint32_t pw = __ldg(tables + (int64_t)l * 256 + e), sw = __ldg(srv_tables + (int64_t)l * 256 + e);
+      if (fast) {  // {pe, server | source flag} at lane slot j*8
+        smw[e * 64 + 2 * j] = pw;
+        smw[e * 64 + 2 * j + 1] = sw | bytes_eq(sw, src);
+      } else {     // pe at j*4, server at 128 + j*4
+        smw[e * 64 + j] = pw;
+        smw[e * 64 + 32 + j] = sw;
+      }
+    }
+    __syncthreads();
     int c = 0;
     {
       int lo = 0, hi = C;
@@ -162,7 +172,7 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
         };
         auto rec8 = [&](uint2 w, uint32_t b_, uint32_t s_, uint32_t src_, uint32_t (&h_)[2], uint32_t& u_,
                         uint32_t (&d_)[2]) {
-          if (fast) dedup_record8_fast(w, b_, s_, src_, h_, u_, d_);
+          if (fast) dedup_record8_fast(w, b_, slot8, h_, u_, d_);
           else dedup_record8(w, b_, s_, src_, h_, u_, d_);
         };
         const int64_t va = (t + 1) >> 1, vb = te >> 1;  // full vectors cover records [2va, 2vb)
