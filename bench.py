@@ -199,8 +199,9 @@ def main():
                     help="BASELINE config: 2 (default, the metric's config), 3 multi-topology, 4 4096 candidates, "
                          "5 100M tokens strong scaling")
     ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
-    ap.add_argument("--algo", choices=["auto", "gather", "count"], default="auto",
-                    help="hop-sum algorithm (include/moeplace_cuda.h MP_ALGO_*); auto = the library's choice")
+    ap.add_argument("--algo", choices=["auto", "gather", "count", "factorized"], default="auto",
+                    help="hop-sum algorithm (include/moeplace_cuda.h MP_ALGO_*); auto = the library's choice "
+                         "(config 4: factorized, as evaluate_many(method='auto') picks for P > 16)")
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (configs 2-4) / total (config 5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-tokens", type=int, default=None, help="cpu_baseline sample (tokens)")
@@ -331,10 +332,37 @@ def main():
     kev = [_events() for _ in range(2)]
     kernel_ms = [[], []]
 
-    algo = {"auto": 0, "gather": 1, "count": 2}[args.algo]
+    algo = {"auto": 0, "gather": 1, "count": 2, "factorized": 0}[args.algo]
+    # config 4 (4096 candidates): the product path is evaluate_many(method="auto") -> factorized (one per-chunk
+    # histogram pass + exact tensor-core contraction); the streaming passes are timed beside it
+    fact = wl == 4 and args.algo in ("auto", "factorized")
+    if args.algo == "factorized" and wl != 4:
+        raise SystemExit("bench: --algo factorized applies to --workload 4")
+    if fact:
+        cnt_c4 = torch.zeros((C, L * E), dtype=torch.int64, device=dev)
+        pe_all4 = ev.pe_matrix(placements, costs, model)
+        out_f4 = torch.zeros((P_, C), dtype=torch.int64, device=dev)
+        max_chunk = int(np.max(trace.chunk_token_counts()))
+        max_pe4 = max(cs.max_p for cs in costs)
+        kev_f = [_events() for _ in range(2)]
+
+    def fstep(timed: bool):
+        cnt_c4.zero_()
+        if timed:
+            kev_f[0][0].record(stream)
+        _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+                  _lib.ptr(cnt_c4), _lib.ptr(err), sh)
+        if timed:
+            kev_f[0][1].record(stream)
+            kev_f[1][0].record(stream)
+        out_f4.copy_(ev.contract_tc(cnt_c4, pe_all4, max_count=max_chunk, max_pe=max_pe4, err=err))
+        if timed:
+            kev_f[1][1].record(stream)
+        if world > 1:
+            dist.all_reduce(out_f4)
 
     def algo_used(hist: bool, W: int) -> str:  # mirrors choose_algo in csrc/stream.cu
-        if args.algo != "auto":
+        if args.algo not in ("auto", "factorized"):
             return {"gather": "gather", "count": "count-contract"}[args.algo]
         return "count-contract" if (hist or W > 1) else "gather"
 
@@ -396,9 +424,10 @@ def main():
         except Exception:
             pass
 
-    launches_per_step = (1 if fused else len(groups) + (1 if with_hist else 0))
+    launches_per_step = 1 if (fused or fact) else len(groups) + (1 if with_hist else 0)
+    run = fstep if fact else step
     for _ in range(args.warmup):
-        step(False)
+        run(False)
     torch.cuda.synchronize()
     if with_hist and not torch.equal(counts.view(L, E), counts0):
         raise SystemExit("bench: histogram of the timed pass differs from the setup histogram")
@@ -411,18 +440,20 @@ def main():
     ev_a, ev_b = _events()
     ev_a.record(stream)
     for _ in range(args.steps):
-        step(False)
+        run(False)
     ev_b.record(stream)
     torch.cuda.synchronize()
     for _ in range(args.steps):  # per-kernel shares with launch-bracketing events on the same stream
-        step(True)
+        run(True)
         torch.cuda.synchronize()
-        kernel_ms[0].append(kev[0][0].elapsed_time(kev[0][1]))
-        if with_hist and not fused:
-            kernel_ms[1].append(kev[1][0].elapsed_time(kev[1][1]))
+        ke = kev_f if fact else kev
+        kernel_ms[0].append(ke[0][0].elapsed_time(ke[0][1]))
+        if fact or (with_hist and not fused):
+            kernel_ms[1].append(ke[1][0].elapsed_time(ke[1][1]))
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
+    _lib.check_err(err, "bench: device data error in the timed steps")
     t_step = torch.tensor([ev_a.elapsed_time(ev_b) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
@@ -435,6 +466,10 @@ def main():
     if fused:
         kname, tkey, launches = ("mp_hist_score_u8 (fused hist+score of 4 placements; count-contract: histogram "
                                  "+ per-(layer,chunk) contraction with the cost tables)"), "fused", 1
+    elif fact:
+        kname, tkey, launches = ("mp_hist_chunks_u8 (factorized evaluator: per-chunk histogram int64 [C][L][E]; "
+                                 "the exact contraction with the 4096 pe rows runs after it as cuBLASLt int8 GEMMs)"), \
+            "hist_chunks", 1
     else:
         Ws = sorted({W for W, _, _, _ in groups})
         kname = f"mp_score_u8 (W={'/'.join(map(str, Ws))}, {len(groups)} launch(es) per step)"
@@ -458,7 +493,9 @@ def main():
                 "peak_source": peak_src}
     if with_hist and not fused:
         roofline["hist_ms"] = float(np.mean(kernel_ms[1]))
-    if wl in (3, 4) and algo_used(False, 4) == "gather":
+    if fact:
+        roofline["contraction_ms"] = float(np.mean(kernel_ms[1]))
+    if wl in (3, 4) and not fact and algo_used(False, 4) == "gather":
         # shared-memory roofline for the W=4 gather: 4 LDS.128 wavefronts per 32 lookups + 4 LDG wavefronts
         # per 512 B, at 1 wavefront / SM / clock (sm_max_mhz)
         mhz = (clocks or {}).get("sm_mhz") or 1965.0
@@ -512,7 +549,26 @@ def main():
 
     # ------- configs 2/4: the factorized evaluator beside the measured gather (not the headline) -------
     factorized = None
-    if wl in (2, 4):
+    passes = None
+    if fact:
+        # the same 4096 hop sums by 256 streaming passes of 16 placements (count-contract), for comparison
+        for _ in range(2):
+            step(False)
+        torch.cuda.synchronize()
+        ok = torch.equal(out_f4, sums_all[:P_ * C].view(P_, C))
+        pa, pb = _events()
+        n_p = max(3, args.steps // 4)
+        pa.record(stream)
+        for _ in range(n_p):
+            step(False)
+        pb.record(stream)
+        torch.cuda.synchronize()
+        p_ms = pa.elapsed_time(pb) / n_p
+        passes = {"ms_per_step": p_ms, "launches_per_step": len(groups), "algorithm": algo_used(False, 4),
+                  "value": n_total * L * P_ / (p_ms / 1e3), "bit_identical_to_step": ok,
+                  "hbm_frac_per_pass": n * L * K / (p_ms / len(groups) / 1e3) / 1e9 / peak,
+                  "note": "evaluate_many(method='count'): 256 mp_score_u8 W=4 passes over the resident trace"}
+    if wl == 2 or (wl == 4 and not fact):
         cnt_c = torch.zeros((C, L * E), dtype=torch.int64, device=dev)
         pe_all = ev.pe_matrix(placements, costs, model)
         out_f = torch.zeros((P_, C), dtype=torch.int64, device=dev)
@@ -555,6 +611,8 @@ def main():
         def api_call():
             if with_hist:
                 return ev.evaluate_with_stats(host, placements, costs[0])[0].counts
+            if fact:
+                return ev.evaluate_many(host, placements, costs)  # auto -> factorized for P > 16
             return ev.score_sums(host, placements, costs)
 
         api_call()  # warm-up
@@ -576,7 +634,9 @@ def main():
             dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e_ms = float(t_e.item())
         api = ("moeplace.eval.evaluate_with_stats(trace in pinned host memory, 4 placements, cost)" if with_hist
-               else f"moeplace.eval.score_sums / evaluate_many(trace in pinned host memory, {P_} placements)")
+               else f"moeplace.eval.evaluate_many(trace in pinned host memory, {P_} placements, method='auto' "
+                    f"-> factorized; per-placement pe tables built inside the call)" if fact
+               else f"moeplace.eval.score_sums(trace in pinned host memory, {P_} placements)")
         e2e = {"value": n_total * L * P_ / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(n * L * K * world),
                "d2h_bytes_per_step": int(((L * E if with_hist else 0) + P_ * C) * 8 * world), "api": api}
@@ -590,7 +650,9 @@ def main():
                                    "16x4x4 = 256 devices) scored in one W=4 pass",
                                 4: "config4: DeepSeek-R1 shape, 1M Zipf(1.2) tokens/GPU, Dragonfly 16x4x4, 4096 candidate "
                                    "placements (ILPLoad + 64 within-layer swaps each, seeds 1000+i) scored per step "
-                                   "(256 W=4 passes)",
+                                   + ("(factorized: one per-chunk histogram pass + exact int8 tensor-core contraction, "
+                                      "what evaluate_many(method='auto') runs for P > 16)" if fact
+                                      else "(256 W=4 passes)"),
                                 5: f"config5: DeepSeek-R1 shape, {n_total} Zipf(1.2) tokens total sharded over "
                                    f"{world} GPU(s), 1500 chunks, FatTree 8x4x8; hist + score of 4 placements"}[wl],
                    "tokens_per_gpu": n, "tokens_total": n_total, "placements": P_, "topologies": kinds,
@@ -598,13 +660,14 @@ def main():
                    else f"trace {n * L * K / 1e6:.0f} MB < 126 MB L2: each step streams it {len(groups)}x; "
                         "first pass per step from HBM, reuse from L2",
                    "parallelism": f"token shards x{world}" + (" + 1 NCCL all_reduce" if world > 1 else "")}
-        cfg["hop_sum_algorithm"] = (algo_used(True, 1) if fused else
+        cfg["hop_sum_algorithm"] = (algo_used(True, 1) if fused else "factorized" if fact else
                                     "/".join(sorted({algo_used(False, W) for W, _, _, _ in groups})))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
                 "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "factorized": factorized,
+                "passes": passes,
                 "kernels_alone": kernels_alone,
                 "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
         emit(line)

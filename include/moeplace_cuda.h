@@ -111,6 +111,17 @@ int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, i
 int mp_hist_chunks_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
                       int E, const int64_t* chunk_bounds, int C, int64_t* counts, int64_t* err, void* stream);
 int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out, void* stream);
+/* Tensor-core form of the same contraction (eval.contract_tc; the GEMMs are cuBLASLt int8 with
+ * int32 accumulation, exact while LE * 127^2 < 2^31):
+ * mp_count_digits: out int8 [ndig*Cp][LEp], out[(a*Cp + c)*LEp + i] = (counts[c*LE + i] >> 7a) & 127
+ *   for c < C, i < LE, 0 in the padding (Cp >= C, LEp >= LE).  A count < 0 or >= 2^(7*ndig) is
+ *   written as 0 and raises MP_DATA_EXPERT_RANGE in err = {1, chunk, index, count}.
+ * mp_digit_combine: out[q*C + c] += sum_{a<ndig} part[q*ldp + a*Cp + c] << (shift0 + 7a), where
+ *   part = int32 [P][ldp] is pe_digit @ digits^T (ldp >= ndig*Cp).                               */
+int mp_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
+                    int64_t* err, void* stream);
+int mp_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0, int64_t* out,
+                     void* stream);
 
 /* ---- placement tables: Placement -> per-expert round-trip hops ---------
  * tables[((l*256 + e)*W + w)] is a u32 whose byte j is pe_q[l][e] = cost[topo_of[q]][l][assign[q][l][e]]

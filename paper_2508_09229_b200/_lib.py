@@ -32,6 +32,8 @@ SIGNATURES = {
     "mp_hist_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p]),
     "mp_hist_chunks_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p]),
     "mp_contract_counts": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
+    "mp_count_digits": (_i32, [_p, _i32, _i64, _i32, _i32, _i64, _p, _p, _p]),
+    "mp_digit_combine": (_i32, [_p, _i32, _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "mp_pack_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _i32, _p, _p]),
     "mp_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p]),
     "mp_token_hops_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p]),

@@ -39,6 +39,10 @@ cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0
                                const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s);
 cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out,
                             cudaStream_t s);
+cudaError_t launch_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
+                                int64_t* err, cudaStream_t s);
+cudaError_t launch_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0,
+                                 int64_t* out, cudaStream_t s);
 cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
                           const int64_t* cids, int64_t* lens_or_offsets, uint8_t* out, cudaStream_t s);
 }  // namespace mp
@@ -114,6 +118,20 @@ int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, i
   if (!counts || !pe || !out || C <= 0 || P <= 0 || LE <= 0) return MP_ERR_ARG;
   if (C > 65535 * 16) return MP_ERR_UNSUPPORTED;
   return status(mp::launch_contract(counts, C, pe, P, LE, out, S(stream)));
+}
+
+int mp_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
+                    int64_t* err, void* stream) {
+  if (!counts || !out || !err || C <= 0 || LE <= 0 || Cp < C || LEp < LE || ndig < 1 || ndig > 8) return MP_ERR_ARG;
+  return status(mp::launch_count_digits(counts, C, LE, ndig, Cp, LEp, out, err, S(stream)));
+}
+
+int mp_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0, int64_t* out,
+                     void* stream) {
+  if (!part || !out || P <= 0 || C <= 0 || Cp < C || ndig < 1 || ldp < (int64_t)ndig * Cp || shift0 < 0 ||
+      shift0 + 7 * ndig > 63)
+    return MP_ERR_ARG;
+  return status(mp::launch_digit_combine(part, P, ldp, C, Cp, ndig, shift0, out, S(stream)));
 }
 
 int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,

@@ -15,6 +15,7 @@
 // An expert byte b of a loaded word becomes its row offset (e << 8) | slot with a single
 // PRMT, so a lookup costs PRMT + LDS (gather) and/or PRMT + ATOMS (histogram).  The trace is
 // streamed with 128-bit L1-no-allocate loads, UNROLL vectors per thread per main-loop batch.
+#include <algorithm>
 #include "common.cuh"
 
 namespace mp {
@@ -229,8 +230,10 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
   // set B = bytes 0..127, free since there are no gather tables): a piece's flush reads and zeroes
   // its set while the next piece already counts into the other one, so one barrier per piece
   // suffices and no per-segment zeroing is needed.
+  // The per-chunk histogram (CHUNKED, W == 0, WC == 0) alternates the two sets the same way.
+  constexpr bool kAltSets = CHUNKED && W == 0;
   int hset = 0;
-  if constexpr (WC > 0) {
+  if constexpr (kAltSets) {
     for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) smw[i] = 0;
   }
   Flat f(t0 * K, t1 * K, L);
@@ -251,7 +254,7 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
         smw[e * 64 + j] = __ldg(tl + e * W + (j % W));
       }
     }
-    if constexpr (HIST && WC == 0) {
+    if constexpr (HIST && !kAltSets) {
       for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) smw[(i >> 5) * 64 + 32 + (i & 31)] = 0;
     }
     __syncthreads();
@@ -283,6 +286,25 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
 #pragma unroll
       for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
     }
+    // per-chunk histogram flush: the same two threads per bin, bin total -> dst[l*E + e] (set zeroed)
+    auto flush_counts = [&](int64_t* dst, int set) {
+      uint32_t n = 0;
+      if (fe < 256) {
+        uint32_t* row = smw + fe * 64 + (set ? 0 : 32);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int rr = (fh * 16 + i + fe) & 31;
+          n += row[rr];
+          row[rr] = 0;
+        }
+      }
+      n += __shfl_xor_sync(0xffffffffu, n, 1);
+      if (!fh && n) {
+        if (fe < E) atomic_add_i64(dst + (int64_t)l * E + fe, (int64_t)n);
+        else report_err(err, MP_DATA_EXPERT_RANGE, l, fe, n);
+      }
+    };
+
     auto flush_contract = [&](int c, int set) {
       uint32_t n = 0;
       if (fe < 256) {
@@ -321,7 +343,7 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
         const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
         ScoreAcc<WW> acc;
         acc.zero();
-        if constexpr (WC > 0) st.hbase = st.base + (hset ? 0u : 128u);
+        if constexpr (kAltSets) st.hbase = st.base + (hset ? 0u : 128u);
         st.range(plane, x, xe, acc);
         if constexpr (W > 0) {
           int q = 0;
@@ -333,9 +355,9 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
           flush_contract(c, hset);
           hset ^= 1;        // the next piece counts into the other set; no second barrier
         } else if constexpr (CHUNKED) {  // per-chunk histogram: counts is [C][L][E]
-          __syncthreads();
-          flush_hist(counts + (int64_t)c * L * E);
-          __syncthreads();
+          __syncthreads();  // every warp's ATOMS into set hset are done
+          flush_counts(counts + (int64_t)c * L * E, hset);
+          hset ^= 1;
         }
         x = xe;
       }
@@ -428,6 +450,56 @@ cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int
   if (P <= 0 || C <= 0 || LE <= 0) return cudaSuccess;
   dim3 grid((unsigned)((P + kCtP - 1) / kCtP), (unsigned)((C + kCtC - 1) / kCtC));
   contract_kernel<<<grid, 256, 0, s>>>(counts, C, pe, P, LE, out);
+  return cudaGetLastError();
+}
+
+// ---- tensor-core contraction operands (factorized evaluator, eval.contract_tc) ----
+// Digit planes of the per-chunk counts for exact int8 GEMMs: out is int8 [ndig * Cp][LEp], row
+// a*Cp + c holds digit a (7 bits) of counts[c][.], zero in the padding rows/columns, so one GEMM
+// against pe [P][LEp] yields every digit's partial sums side by side (N = ndig * Cp).  A count
+// that needs more than ndig digits (or is negative) is reported, never truncated silently.
+__global__ void count_digits_kernel(const int64_t* __restrict__ counts, int C, int64_t LE, int ndig, int Cp,
+                                    int64_t LEp, int8_t* __restrict__ out, int64_t* err) {
+  const int64_t n = (int64_t)Cp * LEp;
+  const int64_t lim = (int64_t)1 << (7 * ndig);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(k / LEp);
+    const int64_t i = k - (int64_t)c * LEp;
+    int64_t v = (c < C && i < LE) ? __ldg(counts + (int64_t)c * LE + i) : 0;
+    if (v < 0 || v >= lim) {
+      report_err(err, MP_DATA_EXPERT_RANGE, c, (int)(i < 0x7fffffff ? i : 0x7fffffff), v);
+      v = 0;
+    }
+    for (int a = 0; a < ndig; ++a) out[((int64_t)a * Cp + c) * LEp + i] = (int8_t)((v >> (7 * a)) & 127);
+  }
+}
+
+// out[q*C + c] += sum_a part[q*ldp + a*Cp + c] << (shift0 + 7a): recombines the int32 digit GEMM
+// partials (exact: each partial < 2^31) into the int64 hop sums.
+__global__ void digit_combine_kernel(const int32_t* __restrict__ part, int P, int64_t ldp, int C, int Cp, int ndig,
+                                     int shift0, int64_t* __restrict__ out) {
+  const int64_t n = (int64_t)P * C;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(k / C), c = (int)(k - (int64_t)q * C);
+    int64_t v = 0;
+    for (int a = 0; a < ndig; ++a) v += (int64_t)__ldg(part + q * ldp + (int64_t)a * Cp + c) << (shift0 + 7 * a);
+    out[k] += v;
+  }
+}
+
+cudaError_t launch_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
+                                int64_t* err, cudaStream_t s) {
+  const int64_t n = (int64_t)Cp * LEp;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  count_digits_kernel<<<grid, 256, 0, s>>>(counts, C, LE, ndig, Cp, LEp, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0,
+                                 int64_t* out, cudaStream_t s) {
+  const int64_t n = (int64_t)P * C;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  digit_combine_kernel<<<grid, 256, 0, s>>>(part, P, ldp, C, Cp, ndig, shift0, out);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,7 @@ same float code on its own integers, so reports are bit-identical, not merely wi
 from __future__ import annotations
 
 import json
+import threading
 from dataclasses import asdict, dataclass, field
 from typing import Any, Optional, Sequence, Union
 
@@ -80,6 +81,25 @@ def report_from_sums(sums: np.ndarray, tokens: np.ndarray, label: str = "") -> E
                       chunk_hop_sums=sums.tolist())
 
 
+def reports_from_sums(sums: np.ndarray, tokens: np.ndarray, labels: Sequence[str]) -> list[EvalReport]:
+    """``report_from_sums`` for every row of int64 [P, C] at once (batched evaluation).  Same floats
+    bit for bit: the per-chunk means form a C-contiguous [P, C'] array, so numpy's row reductions
+    add in the same order as its 1-D ones, and totals / n_tokens is the same Python int division."""
+    sums = np.asarray(sums, dtype=np.int64)
+    tokens = np.asarray(tokens, dtype=np.int64)
+    keep = tokens > 0
+    n_tok = int(tokens.sum())
+    if n_tok == 0:
+        raise MoeplaceError("evaluate: empty trace")
+    totals = sums.sum(axis=1).tolist()
+    stds = np.std(np.ascontiguousarray(sums[:, keep]) / tokens[keep], axis=1).tolist()
+    n_chunks, n_empty = int(keep.sum()), int((~keep).sum())
+    rows = sums.tolist()
+    return [EvalReport(mean_hops_per_token=totals[i] / n_tok, std_hops=stds[i], n_tokens=n_tok, n_chunks=n_chunks,
+                       label=labels[i], empty_chunks=n_empty, hop_sum=totals[i], chunk_hop_sums=rows[i])
+            for i in range(sums.shape[0])]
+
+
 def _as_costs(costs, n: int) -> list[CostMatrix]:
     if isinstance(costs, CostMatrix):
         return [costs] * n
@@ -115,6 +135,44 @@ def _stack_assign(placements: Sequence[Placement], costs: Sequence[CostMatrix], 
         if a.size and (int(a.min()) < 0 or int(a.max()) >= c.S):
             raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {i}, {c.S} devices)")
         out[i] = a
+    return out
+
+
+_STAGE = {"buf": None}            # pinned int32 staging for batched assignments (reused across calls)
+_STAGE_LOCK = threading.Lock()
+_STAGE_MAX_BYTES = 1 << 30          # larger batches use a one-off pinned buffer
+
+
+def _assign_to_device(placements: Sequence[Placement], costs: Sequence[CostMatrix], model: ModelSpec):
+    """Device int32 [P, L, E] assignments of a large batch, checked like ``_stack_assign`` (same
+    errors): the host work is one memcpy per placement into a pinned staging buffer, and the
+    per-placement range check runs on the device after one host-to-device copy."""
+    t = _lib.torch()
+    dev = _lib.require_cuda()
+    P, L, E = len(placements), model.L, model.E
+    nbytes = P * L * E * 4
+    with _STAGE_LOCK:
+        buf = _STAGE["buf"]
+        if buf is None or buf.numel() < P * L * E:
+            buf = t.empty(P * L * E, dtype=t.int32, pin_memory=True)
+            if nbytes <= _STAGE_MAX_BYTES:
+                _STAGE["buf"] = buf
+        host = buf[:P * L * E].numpy().reshape(P, L, E)
+        for i, pl in enumerate(placements):
+            a = np.asarray(pl.assign)
+            if a.shape != (L, E):
+                raise ConfigError(f"placement shape {a.shape} != model [{L}, {E}]")
+            if a.dtype != np.int32 and a.size and (int(a.min()) < 0 or int(a.max()) >= costs[i].S):
+                raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {i}, "
+                                    f"{costs[i].S} devices)")  # checked before narrowing to int32
+            np.copyto(host[i], a, casting="unsafe")
+        out = buf[:P * L * E].to(dev, non_blocking=True).view(P, L, E)
+        flat = out.view(P, -1)
+        S = t.as_tensor(np.asarray([c.S for c in costs], dtype=np.int32), device=dev)
+        bad = (flat.amin(1) < 0) | (flat.amax(1) >= S)
+        first = int(t.nonzero(bad)[0, 0]) if bool(bad.any()) else -1  # syncs: the staging buffer is free again
+    if first >= 0:
+        raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {first}, {costs[first].S} devices)")
     return out
 
 
@@ -200,7 +258,7 @@ def pe_matrix(placements: Sequence[Placement], costs, model: ModelSpec):
     placements = list(placements)
     costs = _as_costs(costs, len(placements))
     dev = _lib.require_cuda()
-    assign = _lib.to_dev(_stack_assign(placements, costs, model), t.int64)
+    assign = _assign_to_device(placements, costs, model).long()
     uniq, topo_of = _unique_costs(costs)
     topo_of = np.asarray(topo_of)
     out = t.empty((len(placements), model.L * model.E), dtype=t.uint8, device=dev)
@@ -220,13 +278,15 @@ def _digits(x, bits: int = 7):
     return d
 
 
-def contract_tc(cnt, pe):
+def contract_tc(cnt, pe, max_count: Optional[int] = None, max_pe: Optional[int] = None, err=None):
     """Exact hop sums [P, C] = pe [P, LE] (uint8) @ cnt^T [LE, C] (int64 counts) on the tensor cores:
-    both operands are split into 7-bit digits (int8 >= 0), every digit pair is one int8 GEMM with
-    int32 accumulation (cuBLASLt; exact since LE * 127^2 < 2^31 for LE <= 133,000), and the
-    partial products are recombined in int64 with weights 128^(a+b).  pe (the large operand for
-    big candidate batches) is split straight from uint8 into at most two digits, without padding
-    copies when P and LE are already GEMM-aligned."""
+    both operands are split into 7-bit digits (int8 >= 0) and every digit pair's products come from
+    int8 GEMMs with int32 accumulation (cuBLASLt; exact since LE * 127^2 < 2^31 for LE <= 133,000).
+    ``mp_count_digits`` writes all count digits as one stacked operand (rows a*Cp + c), so one GEMM
+    per pe digit (one in total when pe < 128) yields every digit's partials side by side, and
+    ``mp_digit_combine`` adds them into int64 with weights 128^(a+b).  ``max_count`` / ``max_pe``
+    bound the operands (no device reduction or sync when given; a count above the bound raises
+    rather than truncating); with ``err`` the caller checks that device error block itself."""
     t = _lib.torch()
     P, LE = pe.shape
     C = cnt.shape[0]
@@ -235,8 +295,14 @@ def contract_tc(cnt, pe):
     Pp, Cp = max(32, -(-P // 32) * 32), max(8, -(-C // 8) * 8)
     LEp = max(16, -(-LE // 16) * 16)  # cuBLASLt int8: K a multiple of 16 (zero padding is exact)
     out = t.zeros((P, C), dtype=t.int64, device=pe.device)
-    da = _digits(cnt)
-    db = 1 if int(pe.max().item()) < 128 else 2
+    if max_count is None:
+        da = _digits(cnt)
+    else:
+        da = 1
+        while max_count >= (1 << (7 * da)):
+            da += 1
+    db = 1 if (max_pe if max_pe is not None else int(pe.max().item())) < 128 else 2
+    cnt = cnt.contiguous()
 
     def pe_digit(b):
         d = pe if db == 1 else ((pe & 127) if b == 0 else (pe >> 7))
@@ -246,16 +312,17 @@ def contract_tc(cnt, pe):
         A[:P, :LE].copy_(d.view(t.int8))
         return A
 
-    B = t.zeros((Cp, LEp), dtype=t.int8, device=pe.device)  # B^T row-major == B column-major
-    Bd = []
-    for a in range(da):
-        B[:C, :LE].copy_(((cnt >> (7 * a)) & 127).to(t.int8))
-        Bd.append(B.clone() if a + 1 < da else B)
+    own_err = err is None
+    if own_err:
+        err = _lib.new_err()
+    B = t.empty((da * Cp, LEp), dtype=t.int8, device=pe.device)  # B^T row-major == B column-major
+    sh = _lib.stream_handle()
+    _lib.call("mp_count_digits", _lib.ptr(cnt), C, LE, da, Cp, LEp, _lib.ptr(B), _lib.ptr(err), sh)
     for b in range(db):
-        A = pe_digit(b)
-        for a in range(da):
-            part = t._int_mm(A, Bd[a].t())  # int32 [Pp, Cp], exact
-            out += part[:P, :C].to(t.int64) << (7 * (a + b))
+        part = t._int_mm(pe_digit(b), B.t())  # int32 [Pp, da*Cp], exact
+        _lib.call("mp_digit_combine", _lib.ptr(part), P, part.shape[1], C, Cp, da, 7 * b, _lib.ptr(out), sh)
+    if own_err:
+        _lib.check_err(err, "contract_tc: per-chunk count outside its digit range")
     return out
 
 
@@ -276,7 +343,10 @@ def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement
     C = trace.n_chunks
     pe = pe_matrix(placements, costs, m)
     if contraction == "tc":
-        out = contract_tc(cnt.view(C, -1), pe)
+        # a per-chunk count is at most the chunk's token count (distinct picks per record)
+        max_count = int(np.max(trace.chunk_token_counts()))
+        max_pe = max(c.max_p for c in _unique_costs(_as_costs(costs, len(placements)))[0])
+        out = contract_tc(cnt.view(C, -1), pe, max_count=max_count, max_pe=max_pe)
     elif contraction == "cuda":
         out = t.zeros((pe.shape[0], C), dtype=t.int64, device=cnt.device)
         _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe), pe.shape[0], m.L * m.E, _lib.ptr(out),
@@ -308,8 +378,7 @@ def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs
         sums = score_sums_factorized(trace, placements, costs)
     else:
         raise ConfigError(f"unknown evaluate method {method!r}")
-    tokens = trace.chunk_token_counts()
-    return [report_from_sums(sums[i], tokens, placements[i].label) for i in range(len(placements))]
+    return reports_from_sums(sums, trace.chunk_token_counts(), [p.label for p in placements])
 
 
 def evaluate(trace: ActivationTrace, placement: Placement, cost: CostMatrix) -> EvalReport:

@@ -86,10 +86,13 @@ def improve_placement(trace: ActivationTrace, start: Placement, cost: CostMatrix
     gen = t.Generator(device=dev)
     gen.manual_seed(seed)
     cur = _lib.to_dev(start.assign, t.int64)
+    max_count = int(max(trace.chunk_token_counts().max(), 0))
+    err = _lib.new_err()
 
     def score(cands):
         pe = t.gather(p.unsqueeze(0).expand(cands.shape[0], -1, -1), 2, cands)  # [B, L, E]
-        sums = contract_tc(cnt, pe.reshape(cands.shape[0], -1).to(t.uint8))
+        sums = contract_tc(cnt, pe.reshape(cands.shape[0], -1).to(t.uint8), max_count=max_count, max_pe=cost.max_p,
+                           err=err)
         return _objective(sums, tokens, objective, lam)
 
     best = float(score(cur.unsqueeze(0))[0].item())
@@ -104,5 +107,6 @@ def improve_placement(trace: ActivationTrace, start: Placement, cost: CostMatrix
         if v < best:
             best, cur = v, cands[i].clone()
         hist.append(best)
+    _lib.check_err(err, "improve_placement: per-chunk count outside its digit range")
     out = Placement(cur.to(t.int32).cpu().numpy(), start.constraints, (start.label or "start") + f"+search[{objective}]")
     return SearchResult(out, best, hist, evaluated)

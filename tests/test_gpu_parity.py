@@ -509,6 +509,19 @@ def test_contract_tc_digit_paths(P, LE, C, pe_hi):
     got = ev.contract_tc(cnt, pe).cpu().numpy()
     want = pe.cpu().numpy().astype(np.int64) @ cnt.cpu().numpy().T
     assert np.array_equal(got, want)
+    # stated operand bounds (no device reductions) give the same integers
+    bounded = ev.contract_tc(cnt, pe, max_count=2 ** 20 - 1, max_pe=pe_hi - 1).cpu().numpy()
+    assert np.array_equal(bounded, want)
+
+
+def test_contract_tc_count_above_the_stated_bound_raises():
+    import torch
+    from moeplace.errors import MoeplaceError
+    pe = torch.ones((40, 64), dtype=torch.uint8, device="cuda")
+    cnt = torch.full((9, 64), 200, dtype=torch.int64, device="cuda")
+    assert ev.contract_tc(cnt, pe, max_count=200).sum().item() == 40 * 9 * 64 * 200
+    with pytest.raises(MoeplaceError):
+        ev.contract_tc(cnt, pe, max_count=100)  # one 7-bit digit cannot hold 200: raised, not truncated
 
 
 @pytest.mark.parametrize("shape", [R1, B16, (2, 4, 1), (1, 256, 3)])

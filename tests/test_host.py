@@ -454,3 +454,20 @@ def test_cpu_fused_pass_matches_separate():
     assert np.array_equal(cnt, ost.counts(sel, 32))
     for q in range(6):
         assert np.array_equal(sums[q], oe.chunk_sums(sel, pes[q], b))
+
+
+def test_batched_reports_equal_single_reports():
+    """reports_from_sums (evaluate_many's batched float derivation) gives the same EvalReports, bit
+    for bit, as report_from_sums per placement, with empty chunks and large sums."""
+    import moeplace.eval as ev
+    rng = np.random.default_rng(7)
+    for P, C in [(1, 1), (3, 17), (64, 150), (9, 401)]:
+        sums = rng.integers(0, 10 ** 12, (P, C))
+        tok = rng.integers(0, 7000, C)
+        if C > 1:
+            tok[rng.integers(1, C)] = 0
+        tok[0] = max(tok[0], 1)
+        sums[:, tok == 0] = 0
+        labels = [f"p{i}" for i in range(P)]
+        batched = ev.reports_from_sums(sums, tok, labels)
+        assert batched == [ev.report_from_sums(sums[i], tok, labels[i]) for i in range(P)]

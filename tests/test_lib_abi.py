@@ -77,6 +77,11 @@ def test_argument_validation_matrix():
         (L.mp_comm_map(P, P, P, P, 4, P, P, Lr, E, 8, P, None, None), ARG),
         (L.mp_pack_server_tables(P, 1, P, P, 5, Lr, E, 8, P, P, None), ARG),
         (L.mp_contract_counts(P, 65535 * 16 + 1, P, 1, 10, P, None), UNS),
+        (L.mp_count_digits(P, 4, 10, 2, 3, 16, P, P, None), ARG),           # Cp < C
+        (L.mp_count_digits(P, 4, 10, 2, 8, 16, P, None, None), ARG),        # err required
+        (L.mp_count_digits(P, 4, 10, 0, 8, 16, P, P, None), ARG),           # no digits
+        (L.mp_digit_combine(P, 4, 8, 3, 8, 2, 0, P, None), ARG),            # ldp < ndig*Cp
+        (L.mp_digit_combine(P, 4, 16, 3, 8, 2, 50, P, None), ARG),          # shift beyond int64
         (L.mp_coeffs(P, 0, P, Lr, E, 8, 1e9, P, None, None), ARG),          # denom 0 with counts
         (L.mp_copy_planes_h2d(P, 8, P, 16, 16, 1, None), ARG),               # dst stride < width
         (L.mp_copy_planes_h2d(P, 16, P, 16, 0, 4, None), 0),                 # empty copy is a no-op
