@@ -54,6 +54,9 @@ __device__ __forceinline__ void table_load(uint32_t a, uint32_t (&t)[W]) {
 // Vectors per thread per main-loop iteration (R1, 10M tokens, B200): histogram / count-contract
 // instances 2: 0.894 / 4: 0.895 / 8: 0.846 / 16: 0.840 / 32: 0.843 ms (hist), fused step 0.936 ->
 // 0.886 ms at 16; gather instances 2: 0.963 / 4: 0.795 / 8: 0.770-0.787 / 16: 0.796 ms (score W=1).
+#ifndef MP_FLUSH_SNAPSHOT
+#define MP_FLUSH_SNAPSHOT 1
+#endif
 #ifndef MP_COUNT_UNROLL
 #define MP_COUNT_UNROLL 16
 #endif
@@ -233,6 +236,10 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
   // The per-chunk histogram (CHUNKED, W == 0, WC == 0) alternates the two sets the same way.
   constexpr bool kAltSets = CHUNKED && W == 0;
   int hset = 0;
+  // Flushes read a set without zeroing it: each flush thread keeps its 16-replica partial of both
+  // sets from the previous flush and reports the difference (exact mod 2^32, and a piece's true
+  // count is < 2^32), which halves the flush's shared-memory traffic (L1TEX is the bound).
+  uint32_t snap0 = 0u, snap1 = 0u;  // two scalars, not an array: no local memory
   if constexpr (kAltSets) {
     for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) smw[i] = 0;
   }
@@ -287,37 +294,41 @@ stream_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, in
       for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
     }
     // per-chunk histogram flush: the same two threads per bin, bin total -> dst[l*E + e] (set zeroed)
-    auto flush_counts = [&](int64_t* dst, int set) {
-      uint32_t n = 0;
+    // bin total of the piece just counted into `set` (two threads per bin, 16 replicas each, rotated so
+    // a warp's 32 loads hit 32 banks); valid in the even lane of each pair
+    auto piece_bin_total = [&](int set) -> uint32_t {
+      uint32_t part = 0;
+      if (fe < 256) {
+        const uint32_t* row = smw + fe * 64 + (set ? 0 : 32);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) part += row[(fh * 16 + i + fe) & 31];
+      }
+#if MP_FLUSH_SNAPSHOT
+      const uint32_t d = part - (set ? snap1 : snap0);
+      if (set) snap1 = part; else snap0 = part;
+#else
+      const uint32_t d = part;
       if (fe < 256) {
         uint32_t* row = smw + fe * 64 + (set ? 0 : 32);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int rr = (fh * 16 + i + fe) & 31;
-          n += row[rr];
-          row[rr] = 0;
-        }
+        for (int i = 0; i < 16; ++i) row[(fh * 16 + i + fe) & 31] = 0;
       }
-      n += __shfl_xor_sync(0xffffffffu, n, 1);
-      if (!fh && n) {
+#endif
+      const uint32_t n = d + __shfl_xor_sync(0xffffffffu, d, 1);
+      return fh ? 0u : n;  // even lane of each pair owns the bin
+    };
+
+    // per-chunk histogram flush: bin total -> dst[l*E + e]
+    auto flush_counts = [&](int64_t* dst, int set) {
+      const uint32_t n = piece_bin_total(set);
+      if (n) {
         if (fe < E) atomic_add_i64(dst + (int64_t)l * E + fe, (int64_t)n);
         else report_err(err, MP_DATA_EXPERT_RANGE, l, fe, n);
       }
     };
 
     auto flush_contract = [&](int c, int set) {
-      uint32_t n = 0;
-      if (fe < 256) {
-        uint32_t* row = smw + fe * 64 + (set ? 0 : 32);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int rr = (fh * 16 + i + fe) & 31;
-          n += row[rr];
-          row[rr] = 0;
-        }
-      }
-      n += __shfl_xor_sync(0xffffffffu, n, 1);
-      if (fh) n = 0;  // even lane of each pair owns the bin
+      const uint32_t n = piece_bin_total(set);
       if (n && counts) {
         if (fe < E) atomic_add_i64(counts + (int64_t)l * E + fe, (int64_t)n);
         else report_err(err, MP_DATA_EXPERT_RANGE, l, fe, n);
