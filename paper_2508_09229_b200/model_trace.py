@@ -10,7 +10,10 @@ Hot path: ``generate_trace`` (kernel ``mp_gen_trace``) and ``estimate_frequencie
 """
 from __future__ import annotations
 
+import os
 import re
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Any, Optional, Sequence
 
@@ -326,6 +329,96 @@ _PARSE_ERR = {1: "malformed line (expected chunk_id<TAB>layer<l>:e,...,e fields)
               5: "repeated expert index", 6: "chunk id too large"}
 
 
+# ---- file <-> device text transfers through a reusable pinned ring ----------------------------
+# 2 x IO_LANES slots of IO_SLOT bytes: IO_LANES slots are read (pread) or written (pwrite) in
+# parallel threads (the kernel copies release the GIL) while the other half is in flight over PCIe
+# on a copy stream, so a text trace moves at file-system-cache speed without a full-size pinned
+# staging copy.
+IO_SLOT = 32 << 20
+IO_LANES = 4
+_IO = {"ring": None, "pool": None}
+_IO_LOCK = threading.Lock()
+
+
+def _io_ring():
+    t = _lib.torch()
+    if _IO["ring"] is None:
+        _IO["ring"] = [t.empty(IO_SLOT, dtype=t.uint8, pin_memory=True) for _ in range(2 * IO_LANES)]
+        _IO["pool"] = ThreadPoolExecutor(IO_LANES, thread_name_prefix="moeplace-io")
+    return _IO["ring"], _IO["pool"]
+
+
+def _file_to_device(fd: int, n: int, dst) -> None:
+    """dst[:n] <- bytes [0, n) of the open file ``fd`` (stream-ordered on the current stream)."""
+    t = _lib.torch()
+    with _IO_LOCK:
+        ring, pool = _io_ring()
+        views = [r.numpy() for r in ring]
+        cs = t.cuda.Stream()
+        cs.wait_stream(t.cuda.current_stream())
+        evs = [None] * len(ring)
+        off, half = 0, 0
+        while off < n:
+            jobs = []
+            for r in range(IO_LANES):
+                o = off + r * IO_SLOT
+                if o >= n:
+                    break
+                k = half * IO_LANES + r
+                if evs[k] is not None:
+                    evs[k].synchronize()  # the slot's previous upload is done
+                m = min(IO_SLOT, n - o)
+                jobs.append((k, o, m, pool.submit(os.preadv, fd, [views[k][:m]], o)))
+            for k, o, m, fut in jobs:
+                if fut.result() != m:
+                    raise MoeplaceError("parse_trace: short read (file changed while loading?)")
+                with t.cuda.stream(cs):
+                    dst[o:o + m].copy_(ring[k][:m], non_blocking=True)
+                    evs[k] = t.cuda.Event()
+                    evs[k].record(cs)
+            off += IO_LANES * IO_SLOT
+            half ^= 1
+        t.cuda.current_stream().wait_stream(cs)
+        for e in evs:
+            if e is not None:
+                e.synchronize()  # the ring is reusable once this returns
+
+
+def _device_to_file(src, n: int, fd: int, base: int) -> None:
+    """Bytes [base, base + n) of the open file ``fd`` <- src[:n] (device uint8)."""
+    t = _lib.torch()
+    with _IO_LOCK:
+        ring, pool = _io_ring()
+        views = [r.numpy() for r in ring]
+        cs = t.cuda.Stream()
+        cs.wait_stream(t.cuda.current_stream())
+        pending = []  # (future) writes of the previous half
+        off, half = 0, 0
+        while off < n:
+            batch = []
+            for r in range(IO_LANES):
+                o = off + r * IO_SLOT
+                if o >= n:
+                    break
+                k = half * IO_LANES + r
+                m = min(IO_SLOT, n - o)
+                with t.cuda.stream(cs):
+                    ring[k][:m].copy_(src[o:o + m], non_blocking=True)
+                    ev = t.cuda.Event()
+                    ev.record(cs)
+                batch.append((k, o, m, ev))
+            for fut in pending:  # the other half's writes overlap this half's downloads
+                fut.result()
+            pending = []
+            for k, o, m, ev in batch:
+                ev.synchronize()
+                pending.append(pool.submit(os.pwritev, fd, [views[k][:m]], base + o))
+            off += IO_LANES * IO_SLOT
+            half ^= 1
+        for fut in pending:
+            fut.result()
+
+
 def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
     """SPEC.md:132-139.  Parse the text trace format; errors raise ``TraceParseError`` with the
     1-based line number (header = line 1).  ``engine="cuda"`` (default) parses on the GPU
@@ -337,30 +430,31 @@ def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
         raise ConfigError(f"unknown parse engine {engine!r}")
     t = _lib.torch()
     dev = _lib.require_cuda()
-    raw = np.fromfile(path, dtype=np.uint8)
-    n = int(raw.size)
-    if n == 0:
-        return ActivationTrace(None, t.zeros((0, 16), dtype=t.uint8), 0, 0, np.zeros(0, np.int64),
-                               np.zeros(1, np.int64), source_is_file=True)
-    head_end = raw[:4096].tobytes().find(b"\n")
-    header = raw[:head_end if head_end >= 0 else min(n, 4096)].tobytes().decode("utf-8", "replace")
-    m = _HEADER.match(header.rstrip("\r"))
-    if not m:
-        raise TraceParseError("missing or malformed header '#moeplace-trace v1 L=<L> E=<E> K=<K>'", 1)
-    try:
-        model = ModelSpec(int(m.group(1)), int(m.group(2)), int(m.group(3)))
-    except ConfigError as e:
-        raise TraceParseError(str(e), 1) from None
-    if model.E > MAX_EXPERTS:
-        raise ConfigError(f"E = {model.E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
+    with open(path, "rb") as f:
+        n = os.fstat(f.fileno()).st_size
+        if n == 0:
+            return ActivationTrace(None, t.zeros((0, 16), dtype=t.uint8), 0, 0, np.zeros(0, np.int64),
+                                   np.zeros(1, np.int64), source_is_file=True)
+        head = f.read(4096)
+        head_end = head.find(b"\n")
+        header = head[:head_end if head_end >= 0 else min(n, 4096)].decode("utf-8", "replace")
+        m = _HEADER.match(header.rstrip("\r"))
+        if not m:
+            raise TraceParseError("missing or malformed header '#moeplace-trace v1 L=<L> E=<E> K=<K>'", 1)
+        try:
+            model = ModelSpec(int(m.group(1)), int(m.group(2)), int(m.group(3)))
+        except ConfigError as e:
+            raise TraceParseError(str(e), 1) from None
+        if model.E > MAX_EXPERTS:
+            raise ConfigError(f"E = {model.E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
+        last_byte = os.pread(f.fileno(), 1, n - 1)[0]
+        pad = (n + 32 + 15) // 16 * 16
+        text = t.empty(pad, dtype=t.uint8, device=dev)
+        text[n:].zero_()
+        _file_to_device(f.fileno(), n, text)  # pinned-ring pipeline: parallel preads + H2D
     if head_end < 0:
         head_end = n
     L, K = model.L, model.K
-    pad = (n + 32 + 15) // 16 * 16
-    host = t.empty(pad, dtype=t.uint8, pin_memory=True)
-    host[:n].copy_(t.from_numpy(raw))
-    host[n:].fill_(0)
-    text = host.to(dev, non_blocking=True)
     nb = (n + 65535) // 65536
     counts = t.empty(nb, dtype=t.int64, device=dev)
     sh = _lib.stream_handle()
@@ -371,7 +465,7 @@ def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
     _lib.call("mp_find_newlines", _lib.ptr(text), n, _lib.ptr(offsets), _lib.ptr(pos), sh)
     pos = pos[:total]
     ends = pos[1:] if total and int(pos[0].item()) == head_end else pos
-    if n > head_end + 1 and raw[-1] != 10:  # last line without a trailing newline
+    if n > head_end + 1 and last_byte != 10:  # last line without a trailing newline
         ends = t.cat([ends, t.tensor([n], dtype=t.int64, device=dev)])
     ends = ends.contiguous()
     N = int(ends.numel())
@@ -384,7 +478,7 @@ def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
     if e != 2 ** 63 - 1:
         line, code = e // 16, e % 16
         raise TraceParseError(_PARSE_ERR.get(code, f"parse error {code}"), int(line) + 2)
-    del text, host
+    del text
     cids = cids[:N]
     if N and not bool((cids[1:] >= cids[:-1]).all().item()):
         order = t.sort(cids, stable=True).indices  # regroup by chunk id
@@ -489,11 +583,10 @@ def write_trace(trace: ActivationTrace, path, engine: str = "auto") -> None:
     out = t.empty(total, dtype=t.uint8, device=dev)
     _lib.call("mp_format_trace_text", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
               _lib.ptr(cids), _lib.ptr(offs), _lib.ptr(out), sh)
-    host = t.empty(total, dtype=t.uint8, pin_memory=True)
-    host.copy_(out)
     with open(path, "wb") as f:
         f.write(header)
-        f.write(memoryview(host.numpy()))
+        f.flush()
+        _device_to_file(out, total, f.fileno(), len(header))
 
 
 def _write_trace_host(trace: ActivationTrace, path) -> None:
