@@ -411,9 +411,202 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
   return cudaGetLastError();
 }
 
+// ---- pipelined-flush streaming kernel (per-chunk histogram and count-contract) ----------------
+// The two-set kernel above needs one CTA barrier per (layer, chunk) piece: every warp waits for the
+// slowest one before the piece is flushed.  Here three replica sets rotate and the barrier is split:
+// a warp counts piece k into set k%3, then waits for piece k-1's completion (all threads arrived on
+// its mbarrier, normally long done), flushes piece k-1 and arrives on piece k's mbarrier.  Arriving
+// after the flush makes "phase k complete" imply "set (k-1)%3 flushed", which is what counting
+// piece k+2 into that set needs, so warps run up to one piece apart and never idle at a barrier.
+// Rows are 128 B (32 lane replicas) per set, so a bin's address is e*128 + set + lane*4 (PRMT byte
+// extract + IMAD on the FMA pipe); 3 x 32 KB of sets -> 2 CTAs/SM.
+#ifndef MP_PIPE_FLUSH
+#define MP_PIPE_FLUSH 1
+#endif
+constexpr int kPipeSets = 3;
+constexpr int kPipeSetBytes = 256 * 128;
+constexpr int kPipeSmem = kPipeSets * kPipeSetBytes;
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// ATOMS increments for bytes [xa, xb) of one plane into the set at shared address sb (= set base + lane*4)
+template <int UNROLL>
+__device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb, uint32_t sb) {
+  const uint32_t tid = threadIdx.x, T = blockDim.x;
+  const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
+  const int64_t tb = max(ha, xb & ~(int64_t)15);
+  for (int64_t x = xa + tid; x < ha; x += T) atoms_inc(sb + ((uint32_t)plane[x] << 7));
+  for (int64_t x = tb + tid; x < xb; x += T) atoms_inc(sb + ((uint32_t)plane[x] << 7));
+  const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
+  const uint32_t nv = (uint32_t)((tb - ha) >> 4);
+  auto vec = [&](const int4& x) {
+    const uint32_t wd[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) atoms_inc(prmt(wd[q], 0u, 0x4440u | (uint32_t)b) * 128u + sb);
+  };
+  uint32_t v = tid;
+  for (; v + (UNROLL - 1) * T < nv; v += UNROLL * T) {
+    int4 x[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) x[u] = ldg_stream(pv + v + u * T);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) vec(x[u]);
+  }
+  for (; v + 3 * T < nv; v += 4 * T) {
+    int4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = ldg_stream(pv + v + u * T);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vec(x[u]);
+  }
+  for (; v < nv; v += T) vec(ldg_stream(pv + v));
+}
+
+// WC == 0: per-chunk histogram, counts is int64 [C][L][E].  WC > 0: count-contract with WC-word
+// tables; counts (nullable) is int64 [L][E] and hop_sums int64 [4*WC][C].
+template <int WC, int UNROLL>
+__global__ void __launch_bounds__(kThreads, 2)
+pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+            const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
+            int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
+  extern __shared__ __align__(128) uint8_t sm[];  // kPipeSets x 256 rows x 128 B
+  __shared__ __align__(8) uint64_t bar[kPipeSets];
+  constexpr int PC = 4 * (WC > 0 ? WC : 1);
+  const int lane = threadIdx.x & 31;
+  const uint32_t base = smem_addr(sm);
+  const uint32_t bar0 = smem_addr(bar);
+  uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
+  for (int i = threadIdx.x; i < kPipeSmem / 4; i += blockDim.x) smw[i] = 0;
+  if (threadIdx.x == 0)
+    for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, blockDim.x);
+  __syncthreads();
+
+  // flush roles: two threads per bin (16 replicas each, rotated: a warp's 32 loads hit 32 banks)
+  const int fe = threadIdx.x >> 1, fh = threadIdx.x & 1;
+  uint32_t snap[kPipeSets] = {0u, 0u, 0u};
+  // piece k-1 awaiting its flush
+  int pk = -1, pl = 0, pc = 0;
+  uint32_t ptw[WC > 0 ? WC : 1];
+  auto flush_prev = [&]() {
+    const int set = pk % kPipeSets;
+    mbar_wait(bar0 + 8 * set, (uint32_t)((pk / kPipeSets) & 1));  // every thread finished counting piece pk
+    uint32_t part = 0;
+    if (fe < 256) {
+      const uint32_t* row = smw + set * (kPipeSetBytes / 4) + fe * 32;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part += row[(fh * 16 + i + fe) & 31];
+    }
+    uint32_t prev = snap[0];
+#pragma unroll
+    for (int b = 1; b < kPipeSets; ++b)
+      if (set == b) prev = snap[b];
+#pragma unroll
+    for (int b = 0; b < kPipeSets; ++b)
+      if (set == b) snap[b] = part;
+    const uint32_t d = part - prev;  // exact mod 2^32: the piece's count is < 2^32
+    uint32_t n = d + __shfl_xor_sync(0xffffffffu, d, 1);
+    if (fh) n = 0;  // even lane of each pair owns the bin
+    if constexpr (WC == 0) {
+      if (n) {
+        if (fe < E) atomic_add_i64(counts + ((int64_t)pc * L + pl) * E + fe, (int64_t)n);
+        else report_err(err, MP_DATA_EXPERT_RANGE, pl, fe, n);
+      }
+    } else {
+      if (n && counts) {
+        if (fe < E) atomic_add_i64(counts + (int64_t)pl * E + fe, (int64_t)n);
+        else report_err(err, MP_DATA_EXPERT_RANGE, pl, fe, n);
+      }
+      if (__any_sync(0xffffffffu, n != 0)) {
+        uint32_t v[PC];
+#pragma unroll
+        for (int w = 0; w < WC; ++w)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[4 * w + j] = n * ((ptw[w] >> (8 * j)) & 0xffu);
+        int q = 0;
+        const uint32_t tot = warp_reduce_scatter<PC>(v, lane, &q);
+        if ((lane & (32 / PC - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + pc, (int64_t)tot);
+      }
+    }
+  };
+
+  int k = 0;  // this CTA's piece counter
+  Flat f(t0 * K, t1 * K, L);
+  for (int64_t g = f.g0; g < f.g1;) {
+    const int l = (int)(g / f.nb);
+    const int64_t off_in = g - (int64_t)l * f.nb;
+    const int64_t seg = min(f.g1 - g, f.nb - off_in);
+    const int64_t x0 = f.b0 + off_in, x1 = x0 + seg;
+    const uint8_t* plane = planes + (int64_t)l * stride;
+    uint32_t tw[WC > 0 ? WC : 1];
+    if constexpr (WC > 0) {
+#pragma unroll
+      for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
+    }
+    int c = chunk_of(bounds, C, x0 / K);
+    int64_t cend = __ldg(bounds + c + 1) * K;
+    for (int64_t x = x0; x < x1;) {
+      while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
+      const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
+      const int set = k % kPipeSets;
+      pipe_count<UNROLL>(plane, x, xe, base + (uint32_t)(set * kPipeSetBytes) + (uint32_t)(lane << 2));
+      if (pk >= 0) flush_prev();
+      mbar_arrive(bar0 + 8 * set);  // counted piece k, flushed piece k-1
+      pk = k++;
+      pl = l;
+      pc = c;
+      if constexpr (WC > 0) {
+#pragma unroll
+        for (int w = 0; w < WC; ++w) ptw[w] = tw[w];
+      }
+      x = xe;
+    }
+    g += seg;
+  }
+  if (pk >= 0) flush_prev();
+}
+
+template <int WC>
+static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                               const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
+                               int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+  auto kern = pipe_kernel<WC, MP_COUNT_UNROLL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kPipeSmem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t total = (t1 - t0) * (int64_t)K * L;
+  int64_t grid = (int64_t)nsm * per_sm;
+  const int64_t min_bytes_per_cta = 64 * 1024;
+  grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
+  kern<<<(unsigned)grid, kThreads, kPipeSmem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
+                                                    hop_sums, err);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                                const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s) {
+#if MP_PIPE_FLUSH
+  return launch_pipe<0>(planes, stride, t0, t1, L, K, E, bounds, C, nullptr, counts, nullptr, err, s);
+#else
   return launch_t<true, 0, 16, true>(planes, stride, t0, t1, L, K, E, bounds, C, nullptr, counts, nullptr, err, s);
+#endif
 }
 
 // ---- exact contraction of per-chunk counts with per-expert costs (factorized evaluator) ----
@@ -545,9 +738,15 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
   }
   if (chosen == MP_ALGO_COUNT) {
     if (!hist) counts = nullptr;  // histogram stays in shared memory
+#if MP_PIPE_FLUSH
+    if (W == 1) return launch_pipe<1>(MP_ARGS);
+    if (W == 2) return launch_pipe<2>(MP_ARGS);
+    if (W == 4) return launch_pipe<4>(MP_ARGS);
+#else
     if (W == 1) return launch_t<true, 0, 16, true, 1>(MP_ARGS);
     if (W == 2) return launch_t<true, 0, 16, true, 2>(MP_ARGS);
     if (W == 4) return launch_t<true, 0, 16, true, 4>(MP_ARGS);
+#endif
     return cudaErrorInvalidValue;
   }
   if (hist) {
