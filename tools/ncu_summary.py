@@ -24,6 +24,10 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 def name_of(k):
     """stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED, WC> -> the bench's traffic keys."""
     import re
+    pm = re.search(r"pipe_kernel<(\d+), \d+>", k)  # pipelined-flush kernel: <WC, UNROLL>
+    if pm:
+        wc = int(pm.group(1))
+        return "hist_chunks" if wc == 0 else "fused" if wc == 1 else f"score_w{wc}"
     mm = re.search(r"stream_kernel<(\w+), (\d+), \d+, \d+(?:, (\w+))?(?:, (\d+))?>", k)
     if not mm:
         return k[:40]
