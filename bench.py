@@ -532,20 +532,28 @@ def main():
             kms_ = xa.elapsed_time(xb) / 10
             gbs = n * L * K / (kms_ / 1e3) / 1e9
             kernels_alone[nm] = {"ms": kms_, "GBps": gbs, "frac": gbs / peak}
-        # L1TEX model (one wavefront per SM per clock): per 512 B of trace one LDG.128 (4 wavefronts) and 16
-        # ATOMS (a each, a fitted live from mp_hist_u8 alone = 4 + 16a wavefronts per 512 B); the GATHER
-        # algorithm adds 16 LDS.32 (1 each).  The count-contract step needs only the histogram's wavefronts.
+        # L1TEX model (the SM's L1TEX/shared pipe moves one wavefront per clock): the step's wavefronts per
+        # launch are the shared-memory wavefronts ncu counted for the same kernel on the same trace
+        # (profiles/traffic.json, from the committed --set full capture; ATOMS + flush reads) plus one per
+        # 128 B of coalesced LDG.128; bound = wavefronts / (148 SMs x SM clock).
         mhz = (clocks or {}).get("sm_mhz") or 1965.0
-        blocks = n * L * K / 512 / 148  # 512-byte blocks per SM
         clk = mhz * 1e6
-        a = (kernels_alone["mp_hist_u8"]["ms"] / 1e3 * clk / blocks - 4) / 16
         if fused:
-            roofline["l1tex_model"] = {
-                "wavefronts_per_512B": {"LDG.128": 4, "ATOMS": 16 * a},
-                "atoms_wavefronts_per_instr": a, "sm_mhz": mhz,
-                "bound_ms": (4 + 16 * a) * blocks / clk * 1e3,
-                "frac_of_l1tex_bound": (4 + 16 * a) * blocks / clk * 1e3 / per_launch_ms,
-                "gather_bound_ms": (4 + 16 + 16 * a) * blocks / clk * 1e3}
+            try:
+                ent = json.loads((ROOT / "profiles" / "traffic.json").read_text())["fused"]
+                shw = ent["shared_wavefronts_per_launch"] * n / ent["tokens"]
+            except Exception:
+                shw = None
+            if shw:
+                ldg = n * L * K / 128
+                bound = (shw + ldg) / 148 / clk * 1e3
+                roofline["l1tex_model"] = {
+                    "shared_wavefronts_per_launch": shw, "ldg_wavefronts_per_launch": ldg,
+                    "wavefronts_per_512B": (shw + ldg) / (n * L * K / 512), "sm_mhz": mhz, "bound_ms": bound,
+                    "frac_of_l1tex_bound": bound / per_launch_ms,
+                    "shared_wavefronts_per_atoms_instr": shw / (n * L * K / 32),
+                    "source": "ncu --set full capture (profiles/r1_ncu_summary.md): "
+                              "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"}
 
     # ------- configs 2/4: the factorized evaluator beside the measured gather (not the headline) -------
     factorized = None

@@ -55,7 +55,9 @@ for r in rows[2:]:
             vals[m] = (r[i], units[i])
     rd = float(vals["dram__bytes_read.sum"][0].replace(",", "")) * SCALE.get(vals["dram__bytes_read.sum"][1], 1)
     wr = float(vals["dram__bytes_write.sum"][0].replace(",", "")) * SCALE.get(vals["dram__bytes_write.sum"][1], 1)
-    traffic.setdefault(nm, {"tokens": tokens, "dram_bytes_per_launch": rd + wr, "alg_bytes": tokens * 58 * 8})
+    shw = float(vals["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][0].replace(",", ""))
+    traffic.setdefault(nm, {"tokens": tokens, "dram_bytes_per_launch": rd + wr, "alg_bytes": tokens * 58 * 8,
+                            "shared_wavefronts_per_launch": shw})
     out.append((nm, vals, rd + wr))
 with open(md, "w") as f:
     f.write(f"# ncu --set full summary ({rep}; R1, {tokens} tokens, Zipf 1.2)\n\n")
