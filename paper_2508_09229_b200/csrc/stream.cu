@@ -711,9 +711,18 @@ cudaError_t launch_digit_combine(const int32_t* part, int P, int64_t ldp, int C,
 // lookup (1/2/4 wavefronts per 32 lookups for W = 1/2/4) on top of the histogram's ATOMS when both are
 // needed; count-contract costs only the histogram.  Measured (R1, 10M tokens): gather W=1 0.80 ms,
 // W=2 1.25, W=4 2.25, fused hist+gather 1.36; count-contract 0.91-0.93 for any W, with or without counts.
+// Token-tiled wins below a per-shape tokens-per-chunk threshold (R1, 10M tokens, crossovers measured
+// in profiles/r1_chunk_granularity.txt): its cost is flat in C but grows with W (1.31 / 2.61 / 5.2 ms
+// for W = 1 / 2 / 4, + 0.83 ms histogram), while the streaming algorithms pay per (layer, chunk) piece.
+int token_threshold(bool hist, int W) {
+  if (W <= 1) return hist ? MP_TOKEN_CHUNK_TOKENS : 2 * MP_TOKEN_CHUNK_TOKENS - 1024;  // 2560 / 4096
+  if (W == 2) return hist ? MP_TOKEN_CHUNK_TOKENS / 2 : 1600;                         // 1280 / 1600
+  return hist ? 700 : 800;
+}
+
 int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K, int max_p) {
   if (algo != MP_ALGO_AUTO) return algo;
-  if (tokens < (int64_t)MP_TOKEN_CHUNK_TOKENS * C && (int64_t)L * K * max_p <= 65535) return MP_ALGO_TOKEN;
+  if (tokens < (int64_t)token_threshold(hist, W) * C && (int64_t)L * K * max_p <= 65535) return MP_ALGO_TOKEN;
   return (hist || W > 1) ? MP_ALGO_COUNT : MP_ALGO_GATHER;
 }
 
