@@ -15,6 +15,10 @@
 // An expert byte b of a loaded word becomes its row offset (e << 8) | slot with a single
 // PRMT, so a lookup costs PRMT + LDS (gather) and/or PRMT + ATOMS (histogram).  The trace is
 // streamed with 128-bit L1-no-allocate loads, UNROLL vectors per thread per main-loop batch.
+// The count-contract and per-chunk-histogram instances run pipe_kernel instead (three rotating
+// replica sets of 128-byte rows and per-set mbarriers in place of a CTA barrier per piece; see
+// the comment above pipe_kernel); stream_kernel keeps the gather, the plain histogram and the
+// MP_PIPE_FLUSH=0 comparison build.
 #include <algorithm>
 #include "common.cuh"
 
