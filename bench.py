@@ -614,13 +614,14 @@ def main():
     e2e = None
     if not args.no_e2e:
         host = trace.to_host(pin=True)
+        cand_host = torch.from_numpy(cand).pin_memory() if fact else None
         steps_e = max(1, args.e2e_steps if wl != 5 else 1)
 
         def api_call():
             if with_hist:
                 return ev.evaluate_with_stats(host, placements, costs[0])[0].counts
-            if fact:
-                return ev.evaluate_many(host, placements, costs)  # auto -> factorized for P > 16
+            if fact:  # the candidate batch as one pinned host array, as a search loop holds it
+                return ev.evaluate_batch(host, cand_host, costs[0])  # auto -> factorized for P > 16
             return ev.score_sums(host, placements, costs)
 
         api_call()  # warm-up
@@ -642,11 +643,12 @@ def main():
             dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e_ms = float(t_e.item())
         api = ("moeplace.eval.evaluate_with_stats(trace in pinned host memory, 4 placements, cost)" if with_hist
-               else f"moeplace.eval.evaluate_many(trace in pinned host memory, {P_} placements, method='auto' "
-                    f"-> factorized; per-placement pe tables built inside the call)" if fact
+               else f"moeplace.eval.evaluate_batch(trace and the int32 [{P_}, L, E] candidate batch in pinned host "
+                    f"memory, method='auto' -> factorized; pe tables, contraction and per-candidate floats inside "
+                    f"the call)" if fact
                else f"moeplace.eval.score_sums(trace in pinned host memory, {P_} placements)")
         e2e = {"value": n_total * L * P_ / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(n * L * K * world),
+               "h2d_bytes_per_step": int(n * L * K * world + (cand.nbytes if fact else 0)),
                "d2h_bytes_per_step": int(((L * E if with_hist else 0) + P_ * C) * 8 * world), "api": api}
         del host
 

@@ -81,21 +81,35 @@ def report_from_sums(sums: np.ndarray, tokens: np.ndarray, label: str = "") -> E
                       chunk_hop_sums=sums.tolist())
 
 
-def reports_from_sums(sums: np.ndarray, tokens: np.ndarray, labels: Sequence[str]) -> list[EvalReport]:
-    """``report_from_sums`` for every row of int64 [P, C] at once (batched evaluation).  Same floats
-    bit for bit: the per-chunk means form a C-contiguous [P, C'] array, so numpy's row reductions
-    add in the same order as its 1-D ones, and totals / n_tokens is the same Python int division."""
+def _batch_floats(sums: np.ndarray, tokens: np.ndarray):
+    """Row-wise EvalReport floats of int64 [P, C] per-chunk sums, bit-identical to
+    ``report_from_sums`` per row: the per-chunk means form a C-contiguous [P, C'] array, so numpy's
+    row reductions add in the same order as its 1-D ones, and totals / n_tokens is an exactly
+    rounded division of exact integers (totals < 2^53 convert to float64 exactly; larger totals
+    take Python's int division)."""
     sums = np.asarray(sums, dtype=np.int64)
     tokens = np.asarray(tokens, dtype=np.int64)
     keep = tokens > 0
     n_tok = int(tokens.sum())
     if n_tok == 0:
         raise MoeplaceError("evaluate: empty trace")
-    totals = sums.sum(axis=1).tolist()
-    stds = np.std(np.ascontiguousarray(sums[:, keep]) / tokens[keep], axis=1).tolist()
-    n_chunks, n_empty = int(keep.sum()), int((~keep).sum())
+    totals = sums.sum(axis=1)
+    if totals.size and int(np.abs(totals).max()) >= 2 ** 53:
+        means = np.array([t / n_tok for t in totals.tolist()], dtype=np.float64)
+    else:
+        means = totals.astype(np.float64) / n_tok
+    stds = np.std(np.ascontiguousarray(sums[:, keep]) / tokens[keep], axis=1)
+    return totals, means, stds, n_tok, int(keep.sum()), int((~keep).sum())
+
+
+def reports_from_sums(sums: np.ndarray, tokens: np.ndarray, labels: Sequence[str]) -> list[EvalReport]:
+    """``report_from_sums`` for every row of int64 [P, C] at once (batched evaluation), same floats
+    bit for bit (``_batch_floats``)."""
+    sums = np.asarray(sums, dtype=np.int64)
+    totals, means, stds, n_tok, n_chunks, n_empty = _batch_floats(sums, tokens)
+    totals, means, stds = totals.tolist(), means.tolist(), stds.tolist()
     rows = sums.tolist()
-    return [EvalReport(mean_hops_per_token=totals[i] / n_tok, std_hops=stds[i], n_tokens=n_tok, n_chunks=n_chunks,
+    return [EvalReport(mean_hops_per_token=means[i], std_hops=stds[i], n_tokens=n_tok, n_chunks=n_chunks,
                        label=labels[i], empty_chunks=n_empty, hop_sum=totals[i], chunk_hop_sums=rows[i])
             for i in range(sums.shape[0])]
 
@@ -254,14 +268,21 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, a
 def pe_matrix(placements: Sequence[Placement], costs, model: ModelSpec):
     """uint8 [P, L*E] per-expert round-trip costs pe_q[l, e] = p_q[l, assign_q[l, e]] on the device
     (one batched gather per distinct cost matrix)."""
-    t = _lib.torch()
     placements = list(placements)
     costs = _as_costs(costs, len(placements))
-    dev = _lib.require_cuda()
-    assign = _assign_to_device(placements, costs, model).long()
+    return _pe_from_device_assign(_assign_to_device(placements, costs, model).long(), costs, model)
+
+
+def _pe_from_device_assign(assign, costs: Sequence[CostMatrix], model: ModelSpec):
+    """pe uint8 [P, L*E] from checked device assignments int64 [P, L, E]."""
+    t = _lib.torch()
+    dev = assign.device
     uniq, topo_of = _unique_costs(costs)
     topo_of = np.asarray(topo_of)
-    out = t.empty((len(placements), model.L * model.E), dtype=t.uint8, device=dev)
+    if len(uniq) == 1:  # one topology: a single gather, no index copies
+        P = assign.shape[0]
+        return t.gather(uniq[0].p.unsqueeze(0).expand(P, -1, -1), 2, assign).reshape(P, -1)
+    out = t.empty((assign.shape[0], model.L * model.E), dtype=t.uint8, device=dev)
     for ti, c in enumerate(uniq):
         idx = t.as_tensor(np.flatnonzero(topo_of == ti), device=dev)
         sel = assign.index_select(0, idx)
@@ -379,6 +400,70 @@ def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs
     else:
         raise ConfigError(f"unknown evaluate method {method!r}")
     return reports_from_sums(sums, trace.chunk_token_counts(), [p.label for p in placements])
+
+
+@dataclass
+class BatchReport:
+    """``evaluate_batch`` result: the EvalReport fields of P placements as arrays, row q = placement
+    q (same values, bit for bit, as ``evaluate_many``'s EvalReports)."""
+
+    mean_hops_per_token: np.ndarray  # float64 [P]
+    std_hops: np.ndarray             # float64 [P]
+    hop_sum: np.ndarray              # int64 [P], exact
+    chunk_hop_sums: np.ndarray       # int64 [P, C], exact, chunk id order
+    n_tokens: int
+    n_chunks: int
+    empty_chunks: int
+
+    def report(self, q: int, label: str = "") -> EvalReport:
+        return EvalReport(mean_hops_per_token=float(self.mean_hops_per_token[q]), std_hops=float(self.std_hops[q]),
+                          n_tokens=self.n_tokens, n_chunks=self.n_chunks, label=label,
+                          empty_chunks=self.empty_chunks, hop_sum=int(self.hop_sum[q]),
+                          chunk_hop_sums=self.chunk_hop_sums[q].tolist())
+
+
+def evaluate_batch(trace: ActivationTrace, assign, costs, method: str = "auto") -> BatchReport:
+    """``evaluate_many`` for a candidate batch given as one integer array ``assign`` [P, L, E]
+    (numpy or torch, host or device; e.g. ``placement.perturb_swaps`` output), extension A18 for
+    search loops: the batch moves to the device in one copy, is range-checked there, and the
+    result is arrays instead of P report objects.  ``costs``: one CostMatrix, or one per
+    placement.  ``method`` as in ``evaluate_many``."""
+    t = _lib.torch()
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        raise MoeplaceError("evaluate: empty trace")
+    dev = _lib.require_cuda()
+    a = assign if isinstance(assign, t.Tensor) else t.from_numpy(np.ascontiguousarray(assign))
+    if a.dim() != 3 or tuple(a.shape[1:]) != (m.L, m.E):
+        raise ConfigError(f"assign batch shape {tuple(a.shape)} != [P, {m.L}, {m.E}]")
+    if a.dtype.is_floating_point or a.dtype == t.bool:
+        raise ConfigError("assign batch must hold integer device ids")
+    P = int(a.shape[0])
+    costs = _as_costs(costs, P)
+    a = a.to(dev, non_blocking=a.is_pinned()).long()
+    S = t.as_tensor(np.asarray([c.S for c in costs], dtype=np.int64), device=dev)
+    flat = a.view(P, -1)
+    bad = (flat.amin(1) < 0) | (flat.amax(1) >= S)
+    if bool(bad.any()):
+        q = int(t.nonzero(bad)[0, 0])
+        raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {q}, {costs[q].S} devices)")
+    if method == "auto":
+        fact_bytes = trace.n_chunks * m.L * m.E * 8
+        method = "factorized" if P > MAX_LANES and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
+    if method == "factorized":
+        cnt = chunk_counts(trace)
+        pe = _pe_from_device_assign(a, costs, m)
+        max_pe = max(c.max_p for c in _unique_costs(costs)[0])
+        sums = contract_tc(cnt.view(trace.n_chunks, -1), pe, max_count=int(np.max(trace.chunk_token_counts())),
+                           max_pe=max_pe).cpu().numpy()
+    elif method in ("gather", "count", "token", "pass"):
+        host = a.to(t.int32).cpu().numpy()
+        pls = [Placement(host[q]) for q in range(P)]
+        sums = score_sums(trace, pls, costs, algo="auto" if method == "pass" else method)
+    else:
+        raise ConfigError(f"unknown evaluate method {method!r}")
+    totals, means, stds, n_tok, n_chunks, n_empty = _batch_floats(sums, trace.chunk_token_counts())
+    return BatchReport(means, stds, totals, np.asarray(sums, dtype=np.int64), n_tok, n_chunks, n_empty)
 
 
 def evaluate(trace: ActivationTrace, placement: Placement, cost: CostMatrix) -> EvalReport:

@@ -187,6 +187,35 @@ def test_public_api_algorithms_and_wide_stats_pass():
         ev.evaluate_with_stats(tr, pls[:17], costs[:17])
 
 
+def test_evaluate_batch_matches_evaluate_many():
+    """evaluate_batch (one [P, L, E] array: numpy, torch host/pinned or device) gives the same
+    integers and floats as evaluate_many's EvalReports, factorized (P > 16) and per pass, and
+    rejects out-of-range devices and bad shapes."""
+    import torch
+    from moeplace.errors import ConfigError, MoeplaceError
+    from helpers import setup_topology
+    L, E, K = B16
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, 1.2, 2501, 9, 8)
+    g, dist, order, attn, cost = setup_topology("Dragonfly", 4, 2, 4, m)
+    base = mpl.place_round_robin(m, attn, order, mpl.Constraints(64, 2))
+    cand = mpl.perturb_swaps(base, 21, 5, 300)
+    pls = [mpl.Placement(cand[i]) for i in range(cand.shape[0])]
+    for n in (21, 6):
+        want = ev.evaluate_many(tr, pls[:n], cost)
+        for arr in (cand[:n], torch.from_numpy(cand[:n]).pin_memory(), torch.from_numpy(cand[:n]).cuda()):
+            for method in ("auto", "factorized", "count"):
+                b = ev.evaluate_batch(tr, arr, cost, method=method)
+                assert b.chunk_hop_sums.tolist() == [r.chunk_hop_sums for r in want], (n, method)
+                assert [b.report(q) for q in range(n)] == [ev.EvalReport(**{**r.__dict__, "label": ""}) for r in want]
+    bad = cand[:3].copy()
+    bad[1, 2, 3] = g.n_devices
+    with pytest.raises(MoeplaceError, match="placement 1"):
+        ev.evaluate_batch(tr, bad, cost)
+    with pytest.raises(ConfigError):
+        ev.evaluate_batch(tr, cand[:, :2], cost)
+
+
 def test_plane_offsets_beyond_2_pow_31():
     """One plane longer than 2^31 bytes (N*K = 2.4e9): 64-bit byte offsets through every piece
     of both algorithms.  Properties: per-layer counts sum to N*K, constant costs give exactly
