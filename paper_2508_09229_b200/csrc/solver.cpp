@@ -21,6 +21,8 @@
 #include <vector>
 #include <queue>
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <limits>
 #include "../../include/moeplace_cuda.h"
 
@@ -159,36 +161,18 @@ struct MCF {
 
 }  // namespace
 
-extern "C" int mp_solve_mcf(const int64_t* w, const uint8_t* p, int L, int E, int S, int c_layer, int c_exp,
-                            int32_t* assign_out, int64_t* objective_out, int64_t* flow_out) {
-  if (!w || !assign_out || L <= 0 || E <= 0 || S <= 0 || c_layer <= 0 || c_exp <= 0) return MP_ERR_ARG;
-  const int64_t LE = (int64_t)L * E;
-  for (int64_t i = 0; i < LE * S; ++i)
-    if (w[i] < 0) return MP_ERR_ARG;
-
-  // class compression is exact only if w depends on s through p alone
-  bool compress = p != nullptr;
-  std::vector<std::vector<int>> cls_of(L);     // per layer: class id per device
-  std::vector<std::vector<int>> cls_rep(L);    // per layer: representative device per class
-  if (compress) {
-    for (int l = 0; l < L; ++l) {
-      std::vector<int> id_of_val(256, -1);
-      cls_of[l].resize(S);
-      for (int s = 0; s < S; ++s) {
-        const int v = p[(int64_t)l * S + s];
-        if (id_of_val[v] < 0) { id_of_val[v] = (int)cls_rep[l].size(); cls_rep[l].push_back(s); }
-        cls_of[l][s] = id_of_val[v];
-      }
-    }
-    for (int l = 0; l < L && compress; ++l)
-      for (int e = 0; e < E && compress; ++e) {
-        const int64_t* row = w + ((int64_t)l * E + e) * S;
-        for (int s = 0; s < S; ++s)
-          if (row[s] != row[cls_rep[l][cls_of[l][s]]]) { compress = false; break; }
-      }
-  }
-
+// Min-cost flow over layers [l0, l1) (indices into the full w / p / assign arrays).
+static int solve_layers(const int64_t* w, const uint8_t* p, int l0, int l1, int E, int S, int c_layer, int c_exp,
+                        bool compress, const std::vector<int>* cls_of_all, const std::vector<int>* cls_rep_all,
+                        int32_t* assign_out, int64_t* objective_out, int64_t* flow_out) {
   // node numbering
+  const int L = l1 - l0;
+  const int64_t LE = (int64_t)L * E;
+  w += (int64_t)l0 * E * S;
+  if (p) p += (int64_t)l0 * S;
+  assign_out += (int64_t)l0 * E;
+  const std::vector<int>* cls_of = cls_of_all + l0;
+  const std::vector<int>* cls_rep = cls_rep_all + l0;
   const int src = 0;
   const int item0 = 1;
   std::vector<int> mid0(L + 1);  // first class/slot node of layer l
@@ -224,8 +208,8 @@ extern "C" int mp_solve_mcf(const int64_t* w, const uint8_t* p, int L, int E, in
 
   int64_t cost = 0;
   const int64_t flow = g.run(src, sink, LE, &cost);
-  if (flow_out) *flow_out = flow;
-  if (objective_out) *objective_out = cost;
+  *flow_out += flow;
+  *objective_out += cost;
   if (flow < LE) return MP_INFEASIBLE;
 
   // read back the assignment
@@ -252,4 +236,71 @@ extern "C" int mp_solve_mcf(const int64_t* w, const uint8_t* p, int L, int E, in
     }
   }
   return MP_OK;
+}
+
+extern "C" int mp_solve_mcf(const int64_t* w, const uint8_t* p, int L, int E, int S, int c_layer, int c_exp,
+                            int32_t* assign_out, int64_t* objective_out, int64_t* flow_out) {
+  if (!w || !assign_out || L <= 0 || E <= 0 || S <= 0 || c_layer <= 0 || c_exp <= 0) return MP_ERR_ARG;
+  const int64_t LE = (int64_t)L * E;
+  for (int64_t i = 0; i < LE * S; ++i)
+    if (w[i] < 0) return MP_ERR_ARG;
+
+  // class compression is exact only if w depends on s through p alone
+  bool compress = p != nullptr;
+  std::vector<std::vector<int>> cls_of(L);     // per layer: class id per device
+  std::vector<std::vector<int>> cls_rep(L);    // per layer: representative device per class
+  if (compress) {
+    for (int l = 0; l < L; ++l) {
+      std::vector<int> id_of_val(256, -1);
+      cls_of[l].resize(S);
+      for (int s = 0; s < S; ++s) {
+        const int v = p[(int64_t)l * S + s];
+        if (id_of_val[v] < 0) { id_of_val[v] = (int)cls_rep[l].size(); cls_rep[l].push_back(s); }
+        cls_of[l][s] = id_of_val[v];
+      }
+    }
+    for (int l = 0; l < L && compress; ++l)
+      for (int e = 0; e < E && compress; ++e) {
+        const int64_t* row = w + ((int64_t)l * E + e) * S;
+        for (int s = 0; s < S; ++s)
+          if (row[s] != row[cls_rep[l][cls_of[l][s]]]) { compress = false; break; }
+      }
+  }
+
+  // Decoupled layers: when L * c_layer <= c_exp the per-device total can never exceed c_exp (each
+  // layer puts at most c_layer experts on a device), so the c_exp arcs carry no constraint and
+  // the problem splits into L independent per-layer flows -- same optimum, each a network of
+  // E items and a handful of classes (all BASELINE configs; 125 s -> well under a second for
+  // four R1 topologies).  Otherwise one network over all layers.
+  int64_t cost = 0, flow = 0;
+  int rc = MP_OK;
+  if ((int64_t)L * c_layer <= (int64_t)c_exp) {
+    // independent layers on host threads (each layer's flow is deterministic; rows are disjoint)
+    const int nt = (int)std::max(1u, std::min<unsigned>((unsigned)L, std::min(16u, std::thread::hardware_concurrency())));
+    std::atomic<int> next(0);
+    std::vector<int64_t> t_cost(nt, 0), t_flow(nt, 0);
+    std::vector<int> t_rc(nt, MP_OK);
+    auto work = [&](int t) {
+      for (int l = next++; l < L; l = next++) {
+        const int r = solve_layers(w, p, l, l + 1, E, S, c_layer, c_exp, compress, cls_of.data(), cls_rep.data(),
+                                   assign_out, &t_cost[t], &t_flow[t]);
+        if (r != MP_OK) t_rc[t] = r;
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < nt; ++t) {
+      cost += t_cost[t];
+      flow += t_flow[t];
+      if (t_rc[t] != MP_OK) rc = t_rc[t];
+    }
+  } else {
+    rc = solve_layers(w, p, 0, L, E, S, c_layer, c_exp, compress, cls_of.data(), cls_rep.data(), assign_out, &cost,
+                      &flow);
+  }
+  if (flow_out) *flow_out = flow;
+  if (objective_out) *objective_out = cost;
+  return rc;
 }

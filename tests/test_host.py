@@ -261,7 +261,8 @@ def test_solver_equals_brute_force_100_instances():
 
 
 def test_solver_compressed_network_matches_highs():
-    """Class-compressed network (w = f*p) vs scipy HiGHS LP on the full network."""
+    """Class-compressed network (w = f*p) vs scipy HiGHS LP on the full network, with c_exp binding
+    (one network over all layers) and slack (L*c_layer <= c_exp: independent per-layer flows)."""
     from scipy.optimize import linprog
     from scipy.sparse import lil_matrix
     rng = np.random.default_rng(7)
@@ -271,7 +272,7 @@ def test_solver_compressed_network_matches_highs():
         f = rng.random((L, E))
         f /= f.sum(axis=1, keepdims=True)
         w, wi = ot.coefficients(f, p)
-        c = mpl.Constraints(5, 2)
+        c = mpl.Constraints(5, 2) if trial % 2 == 0 else mpl.Constraints(6, 2)
         inst = sv.PlacementInstance(w, wi, c, L, E, S, p)
         pl, obj = sv.solve_exact(inst)
         n = L * E * S
