@@ -133,3 +133,41 @@ def test_gather_and_count_contract_agree(c, W, hi, S):
         f, reps = ev.evaluate_with_stats(tr, pls[:n], cost, algo=algo)
         assert np.array_equal(f.counts, ost.counts(sel, E))
         assert [r.chunk_hop_sums for r in reps] == want[:n].tolist()
+
+
+@st.composite
+def big_case(draw):
+    L = draw(st.integers(1, 8))
+    E = draw(st.sampled_from([16, 64, 256]))
+    K = draw(st.integers(1, 8))
+    N = draw(st.integers(5_000, 300_000))
+    C = draw(st.integers(1, 5_000))
+    return L, E, K, N, C, draw(st.integers(0, 2 ** 31)), draw(st.sampled_from([0.0, 1.2, 2.0]))
+
+
+@settings(max_examples=int(__import__("os").environ.get("MP_STRESS_EXAMPLES", "8")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(big_case(), st.sampled_from([1, 2, 4]))
+def test_pipelined_flush_multi_cta_stress(c, W):
+    """Many CTAs, pieces cut by chunk and CTA boundaries, 1-5000 chunks: the pipelined-flush
+    count-contract (three rotating replica sets, per-set mbarriers) and per-chunk histogram equal
+    the per-byte gather and numpy on the same trace."""
+    L, E, K, N, C, seed, s = c
+    m = mt.ModelSpec(L, E, K)
+    tr = mt.generate_trace(m, s, N, C, seed)
+    rng = np.random.default_rng(seed % 991)
+    cost, p = _cost(rng, L, 23, 31)
+    pls = [mpl.Placement(rng.integers(0, 23, (L, E)).astype(np.int32)) for _ in range(4 * W)]
+    want = ev.score_sums(tr, pls, cost, algo="gather")
+    assert np.array_equal(ev.score_sums(tr, pls, cost, algo="count"), want)
+    f, reps = ev.evaluate_with_stats(tr, pls[:4 * W], cost, algo="count")
+    sel = tr.tokens()
+    hist = np.stack([np.bincount(sel[:, l, :].ravel(), minlength=E) for l in range(L)])
+    assert np.array_equal(f.counts, hist)
+    assert [r.chunk_hop_sums for r in reps] == want.tolist()
+    cc = mt.chunk_counts(tr).cpu().numpy()  # per-chunk histogram (pipelined flush, WC = 0)
+    assert np.array_equal(cc.sum(axis=0), hist)
+    b = tr.chunk_bounds
+    for c_ in sorted({0, tr.n_chunks // 2, tr.n_chunks - 1}):
+        part = sel[b[c_]:b[c_ + 1]]
+        assert np.array_equal(cc[c_], np.stack([np.bincount(part[:, l, :].ravel(), minlength=E) for l in range(L)]))
