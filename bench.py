@@ -180,6 +180,25 @@ def run_reference(args, rank: int, world: int) -> None:
     emit(line)
 
 
+def bind_local_cpus(torch, local: int) -> None:
+    """Restrict this rank to the CPUs local to its GPU (sysfs local_cpulist of the GPU's PCI
+    function, intersected with the allowed set), so its pinned host buffers are first-touched on
+    the GPU's NUMA node; a no-op on single-node hosts or when sysfs has no answer."""
+    try:
+        p = torch.cuda.get_device_properties(local)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        cl = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        cpus = set()
+        for part in cl.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus and cpus != os.sched_getaffinity(0):
+            os.sched_setaffinity(0, cpus)
+    except Exception:  # noqa: BLE001 -- best effort
+        pass
+
+
 def emit(line):  # replaced in main() by a writer to the saved stdout descriptor
     print(json.dumps(line), flush=True)
 
@@ -237,6 +256,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        bind_local_cpus(torch, local)  # pinned trace copies land on the GPU's NUMA node
         dist.init_process_group("nccl", device_id=dev)
     wl = args.workload
     model = mt.ModelSpec(L, E, K)
