@@ -133,6 +133,28 @@ def time_oracle(sel, bounds, p, assigns, reps: int = 3, t0: int = 0):
     return best
 
 
+def host_info(run_1thread) -> dict:
+    """SURVEY §8(d) CPU-baseline context: allowed CPUs, CPU model, NUMBA_NUM_THREADS and a
+    single-thread rate (run_1thread() -> token-layers*placements/s with numba set to 1 thread)."""
+    info = {"cpus_allowed": len(os.sched_getaffinity(0)),
+            "numba_num_threads_env": os.environ.get("NUMBA_NUM_THREADS")}
+    try:
+        info["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        import numba
+        n0 = numba.get_num_threads()
+        numba.set_num_threads(1)
+        try:
+            info["value_1thread"] = run_1thread()
+        finally:
+            numba.set_num_threads(n0)
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
 def cpu_threads() -> int:
     try:
         import numba
@@ -169,13 +191,17 @@ def run_reference(args, rank: int, world: int) -> None:
     times = [time_oracle(sel, bounds, p, assigns, reps=1) for _ in range(args.steps)]
     t = float(np.mean(times))
     value = n_sample * L * P / t
+    n1 = min(n_sample, 100_000)
+    b1 = np.minimum(bounds, n1)
+    host = host_info(lambda: n1 * L * P / time_oracle(sel[:n1], b1, p, assigns, reps=2))
     sample = (f"{n_sample} tokens (first {n_sample} of the config-2 trace, regenerated on the CPU), counts + "
               f"hop sums of {P} placements per step; numba parallel, {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": workload(world, TOK_PER_GPU, "cpu-oracle"),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             **host, "sample_1thread": f"first {n1} tokens, 1 numba thread"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -439,10 +465,19 @@ def main():
                "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P_} "
                          f"placements in one pass, oracle/ numba parallel, best of 5, measured before any GPU timing",
                "ms_per_sample": t_cpu * 1e3}
-        try:
-            cpu["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
-        except Exception:
-            pass
+        n1 = min(ns, 100_000 if wl != 4 else 500)
+        b1 = np.minimum(bnd, n1)
+
+        def one_thread():
+            best = float("inf")
+            for _ in range(2):
+                t_a = time.perf_counter()
+                oe.fused_pass(sel[:n1], pes, b1, E)
+                best = min(best, time.perf_counter() - t_a)
+            return n1 * L * P_ / best
+
+        cpu.update(host_info(one_thread))
+        cpu["sample_1thread"] = f"first {n1} tokens, 1 numba thread"
 
     launches_per_step = 1 if (fused or fact) else len(groups) + (1 if with_hist else 0)
     run = fstep if fact else step
