@@ -227,15 +227,16 @@ def _lanes_for(n: int) -> int:
     return 1 if n <= 4 else 2 if n <= 8 else 4
 
 
-ALGOS = {"auto": 0, "gather": 1, "count": 2, "token": 3}  # include/moeplace_cuda.h MP_ALGO_*
+ALGOS = {"auto": 0, "gather": 1, "count": 2, "token": 3, "seg": 4}  # include/moeplace_cuda.h MP_ALGO_*
 
 
 def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, algo: str = "auto") -> np.ndarray:
     """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_ex_u8``), up to 16
     placements per pass.  ``algo``: "gather" (per-byte table lookups), "count" (count-contract:
     per-(layer, chunk) histograms contracted with the tables), "token" (token-tiled: per-token sums
-    across layers reduced per chunk; cost independent of the chunk count) or "auto" (the library's
-    choice for the shape); all give the same integers."""
+    across layers reduced per chunk; cost independent of the chunk count), "seg" (segmented gather:
+    warps own contiguous token ranges and reduce at each chunk boundary; C-independent, K = 8 and
+    costs <= 31) or "auto" (the library's choice for the shape); all give the same integers."""
     if algo not in ALGOS:
         raise ConfigError(f"unknown score algorithm {algo!r}")
     t = _lib.torch()
@@ -484,8 +485,8 @@ def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement],
         raise MoeplaceError("evaluate: empty trace")
     if algo not in ALGOS:
         raise ConfigError(f"unknown score algorithm {algo!r}")
-    if not 1 <= len(placements) <= (4 if algo == "gather" else MAX_LANES):
-        raise ConfigError(f"evaluate_with_stats takes 1..{4 if algo == 'gather' else MAX_LANES} placements")
+    if not 1 <= len(placements) <= (4 if algo in ("gather", "seg") else MAX_LANES):
+        raise ConfigError(f"evaluate_with_stats takes 1..{4 if algo in ('gather', 'seg') else MAX_LANES} placements")
     dev = _lib.require_cuda()
     W = _lanes_for(len(placements))
     tables, max_p = _group_tables(placements, _as_costs(cost, len(placements)), m, W)

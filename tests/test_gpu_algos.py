@@ -15,7 +15,7 @@ from helpers import B16, R1, oracle_sums, random_assign
 
 pytestmark = pytest.mark.gpu
 
-AUTO, GATHER, COUNT, TOKEN = 0, 1, 2, 3
+AUTO, GATHER, COUNT, TOKEN, SEG = 0, 1, 2, 3, 4
 
 
 def _tables(pls, p, m, W):
@@ -51,11 +51,12 @@ def _check(tr, sel, bounds, t0, pls, p, W, hist_ws=(1,)):
     want = np.zeros((4 * W, len(bounds) - 1), np.int64)
     for i, pl in enumerate(pls):
         want[i] = oracle_sums(sel, p, pl.assign, bounds, t0)
-    algos = (AUTO, GATHER, COUNT) + ((TOKEN,) if m.L * m.K * max_p <= 65535 else ())
+    algos = (AUTO, GATHER, COUNT) + ((TOKEN,) if m.L * m.K * max_p <= 65535 else ()) + \
+        ((SEG,) if m.K == 8 and max_p <= 31 else ())
     for algo in algos:
         s, _, _ = _run(tr, tables, W, max_p, algo, hist=False)
         assert np.array_equal(s, want), ("score", W, algo)
-        if W in hist_ws or algo != GATHER:
+        if W in hist_ws or algo not in (GATHER, SEG):
             s, c, e = _run(tr, tables, W, max_p, algo, hist=True)
             assert np.array_equal(s, want), ("hist_score", W, algo)
             assert np.array_equal(c, ost.counts(sel, m.E)), ("counts", W, algo)
@@ -152,6 +153,10 @@ def test_argument_rules_of_the_explicit_entry_points():
     assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 2, 8, P, P, P, GATHER, None) == 3
     assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 3, 8, P, P, P, COUNT, None) == 1
     assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 8, P, 1, P, 1, 8, P, 7, None) == 1
+    # segmented gather: K = 8 and max_p <= 31 only, W = 1 with a histogram
+    assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 6, P, 1, P, 1, 8, P, SEG, None) == 3
+    assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 8, P, 1, P, 1, 40, P, SEG, None) == 3
+    assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 2, 8, P, P, P, SEG, None) == 3
 
 
 def test_public_api_algorithms_and_wide_stats_pass():

@@ -50,7 +50,7 @@ sh = _lib.stream_handle()
 def run(w):
     """fused / hist / scoreW (library's algorithm) and fused_gather / scoreW_gather (forced gather)."""
     algo = 0
-    for suf, code in (("_gather", 1), ("_count", 2), ("_token", 3)):
+    for suf, code in (("_gather", 1), ("_count", 2), ("_token", 3), ("_seg", 4)):
         if w.endswith(suf):
             algo, w = code, w[:-len(suf)]
     if w == "fused":
@@ -95,7 +95,7 @@ res = {}
 bytes_ = a.tokens * L * K
 for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup")):
     base = w
-    for suf in ("_gather", "_count", "_token"):
+    for suf in ("_gather", "_count", "_token", "_seg"):
         base = base[:-len(suf)] if base.endswith(suf) else base
     fn = run if base in ("hist", "score1", "score2", "score4", "fused") else run_ext
     for _ in range(3):
