@@ -20,8 +20,13 @@
 namespace mp {
 
 constexpr int kSegWarps = kThreads / 32;  // 16
+// windows in flight per warp for W = 1 (R1 10M tokens, 4 placements, 1500 / 15k / 150k chunks):
+// 2: 1.035 / 1.112 / 1.895 ms, 4: 0.985 / 1.052 / 1.841 ms, 8: 1.014 / 1.087 / 1.853 ms (spills)
+#ifndef MP_SEG_U1
+#define MP_SEG_U1 4
+#endif
 template <int W>
-__host__ __device__ constexpr int seg_unroll() { return W == 4 ? 2 : 4; }  // windows (64 tokens) in flight per warp
+__host__ __device__ constexpr int seg_unroll() { return W == 4 ? 2 : W == 2 ? 4 : MP_SEG_U1; }  // windows (64 tokens) in flight per warp
 
 template <int W>
 __device__ __forceinline__ void seg_lookup(uint32_t a, uint32_t (&t)[W]) {
