@@ -140,7 +140,7 @@ def test_gather_and_count_contract_agree(c, W, hi, S):
 def big_case(draw):
     L = draw(st.integers(1, 8))
     E = draw(st.sampled_from([16, 64, 256]))
-    K = draw(st.integers(1, 8))
+    K = draw(st.sampled_from([1, 2, 3, 5, 6, 7, 8, 8, 8]))
     N = draw(st.integers(5_000, 300_000))
     C = draw(st.integers(1, 5_000))
     return L, E, K, N, C, draw(st.integers(0, 2 ** 31)), draw(st.sampled_from([0.0, 1.2, 2.0]))
@@ -161,6 +161,11 @@ def test_pipelined_flush_multi_cta_stress(c, W):
     pls = [mpl.Placement(rng.integers(0, 23, (L, E)).astype(np.int32)) for _ in range(4 * W)]
     want = ev.score_sums(tr, pls, cost, algo="gather")
     assert np.array_equal(ev.score_sums(tr, pls, cost, algo="count"), want)
+    if K == 8:  # segmented gather: warp ranges and chunk boundaries at every position
+        assert np.array_equal(ev.score_sums(tr, pls, cost, algo="seg"), want)
+        if W == 1:
+            f2, r2 = ev.evaluate_with_stats(tr, pls, cost, algo="seg")
+            assert [r.chunk_hop_sums for r in r2] == want.tolist()
     f, reps = ev.evaluate_with_stats(tr, pls[:4 * W], cost, algo="count")
     sel = tr.tokens()
     hist = np.stack([np.bincount(sel[:, l, :].ravel(), minlength=E) for l in range(L)])
