@@ -55,6 +55,9 @@ __device__ __forceinline__ void dedup_record8(uint2 v, uint32_t base, uint32_t s
 }
 
 constexpr int kDedupThreads = 512;
+#ifndef MP_DEDUP_U
+#define MP_DEDUP_U 2  // 32-pair windows in flight per warp (K = 8 warp-range path)
+#endif
 
 // Fast K = 8 record for pe bytes <= 31 and server ids < 128 (checked per layer by the CTA).  Row
 // layout of the fast path: slot lane*8 holds {pe word, server word} (one LDS.64 per pick), and bit 7
@@ -143,6 +146,118 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
       }
     }
     __syncthreads();
+    if (K == 8) {
+      // Warp ranges (as in the segmented gather, csrc/seg.cu): the segment's token pairs are split
+      // into 16 contiguous warp ranges; a warp streams 32-pair windows (4 in flight), computes each
+      // record's contribution separately, keeps running sums of its current chunk and reduces them
+      // at every chunk boundary it crosses -- so short chunks cost one warp reduction per boundary
+      // instead of a pass of the whole CTA over every (layer, chunk) piece.
+      const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+      const int64_t m0 = r0 >> 1, m1 = (r1 + 1) >> 1;
+      const int64_t perw = (m1 - m0 + nwarps - 1) / nwarps;
+      const int64_t wm0 = min(m1, m0 + perw * warp), wm1 = min(m1, wm0 + perw);
+      if (wm0 < wm1) {
+        const int64_t wt0 = max(r0, 2 * wm0), wt1 = min(r1, 2 * wm1);
+        int c = 0;
+        {
+          int lo = 0, hi = C;
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(bounds + mid) <= wt0) lo = mid; else hi = mid;
+          }
+          c = lo;
+        }
+        const int64_t T0 = 2 * wm0;
+        const int npairs = (int)(wm1 - wm0);
+        const int ra = (int)(wt0 - T0), rb = (int)(wt1 - T0);
+        auto rel = [&](int64_t x) { return (int)min(x - T0, (int64_t)0x7fffffff); };
+        int nbr = rel(__ldg(bounds + c + 1));
+        uint32_t h16[2] = {0, 0}, d16[2] = {0, 0}, u8 = 0;          // running, narrow lanes
+        uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};  // running, u32
+        int since = 0, recs = 0;
+        auto widen = [&]() {
+          hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
+          dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
+          h16[0] = h16[1] = d16[0] = d16[1] = u8 = 0;
+        };
+        auto flush = [&](int cc) {  // warp-uniform: running sums of chunk cc -> the three outputs
+          widen();
+          uint32_t v[16] = {hop[0], hop[1], hop[2], hop[3], uq[0], uq[1], uq[2], uq[3],
+                            dd[0], dd[1], dd[2], dd[3], 0u, 0u, 0u, 0u};
+          int q = 0;
+          const uint32_t tot = warp_reduce_scatter<16>(v, lane, &q);
+          if ((lane & 1) == 0 && tot && q < 12) {
+            int64_t* dst = q < 4 ? hop_sums : q < 8 ? uniq_sums : dedup_sums;
+            atomic_add_i64(dst + (int64_t)(q & 3) * C + cc, (int64_t)tot);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) hop[i] = uq[i] = dd[i] = 0;
+          recs = 0;
+        };
+        auto rec = [&](uint2 w, uint32_t (&h_)[2], uint32_t& u_, uint32_t (&d_)[2]) {
+          if (fast) dedup_record8_fast(w, base, slot8, h_, u_, d_);
+          else dedup_record8(w, base, slot, src, h_, u_, d_);
+        };
+        auto add_rec = [&](const uint32_t (&h_)[2], uint32_t u_, const uint32_t (&d_)[2]) {
+          h16[0] += h_[0]; h16[1] += h_[1]; d16[0] += d_[0]; d16[1] += d_[1]; u8 += u_;
+        };
+        const uint4* __restrict__ pv = reinterpret_cast<const uint4*>(plane) + wm0;
+        for (int rw = 0; rw < npairs; rw += 32 * MP_DEDUP_U) {
+          uint4 x[MP_DEDUP_U];
+#pragma unroll
+          for (int u = 0; u < MP_DEDUP_U; ++u) {
+            const int r = rw + u * 32 + lane;
+            if (r < npairs) {
+              const int4 vv = ldg_stream(pv + r);
+              x[u] = make_uint4((uint32_t)vv.x, (uint32_t)vv.y, (uint32_t)vv.z, (uint32_t)vv.w);
+            } else {
+              x[u] = make_uint4(0, 0, 0, 0);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < MP_DEDUP_U; ++u) {
+            const int rfirst = rw + u * 32;
+            if (rfirst >= npairs) break;  // warp-uniform
+            const int r = rfirst + lane;
+            const int tA = 2 * r, tB = tA + 1;
+            const bool vA = r < npairs && tA >= ra && tA < rb;
+            const bool vB = r < npairs && tB >= ra && tB < rb;
+            uint32_t hA[2] = {0, 0}, dA[2] = {0, 0}, uA = 0, hB[2] = {0, 0}, dB[2] = {0, 0}, uB = 0;
+            rec(make_uint2(x[u].x, x[u].y), hA, uA, dA);
+            rec(make_uint2(x[u].z, x[u].w), hB, uB, dB);
+            const int wlast = min(2 * (rfirst + 31) + 1, rb - 1);
+            if (nbr > wlast) {
+              if (vA) add_rec(hA, uA, dA);
+              if (vB) add_rec(hB, uB, dB);
+            } else {
+              bool doneA = !vA, doneB = !vB;
+              while (nbr <= wlast) {  // boundary inside the window: records < nb belong to chunk c
+                if (!doneA && tA < nbr) { add_rec(hA, uA, dA); doneA = true; }
+                if (!doneB && tB < nbr) { add_rec(hB, uB, dB); doneB = true; }
+                flush(c);
+                since = 0;
+                ++c;  // c < C - 1 here: bounds[C] >= the trace end > the window
+                nbr = rel(__ldg(bounds + c + 1));
+              }
+              if (!doneA) add_rec(hA, uA, dA);
+              if (!doneB) add_rec(hB, uB, dB);
+            }
+            // narrow lanes: u16 hop/dedup sums take 8 records (8 x 8 x 255 < 2^16), u8 unique counts 31
+            if (++since == 4) {
+              widen();
+              since = 0;
+              // u32 running sums: a warp's total over 32 lanes x 2^15 records x 2040 stays below 2^32
+              if ((recs += 8) >= (1 << 15)) flush(c);
+            }
+          }
+        }
+        flush(c);
+      }
+      g += r1 - r0;
+      continue;
+    }
     int c = 0;
     {
       int lo = 0, hi = C;
@@ -154,61 +269,10 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
     }
     int64_t cend = __ldg(bounds + c + 1);
     for (int64_t t = r0; t < r1;) {
-      // chunk piece [t, te): walk forward from the previous chunk, skipping empty ones
+      // chunk piece [t, te): walk forward from the previous chunk, skipping empty ones (K != 8)
       while (cend <= t && c + 1 < C) cend = __ldg(bounds + (++c) + 1);
       const int64_t te = min(r1, cend);
       uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};
-      if (K == 8) {
-        // SIMD-within-a-register path over 16-byte vectors (two records each), 4 vectors in flight
-        // per thread; lane sums are widened every main-loop iteration (8 records, u16 lanes:
-        // 8*8*255 < 2^16) and after every single-record step
-        uint32_t h16[2] = {0, 0}, d16[2] = {0, 0}, u8 = 0;
-        auto widen = [&]() {
-          hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
-          dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
-          h16[0] = h16[1] = d16[0] = d16[1] = u8 = 0;
-        };
-        auto rec8 = [&](uint2 w, uint32_t b_, uint32_t s_, uint32_t src_, uint32_t (&h_)[2], uint32_t& u_,
-                        uint32_t (&d_)[2]) {
-          if (fast) dedup_record8_fast(w, b_, slot8, h_, u_, d_);
-          else dedup_record8(w, b_, s_, src_, h_, u_, d_);
-        };
-        const int64_t va = (t + 1) >> 1, vb = te >> 1;  // full vectors cover records [2va, 2vb)
-        const int T = blockDim.x;
-        if ((t & 1) && threadIdx.x == 0) {  // lone head record
-          rec8(__ldg(reinterpret_cast<const uint2*>(plane + t * 8)), base, slot, src, h16, u8, d16);
-          widen();
-        }
-        if ((te & 1) && te - 1 > t && threadIdx.x == T - 1) {  // lone tail record
-          rec8(__ldg(reinterpret_cast<const uint2*>(plane + (te - 1) * 8)), base, slot, src, h16, u8, d16);
-          widen();
-        }
-        const uint4* __restrict__ pv = reinterpret_cast<const uint4*>(plane);
-        int64_t v = va + threadIdx.x;
-        for (; v + 3 * T < vb; v += 4 * T) {
-          uint4 x[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int4 r = ldg_stream(pv + v + u * T);
-            x[u] = make_uint4((uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            rec8(make_uint2(x[u].x, x[u].y), base, slot, src, h16, u8, d16);
-            rec8(make_uint2(x[u].z, x[u].w), base, slot, src, h16, u8, d16);
-          }
-          widen();
-        }
-        for (; v < vb; v += T) {
-          const int4 r = ldg_stream(pv + v);
-          const uint4 x = make_uint4((uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w);
-          rec8(make_uint2(x.x, x.y), base, slot, src, h16, u8, d16);
-          rec8(make_uint2(x.z, x.w), base, slot, src, h16, u8, d16);
-          widen();
-        }
-      } else
       for (int64_t r = t + threadIdx.x; r < te; r += blockDim.x) {
         uint32_t ids[kDedupMaxK];
         for (int k = 0; k < K; ++k) ids[k] = plane[r * K + k];

@@ -177,3 +177,32 @@ def test_pipelined_flush_multi_cta_stress(c, W):
     for c_ in sorted({0, tr.n_chunks // 2, tr.n_chunks - 1}):
         part = sel[b[c_]:b[c_ + 1]]
         assert np.array_equal(cc[c_], np.stack([np.bincount(part[:, l, :].ravel(), minlength=E) for l in range(L)]))
+
+
+@settings(max_examples=int(__import__("os").environ.get("MP_STRESS_EXAMPLES", "6")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(1, 6), st.sampled_from([16, 64, 256]), st.integers(2_000, 60_000), st.integers(1, 3_000),
+       st.integers(0, 2 ** 31), st.sampled_from([("FatTree", (4, 2, 4)), ("Dragonfly", (4, 2, 4)),
+                                                 ("DragonflySparse", (64, 1, 1))]))
+def test_dedup_warp_ranges_stress(L, E, N, C, seed, topo_case):
+    """Unique-destination scoring (K = 8 warp-range path) over many CTAs, warp ranges and chunk
+    boundaries at every position, fast (pe <= 31, ids < 128) and general layers: bit-exact vs the
+    oracle."""
+    from helpers import oracle_cost, setup_topology
+    from oracle import evaluate as oe
+    from oracle import gen as og
+    kind, size = topo_case
+    m = mt.ModelSpec(L, E, 8)
+    g, dist, order, attn, cost = setup_topology(kind, *size, m)
+    _, p = oracle_cost(g, attn)
+    tr = mt.generate_trace(m, 1.2, N, C, seed)
+    sel, bounds = og.generate(L, E, 8, 1.2, N, C, seed)
+    rng = np.random.default_rng(seed % 977)
+    pls = [mpl.Placement(random_assign(rng, L, E, g.n_devices)) for _ in range(4)]
+    reps = ev.evaluate_dedup(tr, pls, cost)
+    src = g.device_server[attn.dispatch]
+    for pl, rep in zip(pls, reps):
+        h, u, d = oe.dedup_sums(sel, oe.pe_table(p, pl.assign), g.device_server[pl.assign], src, bounds)
+        assert rep.spec.chunk_hop_sums == h.tolist()
+        assert rep.chunk_uniq_sums == u.tolist()
+        assert rep.chunk_dedup_sums == d.tolist()
