@@ -182,7 +182,7 @@ int mp_hist_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok
   if (r) return r;
   if (E <= 0 || !counts || !err || !chunk_bounds || C <= 0 || !tables || !hop_sums || max_p < 0) return MP_ERR_ARG;
   if (!(W == 1 || W == 2 || W == 4) || algo < MP_ALGO_AUTO || algo > MP_ALGO_SEG) return MP_ERR_ARG;
-  if (max_p > 255 || ((algo == MP_ALGO_GATHER || algo == MP_ALGO_SEG) && W != 1)) return MP_ERR_UNSUPPORTED;
+  if (max_p > 255 || (algo == MP_ALGO_GATHER && W != 1)) return MP_ERR_UNSUPPORTED;
   if (algo == MP_ALGO_SEG && (K != 8 || max_p > 31)) return MP_ERR_UNSUPPORTED;
   if (algo == MP_ALGO_TOKEN && (int64_t)L * K * max_p > 65535) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;

@@ -485,8 +485,8 @@ def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement],
         raise MoeplaceError("evaluate: empty trace")
     if algo not in ALGOS:
         raise ConfigError(f"unknown score algorithm {algo!r}")
-    if not 1 <= len(placements) <= (4 if algo in ("gather", "seg") else MAX_LANES):
-        raise ConfigError(f"evaluate_with_stats takes 1..{4 if algo in ('gather', 'seg') else MAX_LANES} placements")
+    if not 1 <= len(placements) <= (4 if algo == "gather" else MAX_LANES):
+        raise ConfigError(f"evaluate_with_stats takes 1..{4 if algo == 'gather' else MAX_LANES} placements")
     dev = _lib.require_cuda()
     W = _lanes_for(len(placements))
     tables, max_p = _group_tables(placements, _as_costs(cost, len(placements)), m, W)

@@ -56,7 +56,7 @@ def _check(tr, sel, bounds, t0, pls, p, W, hist_ws=(1,)):
     for algo in algos:
         s, _, _ = _run(tr, tables, W, max_p, algo, hist=False)
         assert np.array_equal(s, want), ("score", W, algo)
-        if W in hist_ws or algo not in (GATHER, SEG):
+        if W in hist_ws or algo != GATHER:
             s, c, e = _run(tr, tables, W, max_p, algo, hist=True)
             assert np.array_equal(s, want), ("hist_score", W, algo)
             assert np.array_equal(c, ost.counts(sel, m.E)), ("counts", W, algo)
@@ -156,7 +156,7 @@ def test_argument_rules_of_the_explicit_entry_points():
     # segmented gather: K = 8 and max_p <= 31 only, W = 1 with a histogram
     assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 6, P, 1, P, 1, 8, P, SEG, None) == 3
     assert L.mp_score_ex_u8(P, 64, 0, 8, 1, 8, P, 1, P, 1, 40, P, SEG, None) == 3
-    assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 8, 256, P, 1, P, 2, 8, P, P, P, SEG, None) == 3
+    assert L.mp_hist_score_ex_u8(P, 64, 0, 8, 1, 6, 256, P, 1, P, 2, 8, P, P, P, SEG, None) == 3
 
 
 def test_public_api_algorithms_and_wide_stats_pass():

@@ -130,7 +130,7 @@ def test_gather_and_count_contract_agree(c, W, hi, S):
     for algo in ("gather", "count", "token") + seg:
         assert np.array_equal(ev.score_sums(tr, pls, cost, algo=algo), want), algo
     n = 4 if W == 1 else 4 * W
-    for algo in ("count", "token") + (seg if W == 1 else ()):
+    for algo in ("count", "token") + seg:
         f, reps = ev.evaluate_with_stats(tr, pls[:n], cost, algo=algo)
         assert np.array_equal(f.counts, ost.counts(sel, E))
         assert [r.chunk_hop_sums for r in reps] == want[:n].tolist()

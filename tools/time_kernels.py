@@ -53,9 +53,10 @@ def run(w):
     for suf, code in (("_gather", 1), ("_count", 2), ("_token", 3), ("_seg", 4)):
         if w.endswith(suf):
             algo, w = code, w[:-len(suf)]
-    if w == "fused":
-        t, mp_ = tabs[1]
-        _lib.call("mp_hist_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t), 1, mp_,
+    if w.startswith("fused"):  # fused = histogram + 4 placements; fused2 / fused4 = + 8 / 16 placements
+        Wf = int(w[5:] or 1)
+        t, mp_ = tabs[Wf]
+        _lib.call("mp_hist_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(t), Wf, mp_,
                   _lib.ptr(cnt), _lib.ptr(s), _lib.ptr(err), algo, sh)
     elif w == "hist":
         _lib.call("mp_hist_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(cnt), _lib.ptr(err), sh)
@@ -97,7 +98,7 @@ for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4"
     base = w
     for suf in ("_gather", "_count", "_token", "_seg"):
         base = base[:-len(suf)] if base.endswith(suf) else base
-    fn = run if base in ("hist", "score1", "score2", "score4", "fused") else run_ext
+    fn = run if base in ("hist", "score1", "score2", "score4", "fused", "fused2", "fused4") else run_ext
     for _ in range(3):
         fn(w)
     ts = []
