@@ -109,7 +109,8 @@ class ClockSampler:
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"], "samples": 0}
         return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "sm_min_mhz": float(min(self.sm)), "source": "nvml"}
+                "samples": len(self.sm), "sm_min_mhz": float(min(self.sm)), "source": "nvml",
+                "window": "warm-up + timed steps (+ identical untimed steps until >= 8 samples)"}
 
 
 def cpu_sample(trace, n_sample: int):
@@ -481,14 +482,15 @@ def main():
 
     launches_per_step = 1 if (fused or fact) else len(groups) + (1 if with_hist else 0)
     run = fstep if fact else step
+    # the clock poller starts before the warm-up so it is already sampling when timing begins
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
     for _ in range(args.warmup):
         run(False)
     torch.cuda.synchronize()
     if with_hist and not torch.equal(counts.view(L, E), counts0):
         raise SystemExit("bench: histogram of the timed pass differs from the setup histogram")
-    sampler = ClockSampler(local) if rank == 0 else None
-    if sampler:
-        sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -507,6 +509,16 @@ def main():
             kernel_ms[1].append(ke[1][0].elapsed_time(ke[1][1]))
     if world > 1:
         dist.barrier()
+    if sampler and world == 1:
+        # a short timed region can end before the poller has a handful of samples: keep the GPU on
+        # the identical (untimed) step until it has >= 8, so the reported clocks are under this load
+        extra = 0
+        while len(sampler.sm) < 8 and extra < 2000:
+            run(False)
+            extra += 1
+            if extra % 50 == 0:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
     _lib.check_err(err, "bench: device data error in the timed steps")
     t_step = torch.tensor([ev_a.elapsed_time(ev_b) / args.steps], dtype=torch.float64, device=dev)
