@@ -13,8 +13,9 @@
 // spread every (layer, chunk) piece over the whole CTA, so short chunks leave most threads idle;
 // here a boundary costs one warp reduction wherever it falls.
 // Per-token sums of 8 lookups fit u8 lanes (8 * 31 < 256); running sums are u16 lanes widened
-// into u32 every 64 windows and at each flush.  With HIST (W = 1) every byte also increments the
-// lane-replicated histogram, flushed per segment (the fused statistics + scoring pass).
+// into u32 every 64 windows and at each flush.  With HIST every byte also increments the
+// lane-replicated histogram (W = 1: in the table rows' free half, one PRMT per address; W = 2 / 4:
+// a separate region of 128-byte rows, PRMT byte extract + IMAD), flushed per segment.
 #include "common.cuh"
 
 namespace mp {
@@ -48,14 +49,24 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
            int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
   constexpr int K = 8;
   constexpr int P = 4 * W;
-  extern __shared__ __align__(128) uint8_t sm[];  // 256 rows x 256 B + a 128-byte trash row
+  // 256 rows x 256 B of tables (W = 1: bytes 128-255 of each row hold the histogram replicas);
+  // W > 1 with HIST: + a 256 rows x 128 B histogram region; then a 128-byte trash row
+  extern __shared__ __align__(128) uint8_t sm[];
+  constexpr bool kHistRegion = HIST && W > 1;
+  constexpr int kHistWords = 256 * 256 / 4;  // word offset of the separate histogram region
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t base = smem_addr(sm);
   const uint32_t hbase = base + 128;
   const uint32_t slot = W == 4 ? (uint32_t)((lane & 7) << 4) : W == 2 ? (uint32_t)(lane << 3) : (uint32_t)(lane << 2);
   const uint32_t hslot = (uint32_t)(lane << 2);
-  const uint32_t trash = base + 256 * 256 + hslot;  // increments of masked-out tokens land here (no branch)
+  const uint32_t hreg = base + 256 * 256 + hslot;  // W > 1: bin e of this lane at hreg + e * 128
+  const uint32_t trash = base + 256 * 256 + (kHistRegion ? 256 * 128 : 0) + hslot;  // masked-out tokens (no branch)
+  // histogram address of byte b of `word` (lane replica)
+  auto haddr = [&](uint32_t word, int b) -> uint32_t {
+    if constexpr (kHistRegion) return prmt(word, 0u, 0x4440u | (uint32_t)b) * 128u + hreg;
+    else return hbase + prmt(word, hslot, sel_row(b));
+  };
 
   uint32_t acc16[2 * W], acc32[P];
 #pragma unroll
@@ -105,7 +116,9 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
         const int e = i / WPR, j = i % WPR;
         smw[e * 64 + j] = __ldg(tl + e * W + (j % W));
       }
-      if constexpr (HIST)
+      if constexpr (kHistRegion)
+        for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) smw[kHistWords + i] = 0;
+      else if constexpr (HIST)
         for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) smw[(i >> 5) * 64 + 32 + (i & 31)] = 0;
     }
     __syncthreads();
@@ -164,7 +177,7 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
             seg_lookup<W>(base + off, t);
 #pragma unroll
             for (int w = 0; w < W; ++w) sA[w] += t[w];
-            if constexpr (HIST) atoms_inc(vA ? hbase + prmt(word, hslot, sel_row(k & 3)) : trash);
+            if constexpr (HIST) atoms_inc(vA ? haddr(word, k & 3) : trash);
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -174,7 +187,7 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
             seg_lookup<W>(base + off, t);
 #pragma unroll
             for (int w = 0; w < W; ++w) sB[w] += t[w];
-            if constexpr (HIST) atoms_inc(vB ? hbase + prmt(word, hslot, sel_row(k & 3)) : trash);
+            if constexpr (HIST) atoms_inc(vB ? haddr(word, k & 3) : trash);
           }
           // last valid token of this window (warp-uniform)
           const int wlast = min(2 * (rfirst + 31) + 1, rb - 1);
@@ -206,7 +219,7 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
     if constexpr (HIST) {
       __syncthreads();
       for (int e = threadIdx.x; e < 256; e += blockDim.x) {
-        const uint32_t* row = smw + e * 64 + 32;
+        const uint32_t* row = kHistRegion ? smw + kHistWords + e * 32 : smw + e * 64 + 32;
         uint32_t sum = 0;
 #pragma unroll 8
         for (int r = 0; r < 32; ++r) sum += row[(r + e) & 31];
@@ -225,7 +238,7 @@ static cudaError_t launch_seg_t(const uint8_t* planes, int64_t stride, int64_t t
                                 const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                                 int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   auto kern = seg_kernel<W, HIST>;
-  const int smem = 256 * 256 + 128;
+  const int smem = 256 * 256 + ((HIST && W > 1) ? 256 * 128 : 0) + 128;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -240,13 +253,15 @@ static cudaError_t launch_seg_t(const uint8_t* planes, int64_t stride, int64_t t
   return cudaGetLastError();
 }
 
-// K = 8 and max_p <= 31 only (the caller checks); hist requires W = 1.
+// K = 8 and max_p <= 31 only (the caller checks).
 cudaError_t launch_seg(bool hist, int W, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int E,
                        const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts, int64_t* hop_sums,
                        int64_t* err, cudaStream_t s) {
   if (hist) {
-    if (W != 1) return cudaErrorInvalidValue;
-    return launch_seg_t<1, true>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
+    if (W == 1) return launch_seg_t<1, true>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
+    if (W == 2) return launch_seg_t<2, true>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
+    if (W == 4) return launch_seg_t<4, true>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
+    return cudaErrorInvalidValue;
   }
   if (W == 1) return launch_seg_t<1, false>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
   if (W == 2) return launch_seg_t<2, false>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);

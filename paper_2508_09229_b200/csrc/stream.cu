@@ -734,9 +734,9 @@ int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K,
   if (K == 8 && max_p <= 31) {
     // SEG below seg_hi tokens per chunk, TOKEN below tok_lo (R1, 10M tokens: hist+W=1 count 1.22 /
     // seg 1.40 / token 2.14 ms at C = 1500, seg 1.41 vs count 1.98 at C = 3000; W = 4 seg 3.8 vs
-    // token 5.2 ms even at 67 tokens per chunk).  With a histogram and W > 1, SEG means the plain
-    // histogram pass + the segmented scorer (0.83 ms + the score pass).
-    const int seg_hi = hist ? (W == 1 ? 5000 : W == 2 ? 3000 : 1600) : W == 1 ? 6000 : W == 2 ? 5000 : 2500;
+    // token 5.2 ms even at 67 tokens per chunk; histogram + 8 placements seg 1.85 vs count 2.02 ms
+    // at C = 3000, + 16 placements seg 2.88 vs count 2.60 at C = 5000 and 2.96 vs 6.45 at 15000).
+    const int seg_hi = hist ? (W == 1 ? 5000 : W == 2 ? 4000 : 1600) : W == 1 ? 6000 : W == 2 ? 5000 : 2500;
     const int tok_lo = hist ? (W == 1 ? 70 : 0) : W == 1 ? 170 : 0;
     if (tok_ok && tokens < (int64_t)tok_lo * C) return MP_ALGO_TOKEN;
     if (tokens < (int64_t)seg_hi * C) return MP_ALGO_SEG;
@@ -760,15 +760,8 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
   const int widen = max_p <= 15 ? 16 : max_p <= 63 ? 4 : 1;
   if (W == 0) return launch_t<true, 0, 16>(MP_ARGS);
   const int chosen = choose_algo(hist, W, algo, t1 - t0, C, L, K, max_p);
-  if (chosen == MP_ALGO_SEG) {
-    if (hist && W > 1) {  // the segmented scorer fuses the histogram for W = 1 only
-      const cudaError_t e = launch_t<true, 0, 16>(planes, stride, t0, t1, L, K, E, nullptr, 1, nullptr, counts, nullptr,
-                                                   err, s);
-      if (e != cudaSuccess) return e;
-      return launch_seg(false, W, planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
-    }
+  if (chosen == MP_ALGO_SEG)
     return launch_seg(hist, W, planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
-  }
   if (chosen == MP_ALGO_TOKEN) {
     if (hist) {  // histogram pass (per-layer flushes only) + the token-tiled scorer
       const cudaError_t e = launch_t<true, 0, 16>(planes, stride, t0, t1, L, K, E, nullptr, 1, nullptr, counts, nullptr,
