@@ -167,8 +167,8 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
  *     down sharply for short chunks.  Requires L*K*max_p <= 65535 (else MP_ERR_UNSUPPORTED);
  *     with a histogram it is mp_hist_u8 + the token pass;
  *   MP_ALGO_AUTO:   the faster one for the shape, by average tokens per chunk (measured
- *     crossovers): when SEG applies (K = 8, max_p <= 31) SEG below 5000 / 4000 / 1600 (with a
- *     histogram, W = 1 / 2 / 4) and 6000 / 5000 / 2500 (score-only) tokens per chunk, TOKEN
+ *     crossovers): when SEG applies (K = 8, max_p <= 31) SEG below 5000 / 3000 / 1800 (with a
+ *     histogram, W = 1 / 2 / 4) and 4000 / 6000 / 2500 (score-only) tokens per chunk, TOKEN
  *     below 70 (histogram, W = 1) / 170 (score-only W = 1); otherwise TOKEN below MP_TOKEN_CHUNK_TOKENS (W = 1 with
  *     a histogram; half of it for W = 2, 700 for W = 4; score-only 4096 / 1600 / 800) when the
  *     limit above holds; else GATHER for score-only W = 1 and COUNT otherwise.  This is what

@@ -427,6 +427,9 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
 #ifndef MP_PIPE_FLUSH
 #define MP_PIPE_FLUSH 1
 #endif
+#ifndef MP_PIPE_GTAIL4
+#define MP_PIPE_GTAIL4 1  // guarded 4-vector tail batches (C = 3000: hist_chunks 1.905 -> 1.472, W = 4 pass 2.10 -> 1.80 ms)
+#endif
 constexpr int kPipeSets = 3;
 constexpr int kPipeSetBytes = 256 * 128;
 constexpr int kPipeSmem = kPipeSets * kPipeSetBytes;
@@ -469,6 +472,17 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) vec(x[u]);
   }
+#if MP_PIPE_GTAIL4
+  // tail: guarded batches of 4 (a short piece's rest in one or two load round trips)
+  for (; v < nv; v += 4 * T) {
+    int4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = v + u * T < nv ? ldg_stream(pv + v + u * T) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + u * T < nv) vec(x[u]);
+  }
+#else
   for (; v + 3 * T < nv; v += 4 * T) {
     int4 x[4];
 #pragma unroll
@@ -477,6 +491,7 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
     for (int u = 0; u < 4; ++u) vec(x[u]);
   }
   for (; v < nv; v += T) vec(ldg_stream(pv + v));
+#endif
 }
 
 // WC == 0: per-chunk histogram, counts is int64 [C][L][E].  WC > 0: count-contract with WC-word
@@ -734,9 +749,9 @@ int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K,
   if (K == 8 && max_p <= 31) {
     // SEG below seg_hi tokens per chunk, TOKEN below tok_lo (R1, 10M tokens: hist+W=1 count 1.22 /
     // seg 1.40 / token 2.14 ms at C = 1500, seg 1.41 vs count 1.98 at C = 3000; W = 4 seg 3.8 vs
-    // token 5.2 ms even at 67 tokens per chunk; histogram + 8 placements seg 1.85 vs count 2.02 ms
-    // at C = 3000, + 16 placements seg 2.88 vs count 2.60 at C = 5000 and 2.96 vs 6.45 at 15000).
-    const int seg_hi = hist ? (W == 1 ? 5000 : W == 2 ? 4000 : 1600) : W == 1 ? 6000 : W == 2 ? 5000 : 2500;
+    // token 5.2 ms even at 67 tokens per chunk; re-measured with the guarded count-contract tail:
+    // profiles/r1_chunk_granularity.txt).
+    const int seg_hi = hist ? (W == 1 ? 5000 : W == 2 ? 3000 : 1800) : W == 1 ? 4000 : W == 2 ? 6000 : 2500;
     const int tok_lo = hist ? (W == 1 ? 70 : 0) : W == 1 ? 170 : 0;
     if (tok_ok && tokens < (int64_t)tok_lo * C) return MP_ALGO_TOKEN;
     if (tokens < (int64_t)seg_hi * C) return MP_ALGO_SEG;
