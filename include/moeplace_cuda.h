@@ -250,6 +250,14 @@ int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev
 int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t src_stride, int64_t width, int rows,
                        void* stream);
 
+/* ---- token-major ingestion (an ActivationTrace is per token) --------------------
+ * planes[l][(tok_out + i)*K + k] = tokens[(i*L + l)*K + k] for i < n: the device transpose of a
+ * token-major uint8 [n][L][K] slice (router output, or a host array streamed slice by slice) into
+ * the layer planes.  `tokens` is a device pointer; K = 8 with an 8-byte aligned `tokens` takes the
+ * tiled u64 transpose.                                                                            */
+int mp_tokens_to_planes_u8(const uint8_t* tokens, int64_t n, int L, int K, uint8_t* planes, int64_t plane_stride,
+                           int64_t tok_out, void* stream);
+
 /* ---- solve_exact: min-cost flow on the class-compressed FlowNetwork ------
  * HOST function (the ILP solve stays on the host).  Costs w_int[l][e][s] are int64 >= 0 in
  * host memory.  When p (host uint8[L][S]) is given, w_int must depend on s only through

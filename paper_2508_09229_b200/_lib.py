@@ -49,6 +49,7 @@ SIGNATURES = {
     "mp_coeffs": (_i32, [_p, _i64, _p, _i32, _i32, _i32, _dbl, _p, _p, _p]),
     "mp_comm_map": (_i32, [_p, _p, _p, _p, _i32, _p, _p, _i32, _i32, _i32, _p, _p, _p]),
     "mp_copy_planes_h2d": (_i32, [_p, _i64, _p, _i64, _i64, _i32, _p]),
+    "mp_tokens_to_planes_u8": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _i64, _p]),
     "mp_solve_mcf": (_i32, [_p, _p, _i32, _i32, _i32, _i32, _i32, _p, _p, _p]),
 }
 

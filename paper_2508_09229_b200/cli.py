@@ -72,16 +72,21 @@ class ExperimentConfig:
             cfg.topology_spec(kind)
         return cfg
 
-    @classmethod
-    def load(cls, path) -> "ExperimentConfig":
+    @staticmethod
+    def read_json(path) -> dict:
+        """The raw config document: a JSON object, else ConfigError (CLI exit 2)."""
         try:
             with open(path) as f:
                 d = json.load(f)
-        except json.JSONDecodeError as e:
+        except (json.JSONDecodeError, UnicodeDecodeError) as e:
             raise ConfigError(f"{path}: invalid JSON ({e})") from None
         if not isinstance(d, dict):
             raise ConfigError(f"{path}: the config must be a JSON object")
-        return cls.from_dict(d)
+        return d
+
+    @classmethod
+    def load(cls, path) -> "ExperimentConfig":
+        return cls.from_dict(cls.read_json(path))
 
     def model_spec(self) -> ModelSpec:
         return ModelSpec(int(self.values["L"]), int(self.values["E"]), int(self.values["K"]))
@@ -235,8 +240,7 @@ def ablate_clayer(cfg: ExperimentConfig, values) -> list:
 def _cfg_from_args(a) -> ExperimentConfig:
     d = {}
     if getattr(a, "config", None):
-        with open(a.config) as f:
-            d = json.load(f)
+        d = ExperimentConfig.read_json(a.config)  # invalid JSON / non-object -> ConfigError (exit 2)
     for k in DEFAULTS:
         v = getattr(a, k, None)
         if v is not None and k not in d:  # --config overrides flags

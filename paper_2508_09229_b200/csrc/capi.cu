@@ -43,6 +43,8 @@ cudaError_t launch_count_digits(const int64_t* counts, int C, int64_t LE, int nd
                                 int64_t* err, cudaStream_t s);
 cudaError_t launch_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0,
                                  int64_t* out, cudaStream_t s);
+cudaError_t launch_tokens_to_planes(const uint8_t* tok, int64_t n, int L, int K, uint8_t* planes, int64_t stride,
+                                    int64_t t_out, cudaStream_t s);
 cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
                           const int64_t* cids, int64_t* lens_or_offsets, uint8_t* out, cudaStream_t s);
 }  // namespace mp
@@ -299,6 +301,13 @@ int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t s
   if (width == 0 || rows == 0) return MP_OK;
   return status(cudaMemcpy2DAsync(dst, (size_t)dst_stride, src, (size_t)src_stride, (size_t)width, (size_t)rows,
                                   cudaMemcpyHostToDevice, S(stream)));
+}
+
+int mp_tokens_to_planes_u8(const uint8_t* tokens, int64_t n, int L, int K, uint8_t* planes, int64_t plane_stride,
+                           int64_t tok_out, void* stream) {
+  if (!tokens || !planes || n < 0 || L <= 0 || K <= 0 || tok_out < 0) return MP_ERR_ARG;
+  if (!aligned16(planes) || (plane_stride & 15) != 0 || plane_stride < (tok_out + n) * (int64_t)K) return MP_ERR_ARG;
+  return status(mp::launch_tokens_to_planes(tokens, n, L, K, planes, plane_stride, tok_out, S(stream)));
 }
 
 }  // extern "C"

@@ -18,8 +18,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, MoeplaceError
-from .model_trace import (ActivationTrace, FrequencyTable, ModelSpec, chunk_counts, frequencies_from_counts, sweep,
-                          validate_trace)
+from .model_trace import ActivationTrace, FrequencyTable, ModelSpec, chunk_counts, frequencies_from_counts, sweep
 from .placement import CostMatrix, Placement
 
 MAX_LANES = 16  # placements scored per pass (W = 4 words of four u8 lanes)
@@ -541,6 +540,9 @@ def evaluate_dedup(trace: ActivationTrace, placements: Sequence[Placement], cost
         for c in gcost:
             if c.dist is None or c.attn is None:
                 raise ConfigError("evaluate_dedup needs cost matrices built by cost_matrix(dist, attn)")
+            if c.dist.graph.n_servers > 256:  # server ids are one byte in the dedup tables
+                raise ConfigError(f"evaluate_dedup supports at most 256 servers, topology has "
+                                  f"{c.dist.graph.n_servers}")
         tables, max_p = _group_tables(grp, gcost, m, 1)
         uniq, topo_of = _unique_costs(gcost)
         S = max(c.S for c in uniq)
@@ -586,18 +588,24 @@ def token_hops_all(trace: ActivationTrace, placements: Sequence[Placement], cost
         raise MoeplaceError("token_hops_all: empty trace")
     placements = list(placements)
     costs = _as_costs(costs, len(placements))
-    planes = trace.device_planes()
-    validate_trace(trace)
     n = trace.n_tokens
+    dev = _lib.require_cuda()
     out = np.zeros((len(placements), n), dtype=np.int64)
     for g0 in range(0, len(placements), 4):
         grp = placements[g0:g0 + 4]
         tables, max_p = _group_tables(grp, costs[g0:g0 + 4], m, 1)
-        hops = t.empty((4, n), dtype=t.int32, device=planes.device)
-        scratch = t.empty((m.L, 256, 32), dtype=t.int32, device=planes.device)
-        _lib.call("mp_token_hops_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
-                  _lib.ptr(tables), max_p, _lib.ptr(scratch), _lib.ptr(hops), _lib.stream_handle())
-        out[g0:g0 + len(grp)] = hops[:len(grp)].cpu().numpy().astype(np.int64)
+        scratch = t.empty((m.L, 256, 32), dtype=t.int32, device=dev)
+        done = [0]
+
+        def launch(planes, stride, t0, t1, bounds):  # per-token outputs land at the slice's offset
+            hops = t.empty((4, t1 - t0), dtype=t.int32, device=dev)
+            _lib.call("mp_token_hops_u8", _lib.ptr(planes), stride, t0, t1, m.L, m.K, _lib.ptr(tables), max_p,
+                      _lib.ptr(scratch), _lib.ptr(hops), _lib.stream_handle())
+            o = done[0]
+            out[g0:g0 + len(grp), o:o + t1 - t0] = hops[:len(grp)].cpu().numpy()
+            done[0] = o + t1 - t0
+
+        sweep(trace, launch)
     return out
 
 

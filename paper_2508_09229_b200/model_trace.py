@@ -83,16 +83,23 @@ class FrequencyTable:
 class ActivationTrace:
     """SPEC.md:104-107.  ``planes[:, t*K:(t+1)*K]`` are token t's selections, tokens
     ``[tok_begin, tok_begin + n_tokens)`` belong to this view, chunk c spans tokens
-    ``[chunk_bounds[c], chunk_bounds[c+1])`` and carries label ``chunk_ids[c]``."""
+    ``[chunk_bounds[c], chunk_bounds[c+1])`` and carries label ``chunk_ids[c]``.
+
+    ``layout="tokens"`` holds the SPEC's own token-major form instead: ``planes`` is a host uint8
+    tensor [N, L, K] (pinned for the streamed end-to-end path, ``from_host_tokens``); every pass
+    streams it to the device slice by slice and transposes each slice into layer planes there
+    (``mp_tokens_to_planes_u8``), so no host transpose is ever made."""
 
     model: Optional[ModelSpec]
-    planes: Any                # torch.uint8 [L, stride] (CUDA, or CPU until first device use)
+    planes: Any                # torch.uint8 [L, stride] (CUDA or host), or [N, L, K] host when layout="tokens"
     tok_begin: int
     n_tokens: int
     chunk_ids: np.ndarray      # int64 [C], ascending
     chunk_bounds: np.ndarray   # int64 [C+1], absolute token indices into planes
     source_is_file: bool = False
     _validated: bool = field(default=False, repr=False)
+    layout: str = "planes"
+    _dev: Any = field(default=None, repr=False)  # device planes of this view's tokens (host traces)
 
     @property
     def n_chunks(self) -> int:
@@ -111,18 +118,59 @@ class ActivationTrace:
     def token_chunk_ids(self) -> np.ndarray:
         return np.repeat(self.chunk_ids, self.chunk_token_counts())
 
-    def device_planes(self):
-        """The planes on the CUDA device (uploaded once, host->device, if the trace came from a file)."""
-        t = _lib.torch()
-        dev = _lib.require_cuda()
-        if not self.planes.is_cuda:
-            self.planes = self.planes.to(dev, non_blocking=True)
-        return self.planes
+    @property
+    def on_device(self) -> bool:
+        return self.planes is not None and self.planes.is_cuda and self.layout == "planes"
 
-    def to_host(self, pin: bool = True) -> "ActivationTrace":
-        """A copy whose planes live in (pinned) host memory: evaluating it streams the trace
-        through the device slice by slice (the end-to-end path), without caching it there."""
+    def device_view(self):
+        """(planes, t0, t1): this view's tokens as CUDA layer planes.  A device-resident trace
+        returns its own planes and token range (no copy).  A host-resident one uploads ONLY the
+        view's tokens (transposed on the device when token-major) into planes cached on this view
+        object; the caller's host planes are never replaced, so other views and the streamed
+        passes keep streaming."""
+        if self.on_device:
+            return self.planes, self.tok_begin, self.tok_end
+        if self._dev is None:
+            t = _lib.torch()
+            dev = _lib.require_cuda()
+            m = self.model
+            n, K = self.n_tokens, m.K
+            planes = t.empty((m.L, _plane_stride(n, K)), dtype=t.uint8, device=dev)
+            a = self.tok_begin
+            if self.layout == "tokens":
+                tok = self.planes[a:a + n].to(dev, non_blocking=True).contiguous()
+                _lib.call("mp_tokens_to_planes_u8", _lib.ptr(tok), n, m.L, K, _lib.ptr(planes), planes.shape[1], 0,
+                          _lib.stream_handle())
+            else:
+                _lib.call("mp_copy_planes_h2d", _lib.ptr(planes), planes.shape[1],
+                          C_void(self.planes.data_ptr() + a * K), self.planes.shape[1], n * K, m.L,
+                          _lib.stream_handle())
+            self._dev = planes
+        return self._dev, 0, self.n_tokens
+
+    def device_planes(self):
+        """The planes of this view on the CUDA device (``device_view()[0]``)."""
+        return self.device_view()[0]
+
+    def to_host(self, pin: bool = True, layout: str = "planes") -> "ActivationTrace":
+        """A copy whose data live in (pinned) host memory: evaluating it streams the trace
+        through the device slice by slice (the end-to-end path), without caching it there.
+        ``layout="tokens"`` gives the SPEC's token-major [N, L, K] form (transposed on the device
+        before the download)."""
         t = _lib.torch()
+        if layout not in ("planes", "tokens"):
+            raise ConfigError(f"unknown trace layout {layout!r}")
+        if layout == "tokens":
+            m = self.model
+            planes, t0, t1 = self.device_view()
+            src = planes[:, t0 * m.K:t1 * m.K].view(m.L, self.n_tokens, m.K).permute(1, 0, 2)
+            h = t.empty((self.n_tokens, m.L, m.K), dtype=t.uint8, pin_memory=pin)
+            h.copy_(src)
+            b = self.chunk_bounds - self.tok_begin
+            return ActivationTrace(self.model, h, 0, self.n_tokens, self.chunk_ids.copy(), b.astype(np.int64),
+                                   self.source_is_file, self._validated, layout="tokens")
+        if self.layout == "tokens":
+            raise ConfigError("to_host(layout='planes') of a token-major trace: evaluate it directly")
         if pin:  # allocate pinned and copy once (no pageable intermediate: half the peak host memory)
             h = t.empty(self.planes.shape, dtype=self.planes.dtype, pin_memory=True)
             h.copy_(self.planes)
@@ -138,6 +186,8 @@ class ActivationTrace:
             K = m.K if m else 0
             L = m.L if m else 0
             return np.zeros((0, L, K), dtype=np.uint8)
+        if self.layout == "tokens":
+            return self.planes[self.tok_begin:self.tok_end].numpy().copy()
         K = m.K
         x = self.planes[:, self.tok_begin * K:self.tok_end * K].cpu().numpy()
         return np.ascontiguousarray(x.reshape(m.L, self.n_tokens, K).transpose(1, 0, 2))
@@ -147,7 +197,7 @@ class ActivationTrace:
         b = self.chunk_bounds
         return ActivationTrace(self.model, self.planes, int(b[chunk_lo]), int(b[chunk_hi] - b[chunk_lo]),
                                self.chunk_ids[chunk_lo:chunk_hi].copy(), b[chunk_lo:chunk_hi + 1].copy(),
-                               self.source_is_file, self._validated)
+                               self.source_is_file, self._validated, layout=self.layout)
 
     @classmethod
     def from_router_topk(cls, model: ModelSpec, topk_ids, chunk_bounds: Optional[Sequence[int]] = None,
@@ -166,8 +216,10 @@ class ActivationTrace:
         N = int(ids.shape[0])
         if N and (int(ids.min()) < 0 or int(ids.max()) >= model.E):
             raise MoeplaceError(f"router ids outside [0, {model.E})")
-        planes = t.zeros((model.L, _plane_stride(N, model.K)), dtype=t.uint8, device=dev)
-        planes[:, :N * model.K] = ids.to(t.uint8).permute(1, 0, 2).reshape(model.L, N * model.K)
+        planes = t.empty((model.L, _plane_stride(N, model.K)), dtype=t.uint8, device=dev)
+        u8 = ids.to(t.uint8).contiguous()
+        _lib.call("mp_tokens_to_planes_u8", _lib.ptr(u8), N, model.L, model.K, _lib.ptr(planes), planes.shape[1], 0,
+                  _lib.stream_handle())
         b = np.array([0, N] if chunk_bounds is None else list(chunk_bounds), dtype=np.int64)
         if b[0] != 0 or b[-1] != N or (np.diff(b) < 0).any():
             raise ConfigError("chunk_bounds must ascend from 0 to N")
@@ -181,7 +233,8 @@ class ActivationTrace:
                     device=None) -> "ActivationTrace":
         """Build a trace from token-major selections [N, L, K] and per-token chunk labels.
         Tokens are stably regrouped by ascending chunk id (evaluation is invariant under
-        permutation within a chunk)."""
+        permutation within a chunk); the token-major bytes are uploaded as they are
+        and transposed into layer planes on the device (``mp_tokens_to_planes_u8``)."""
         sel = np.asarray(selections)
         if sel.ndim != 3 or sel.shape[1:] != (model.L, model.K):
             raise ConfigError(f"selections must have shape [N, {model.L}, {model.K}], got {sel.shape}")
@@ -191,29 +244,55 @@ class ActivationTrace:
         cid = np.zeros(N, dtype=np.int64) if chunk_of_token is None else np.asarray(chunk_of_token, dtype=np.int64)
         if cid.shape != (N,):
             raise ConfigError("chunk_of_token must have one label per token")
-        order = np.argsort(cid, kind="stable")
-        sel, cid = sel[order], cid[order]
+        if N and (cid[1:] < cid[:-1]).any():
+            order = np.argsort(cid, kind="stable")
+            sel, cid = sel[order], cid[order]
         ids, counts = np.unique(cid, return_counts=True)
         bounds = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        return cls(model, _planes_from_tokens(model, sel.astype(np.uint8), device), 0, N, ids.astype(np.int64), bounds)
+        tok = np.ascontiguousarray(sel, dtype=np.uint8)
+        tr = cls(model, _lib.torch().from_numpy(tok), 0, N, ids.astype(np.int64), bounds, layout="tokens")
+        if device is not None and str(device) == "cpu":
+            return tr
+        if _lib.torch().cuda.is_available():
+            planes, _, _ = tr.device_view()
+            return cls(model, planes, 0, N, tr.chunk_ids, bounds)
+        return tr
+
+    @classmethod
+    def from_host_tokens(cls, model: ModelSpec, selections, chunk_bounds: Optional[Sequence[int]] = None,
+                         chunk_ids: Optional[Sequence[int]] = None, pin: bool = True) -> "ActivationTrace":
+        """The SPEC-shaped end-to-end input: token-major uint8 selections [N, L, K] held in host
+        memory, tokens already grouped by chunk (``chunk_bounds`` ascending from 0 to N; default
+        one chunk).  Nothing is transposed or copied on the host beyond one pinned staging copy
+        (none when ``selections`` is already a pinned uint8 tensor): every pass streams the
+        token-major slices to the device and transposes them there (``mp_tokens_to_planes_u8``)."""
+        t = _lib.torch()
+        if model.E > MAX_EXPERTS:
+            raise ConfigError(f"E = {model.E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
+        x = selections if isinstance(selections, t.Tensor) else t.from_numpy(np.ascontiguousarray(selections))
+        if x.dim() != 3 or tuple(x.shape[1:]) != (model.L, model.K):
+            raise ConfigError(f"selections must have shape [N, {model.L}, {model.K}], got {tuple(x.shape)}")
+        if x.is_cuda:
+            raise ConfigError("from_host_tokens takes host selections (use from_router_topk for device ids)")
+        if x.dtype != t.uint8:
+            if x.numel() and (int(x.min()) < 0 or int(x.max()) >= model.E):
+                raise MoeplaceError(f"expert index outside [0, {model.E})")
+            x = x.to(t.uint8)
+        x = x.contiguous()
+        if pin and not x.is_pinned():
+            x = x.pin_memory()
+        N = int(x.shape[0])
+        b = np.array([0, N] if chunk_bounds is None else list(chunk_bounds), dtype=np.int64)
+        if b[0] != 0 or b[-1] != N or (np.diff(b) < 0).any():
+            raise ConfigError("chunk_bounds must ascend from 0 to N")
+        cid = np.arange(len(b) - 1, dtype=np.int64) if chunk_ids is None else np.asarray(chunk_ids, dtype=np.int64)
+        if cid.shape != (len(b) - 1,) or (np.diff(cid) <= 0).any():
+            raise ConfigError("chunk_ids must be one ascending id per chunk")
+        return cls(model, x, 0, N, cid, b, layout="tokens")
 
 
 def _plane_stride(n_tokens: int, K: int) -> int:
     return max(16, (n_tokens * K + 15) // 16 * 16)
-
-
-def _planes_from_tokens(model: ModelSpec, sel: np.ndarray, device=None):
-    t = _lib.torch()
-    N = sel.shape[0]
-    stride = _plane_stride(N, model.K)
-    host = np.zeros((model.L, stride), dtype=np.uint8)
-    host[:, :N * model.K] = sel.transpose(1, 0, 2).reshape(model.L, N * model.K)
-    x = t.from_numpy(host)
-    if device is not None:
-        x = x.to(device)
-    elif t.cuda.is_available():
-        x = x.to(_lib.require_cuda())
-    return x
 
 
 def default_attention_placement(model: ModelSpec, order: Sequence[int]) -> AttentionPlacement:
@@ -423,11 +502,10 @@ def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
     """SPEC.md:132-139.  Parse the text trace format; errors raise ``TraceParseError`` with the
     1-based line number (header = line 1).  ``engine="cuda"`` (default) parses on the GPU
     (``mp_count_newlines``/``mp_find_newlines``/``mp_parse_trace_text``) straight into the
-    device planes; ``engine="host"`` is the host parser for CPU-only tooling."""
-    if engine == "host":
-        return _parse_trace_host(path)
+    device planes.  There is no host parser: the path has no CPU fallback (the tests' checker is
+    ``oracle/textio.py``)."""
     if engine != "cuda":
-        raise ConfigError(f"unknown parse engine {engine!r}")
+        raise ConfigError(f"unknown parse engine {engine!r} (the trace parser runs on the device only)")
     t = _lib.torch()
     dev = _lib.require_cuda()
     with open(path, "rb") as f:
@@ -494,94 +572,36 @@ def parse_trace(path, engine: str = "cuda") -> ActivationTrace:
     return ActivationTrace(model, planes, 0, N, ids.astype(np.int64), bounds, source_is_file=True, _validated=True)
 
 
-def _parse_trace_host(path) -> ActivationTrace:
-    """Host text parser (engine="host"): for CPU-only tooling and as the error-message reference."""
-    with open(path, "r") as f:
-        text = f.read()
-    lines = text.split("\n")
-    if lines and lines[-1] == "":
-        lines.pop()
-    if not lines:
-        t = _lib.torch()
-        return ActivationTrace(None, t.zeros((0, 16), dtype=t.uint8), 0, 0, np.zeros(0, np.int64),
-                               np.zeros(1, np.int64), source_is_file=True)
-    m = _HEADER.match(lines[0])
-    if not m:
-        raise TraceParseError("missing or malformed header '#moeplace-trace v1 L=<L> E=<E> K=<K>'", 1)
-    try:
-        model = ModelSpec(int(m.group(1)), int(m.group(2)), int(m.group(3)))
-    except ConfigError as e:
-        raise TraceParseError(str(e), 1) from None
-    L, E, K = model.L, model.E, model.K
-    N = len(lines) - 1
-    sel = np.empty((N, L, K), dtype=np.int64)
-    cid = np.empty(N, dtype=np.int64)
-    for i, line in enumerate(lines[1:]):
-        ln = i + 2
-        parts = line.rstrip("\r").split("\t")
-        if len(parts) != L + 1:
-            raise TraceParseError(f"expected {L} layer fields, found {len(parts) - 1}", ln)
-        try:
-            cid[i] = int(parts[0])
-        except ValueError:
-            raise TraceParseError(f"bad chunk id {parts[0]!r}", ln) from None
-        if cid[i] < 0:
-            raise TraceParseError(f"negative chunk id {cid[i]}", ln)
-        for l in range(L):
-            fm = _FIELD.match(parts[l + 1])
-            if not fm or int(fm.group(1)) != l:
-                raise TraceParseError(f"malformed field {parts[l + 1]!r} (expected layer{l}:e,...)", ln)
-            items = fm.group(2).split(",")
-            if len(items) != K:
-                raise TraceParseError(f"layer {l}: expected {K} experts, found {len(items)}", ln)
-            try:
-                vals = [int(v) for v in items]
-            except ValueError:
-                raise TraceParseError(f"layer {l}: non-integer expert index", ln) from None
-            for v in vals:
-                if v < 0 or v >= E:
-                    raise TraceParseError(f"layer {l}: expert index {v} outside [0, {E})", ln)
-            if len(set(vals)) != K:
-                raise TraceParseError(f"layer {l}: repeated expert index", ln)
-            sel[i, l] = vals
-    if E > MAX_EXPERTS:
-        raise ConfigError(f"E = {E} exceeds the one-byte device id format (E <= {MAX_EXPERTS})")
-    tr = ActivationTrace.from_tokens(model, sel.astype(np.uint8), cid, device="cpu")
-    tr.source_is_file = True
-    tr._validated = True
-    return tr
-
-
-def write_trace(trace: ActivationTrace, path, engine: str = "auto") -> None:
+def write_trace(trace: ActivationTrace, path, engine: str = "cuda") -> None:
     """SPEC.md:132-139, 170.  Canonical text form: header, then one line per token in
-    chunk-grouped order.  ``engine="cuda"`` formats on the device (two passes: per-line lengths,
-    prefix sum, each thread writes its line; ``mp_format_lengths`` / ``mp_format_trace_text``)
-    then writes the buffer; ``"auto"`` uses it when the planes are on the GPU."""
+    chunk-grouped order, formatted on the device (two passes: per-line lengths, prefix sum, each
+    thread writes its line; ``mp_format_lengths`` / ``mp_format_trace_text``) and written through
+    the pinned ring.  A host-resident trace is uploaded (only the view's tokens) first; there is
+    no host writer (no CPU fallback; ``engine`` other than "cuda" raises)."""
     m = trace.model
-    if engine == "auto":
-        engine = "cuda" if (m is not None and trace.n_tokens and trace.planes.is_cuda) else "host"
-    if engine == "host":
-        return _write_trace_host(trace, path)
-    if engine != "cuda":
-        raise ConfigError(f"unknown write engine {engine!r}")
+    if engine not in ("cuda", "auto"):
+        raise ConfigError(f"unknown write engine {engine!r} (the trace writer runs on the device only)")
+    if m is None:
+        with open(path, "w"):
+            return
     t = _lib.torch()
     header = f"#moeplace-trace v1 L={m.L} E={m.E} K={m.K}\n".encode()
     if trace.n_tokens == 0:
         with open(path, "wb") as f:
             f.write(header)
         return
-    planes = trace.device_planes()
+    planes, t0, t1 = trace.device_view()
     dev = planes.device
     n = trace.n_tokens
     cids = _lib.to_dev(trace.token_chunk_ids(), t.int64)
     lens = t.empty(n, dtype=t.int64, device=dev)
     sh = _lib.stream_handle()
-    _lib.call("mp_format_lengths", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
+    _lib.call("mp_format_lengths", _lib.ptr(planes), planes.shape[1], t0, t1, m.L, m.K,
               _lib.ptr(cids), _lib.ptr(lens), sh)
     offs = (t.cumsum(lens, 0) - lens).contiguous()
     total = int(lens.sum().item())
     out = t.empty(total, dtype=t.uint8, device=dev)
-    _lib.call("mp_format_trace_text", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K,
+    _lib.call("mp_format_trace_text", _lib.ptr(planes), planes.shape[1], t0, t1, m.L, m.K,
               _lib.ptr(cids), _lib.ptr(offs), _lib.ptr(out), sh)
     with open(path, "wb") as f:
         f.write(header)
@@ -591,21 +611,6 @@ def write_trace(trace: ActivationTrace, path, engine: str = "auto") -> None:
         except (OSError, AttributeError):
             pass
         _device_to_file(out, total, f.fileno(), len(header))
-
-
-def _write_trace_host(trace: ActivationTrace, path) -> None:
-    """Host text writer (engine="host")."""
-    m = trace.model
-    with open(path, "w") as f:
-        if m is None:
-            return
-        f.write(f"#moeplace-trace v1 L={m.L} E={m.E} K={m.K}\n")
-        sel = trace.tokens()
-        cid = trace.token_chunk_ids()
-        prefixes = [f"layer{l}:" for l in range(m.L)]
-        for t in range(sel.shape[0]):
-            f.write(str(int(cid[t])) + "\t" + "\t".join(
-                prefixes[l] + ",".join(str(int(v)) for v in sel[t, l]) for l in range(m.L)) + "\n")
 
 
 _BIN_MAGIC = b"MPTRACE1"
@@ -620,7 +625,8 @@ def write_trace_binary(trace: ActivationTrace, path) -> None:
     if m is None:
         raise ConfigError("cannot write an empty (model-less) trace")
     K = m.K
-    planes = trace.planes[:, trace.tok_begin * K:trace.tok_end * K].contiguous().cpu().numpy()
+    dplanes, t0, t1 = trace.device_view()
+    planes = dplanes[:, t0 * K:t1 * K].contiguous().cpu().numpy()
     bounds = (trace.chunk_bounds - trace.tok_begin).astype(np.int64)
     hdr = json.dumps({"L": m.L, "E": m.E, "K": K, "n_tokens": trace.n_tokens, "n_chunks": trace.n_chunks}).encode()
     with open(path, "wb") as f:
@@ -660,24 +666,37 @@ def read_trace_binary(path, device: str = "pinned") -> ActivationTrace:
 
 
 def validate_trace(trace: ActivationTrace) -> None:
-    """Check the ActivationTrace invariants on the device (``mp_validate_u8``)."""
+    """Check the ActivationTrace invariants on the device (``mp_validate_u8``).
+    A host-resident trace is validated slice by slice as it streams (``sweep``)."""
     if trace._validated or trace.n_tokens == 0:
         return
+    if not trace.on_device:
+        sweep(trace, lambda *a: None)
+        return
     m = trace.model
-    planes = trace.device_planes()
+    planes = trace.planes
     err = _lib.new_err()
     _lib.call("mp_validate_u8", _lib.ptr(planes), planes.shape[1], trace.tok_begin, trace.tok_end, m.L, m.K, m.E,
               _lib.ptr(err), _lib.stream_handle())
-    flag, enc, _, n = _lib.read_err(err)
-    if flag:
-        key = (2 ** 63 - 1) - enc
-        code, tl = key % 8, key // 8
-        tok, layer = tl // m.L, tl % m.L
-        what = "expert index >= E" if code == _lib.DATA_EXPERT_RANGE else "repeated expert index"
-        if trace.source_is_file:
-            raise TraceParseError(f"layer {layer}: {what}", tok - trace.tok_begin + 2)
-        raise MoeplaceError(f"token {tok - trace.tok_begin}, layer {layer}: {what} ({n} bad records)")
+    _raise_invalid(trace, err, 0)
     trace._validated = True
+
+
+def _raise_invalid(trace: ActivationTrace, err, base: int) -> None:
+    """Raise the SPEC error for a flagged mp_validate_u8 err block.  The kernel reports token
+    indices of the planes it checked; ``base`` maps them to the trace's numbering (0 for the
+    trace's own planes, the slice's first token for a streamed slice)."""
+    flag, enc, _, n = _lib.read_err(err)
+    if not flag:
+        return
+    m = trace.model
+    key = (2 ** 63 - 1) - enc
+    code, tl = key % 8, key // 8
+    tok, layer = tl // m.L + base, tl % m.L  # absolute token index
+    what = "expert index >= E" if code == _lib.DATA_EXPERT_RANGE else "repeated expert index"
+    if trace.source_is_file:
+        raise TraceParseError(f"layer {layer}: {what}", tok - trace.tok_begin + 2)
+    raise MoeplaceError(f"token {tok - trace.tok_begin}, layer {layer}: {what} ({n} bad records)")
 
 
 # ---- statistics (SPEC.md:140-161) -----------------------------------------------------------
@@ -691,56 +710,70 @@ STREAM_BLOCK_TOKENS = 1 << 20  # host-streaming slice (R1: 464 MB per slice)
 
 
 def sweep(trace: ActivationTrace, launch) -> None:
-    """Run ``launch(planes, stride, t0, t1, bounds)`` over the whole trace.
+    """Run ``launch(planes, stride, t0, t1, bounds)`` over the whole trace, in token order.
 
-    Device-resident planes: one call.  Pinned host planes (the end-to-end path): the trace is
-    streamed through two device slices — the 2-D H2D copy of slice i+1 (``mp_copy_planes_h2d`` on
-    a copy stream) overlaps the kernels on slice i — and ``launch`` accumulates per slice (every
-    kernel output is additive over token ranges).  Other host planes are uploaded once and cached.
+    Device-resident planes: one call.  Host-resident traces (the end-to-end path) stream through
+    two device slices of STREAM_BLOCK_TOKENS tokens: the H2D copy of slice i+1 (on a copy stream)
+    overlaps the kernels on slice i, and ``launch`` accumulates per slice (every kernel output is
+    additive over token ranges).  Layer planes move with one 2-D copy per slice
+    (``mp_copy_planes_h2d``); token-major [N, L, K] selections move as one contiguous copy and are
+    transposed into the slice's planes on the device (``mp_tokens_to_planes_u8``).  Nothing is
+    cached on the device, so a trace larger than HBM streams too.
     """
     t = _lib.torch()
     if trace.n_tokens == 0:
         return
-    planes = trace.planes
-    if planes.is_cuda or not planes.is_pinned():
-        planes = trace.device_planes()
+    if trace.on_device:
         validate_trace(trace)
+        planes = trace.planes
         bounds = _lib.to_dev(trace.chunk_bounds, t.int64)
         launch(planes, planes.shape[1], trace.tok_begin, trace.tok_end, bounds)
         return
+    src = trace.planes
     m = trace.model
     dev = _lib.require_cuda()
-    K = m.K
+    K, L = m.K, m.L
+    tok_major = trace.layout == "tokens"
     T = min(STREAM_BLOCK_TOKENS, trace.n_tokens)
     blocks = [(a, min(a + T, trace.tok_end)) for a in range(trace.tok_begin, trace.tok_end, T)]
     rel = np.stack([np.clip(trace.chunk_bounds, a, b) - a for a, b in blocks]).astype(np.int64)
     d_rel = _lib.to_dev(rel, t.int64)
-    stride = max(16, (T * K + 15) // 16 * 16)
-    bufs = [t.empty((m.L, stride), dtype=t.uint8, device=dev) for _ in range(min(2, len(blocks)))]
+    stride = _plane_stride(T, K)
+    nbuf = min(2, len(blocks))
+    if tok_major:  # staging for the token-major bytes; ONE plane slice (transpose + launch share a stream)
+        bufs = [t.empty(T * L * K, dtype=t.uint8, device=dev) for _ in range(nbuf)]
+        pbuf = t.empty((L, stride), dtype=t.uint8, device=dev)
+    else:
+        bufs = [t.empty((L, stride), dtype=t.uint8, device=dev) for _ in range(nbuf)]
     comp = t.cuda.current_stream()
     copy = t.cuda.Stream()
     copied = [t.cuda.Event() for _ in bufs]
     free = [t.cuda.Event() for _ in bufs]
     copy.wait_stream(comp)  # d_rel and the outputs are ready before the first slice lands
-    src_stride = planes.shape[1]
+    sh = _lib.stream_handle()
     for i, (a, b) in enumerate(blocks):
-        j = i % len(bufs)
+        j = i % nbuf
+        n = b - a
         with t.cuda.stream(copy):
-            if i >= len(bufs):
+            if i >= nbuf:
                 copy.wait_event(free[j])
-            _lib.call("mp_copy_planes_h2d", _lib.ptr(bufs[j]), stride, C_void(planes.data_ptr() + a * K), src_stride,
-                      (b - a) * K, m.L, C_void(copy.cuda_stream))
+            if tok_major:
+                bufs[j][:n * L * K].copy_(src[a:b].view(-1), non_blocking=True)
+            else:
+                _lib.call("mp_copy_planes_h2d", _lib.ptr(bufs[j]), stride, C_void(src.data_ptr() + a * K),
+                          src.shape[1], n * K, L, C_void(copy.cuda_stream))
             copied[j].record(copy)
         comp.wait_event(copied[j])
+        if tok_major:
+            _lib.call("mp_tokens_to_planes_u8", _lib.ptr(bufs[j]), n, L, K, _lib.ptr(pbuf), stride, 0, sh)
+            planes = pbuf
+        else:
+            planes = bufs[j]
         if not trace._validated:
             err = _lib.new_err()
-            _lib.call("mp_validate_u8", _lib.ptr(bufs[j]), stride, 0, b - a, m.L, K, m.E, _lib.ptr(err),
-                      _lib.stream_handle())
-            flag, enc, _, n = _lib.read_err(err)
-            if flag:
-                key = (2 ** 63 - 1) - enc
-                raise MoeplaceError(f"token {a + (key // 8) // m.L - trace.tok_begin}: invalid record ({n} bad)")
-        launch(bufs[j], stride, 0, b - a, d_rel[i])
+            _lib.call("mp_validate_u8", _lib.ptr(planes), stride, 0, n, L, K, m.E, _lib.ptr(err), sh)
+            _raise_invalid(trace, err, a)
+        launch(planes, stride, 0, n, d_rel[i])
         free[j].record(comp)
     trace._validated = True
     comp.wait_stream(copy)

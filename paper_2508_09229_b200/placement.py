@@ -14,7 +14,7 @@ from typing import Any, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .errors import ConfigError, InfeasibleError, MoeplaceError
+from .errors import ConfigError, InfeasibleError, MoeplaceError, TraceParseError
 from .model_trace import AttentionPlacement, ModelSpec
 from .topology import DistanceMatrix
 
@@ -221,8 +221,12 @@ def read_placement(path, model: ModelSpec, c: Optional[Constraints] = None, n_de
         header = next(r, None)
         if header != ["layer", "expert", "device"]:
             raise ConfigError(f"{path}: expected header layer,expert,device")
-        for row in r:
-            l, e, s = (int(v) for v in row)
+        for ln, row in enumerate(r, start=2):
+            try:
+                l, e, s = (int(v) for v in row)
+            except ValueError:  # short row, extra field or non-integer: a parse error at that line (exit 4)
+                raise TraceParseError(f"{path}: expected three integers 'layer,expert,device', got {row!r}",
+                                      ln) from None
             if not (0 <= l < model.L and 0 <= e < model.E):
                 raise ConfigError(f"{path}: ({l}, {e}) outside the model shape")
             assign[l, e] = s

@@ -266,8 +266,8 @@ def test_data_errors_are_reported():
         mt.estimate_frequencies(tr, m)
     bad = np.array([[[0, 9], [2, 3]]], dtype=np.uint8)
     import torch
-    tr2 = mt.ActivationTrace(m, mt._planes_from_tokens(m, bad), 0, 1, np.zeros(1, np.int64),
-                             np.array([0, 1], np.int64))
+    tr2 = mt.ActivationTrace(m, torch.from_numpy(bad), 0, 1, np.zeros(1, np.int64), np.array([0, 1], np.int64),
+                             layout="tokens")  # token-major host trace: validated slice by slice on the device
     with pytest.raises(MoeplaceError):
         mt.estimate_frequencies(tr2, m)
     with pytest.raises(MoeplaceError):
@@ -345,6 +345,45 @@ def test_host_streaming_matches_device(monkeypatch):
     assert not host.planes.is_cuda  # streamed, not cached on the device
 
 
+@pytest.mark.parametrize("shape", [R1, B16, (3, 5, 2)])
+def test_token_major_host_streaming_matches_device(monkeypatch, shape):
+    """SPEC-shaped end-to-end input: token-major [N, L, K] selections in pinned host memory,
+    streamed slice by slice and transposed on the device (mp_tokens_to_planes_u8; K = 8 takes the
+    tiled u64 transpose), give the device-resident integers -- slices cut through chunks, views
+    start mid-slice, per-token hops land at the right offsets."""
+    import moeplace.model_trace as mtm
+    monkeypatch.setattr(mtm, "STREAM_BLOCK_TOKENS", 1000)
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    g, dist, order, attn, cost = setup_topology("FatTree", 2, 2, 8, m)
+    tr = mt.generate_trace(m, 1.2, 4321, 9, 21)
+    rng = np.random.default_rng(3)
+    pls = [mpl.Placement(random_assign(rng, L, E, g.n_devices)) for _ in range(5)]
+    host = mt.ActivationTrace.from_host_tokens(m, tr.tokens(), tr.chunk_bounds)
+    assert host.layout == "tokens" and host.planes.is_pinned()
+    assert np.array_equal(host.tokens(), tr.tokens())
+    assert np.array_equal(ev.score_sums(host, pls, cost), ev.score_sums(tr, pls, cost))
+    f_h, r_h = ev.evaluate_with_stats(host, pls[:4], cost)
+    f_d, r_d = ev.evaluate_with_stats(tr, pls[:4], cost)
+    assert np.array_equal(f_h.counts, f_d.counts)
+    assert [r.chunk_hop_sums for r in r_h] == [r.chunk_hop_sums for r in r_d]
+    v_h, v_d = host.view(2, 7), tr.view(2, 7)
+    assert np.array_equal(ev.score_sums(v_h, pls, cost), ev.score_sums(v_d, pls, cost))
+    assert np.array_equal(ev.token_hops_all(v_h, pls[:2], cost), ev.token_hops_all(v_d, pls[:2], cost))
+    assert np.array_equal(v_h.device_planes()[:, :v_h.n_tokens * K].cpu().numpy(),
+                          v_d.planes[:, v_d.tok_begin * K:v_d.tok_end * K].cpu().numpy())
+    # router ids on the device: the same transpose kernel
+    import torch
+    r = mt.ActivationTrace.from_router_topk(m, torch.as_tensor(tr.tokens(), device="cuda").long(), tr.chunk_bounds)
+    assert np.array_equal(r.tokens(), tr.tokens())
+    # invalid ids in a token-major host trace are caught while streaming
+    bad = tr.tokens()
+    bad[1234, L - 1, 0] = bad[1234, L - 1, K - 1] if K > 1 else E
+    hb = mt.ActivationTrace.from_host_tokens(m, bad, tr.chunk_bounds)
+    with pytest.raises(MoeplaceError):
+        mt.estimate_frequencies(hb, m)
+
+
 @pytest.mark.parametrize("shape,kind,size", [
     (R1, "FatTree", (4, 2, 4)), (B16, "Dragonfly", (4, 2, 4)), ((3, 16, 5), "DragonflySparse", (4, 2, 4)),
     # K = 8 general path: pe bytes up to 36 in some layers (fast and general layers mixed), and
@@ -387,13 +426,16 @@ def _write_lines(path, lines, trailing="\n"):
     (["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,3", ""], 3),
     (["garbage"], 1),
 ])
-def test_device_parser_errors_match_host(tmp_path, lines, line_no):
+def test_device_parser_errors_match_oracle(tmp_path, lines, line_no):
+    from oracle.textio import TextParseError, parse_text
     f = tmp_path / "t.txt"
     _write_lines(f, lines)
-    for engine in ("host", "cuda"):
-        with pytest.raises(TraceParseError) as e:
-            mt.parse_trace(f, engine=engine)
-        assert e.value.line_no == line_no, engine
+    with pytest.raises(TextParseError) as e:
+        parse_text(f)
+    assert e.value.line_no == line_no
+    with pytest.raises(TraceParseError) as e:
+        mt.parse_trace(f)
+    assert e.value.line_no == line_no
 
 
 def test_device_parser_roundtrip_and_regroup(tmp_path):
@@ -401,10 +443,11 @@ def test_device_parser_roundtrip_and_regroup(tmp_path):
     tr = mt.generate_trace(m, 1.2, 3001, 17, 5)
     f = tmp_path / "t.txt"
     mt.write_trace(tr, f)
+    from oracle.textio import parse_text, regroup
     d = mt.parse_trace(f)  # device engine
-    h = mt.parse_trace(f, engine="host")
+    _, hsel, hcid = parse_text(f)
     assert d.planes.is_cuda
-    assert np.array_equal(d.tokens(), tr.tokens()) and np.array_equal(h.tokens(), tr.tokens())
+    assert np.array_equal(d.tokens(), tr.tokens()) and np.array_equal(hsel, tr.tokens())
     assert np.array_equal(d.chunk_bounds, tr.chunk_bounds) and np.array_equal(d.chunk_ids, tr.chunk_ids)
     g = tmp_path / "u.txt"
     mt.write_trace(d, g)
@@ -413,8 +456,8 @@ def test_device_parser_roundtrip_and_regroup(tmp_path):
     lines = ["#moeplace-trace v1 L=2 E=5 K=2", "7\t0:0,1\t1:2,3\r", "3\tlayer0:4,1\tlayer1:0,3", "7\tlayer0:2,1\t1:2,4"]
     _write_lines(tmp_path / "v.txt", lines, trailing="")
     a = mt.parse_trace(tmp_path / "v.txt")
-    b = mt.parse_trace(tmp_path / "v.txt", engine="host")
-    assert np.array_equal(a.tokens(), b.tokens())
+    bsel, _, _ = regroup(*parse_text(tmp_path / "v.txt")[1:])
+    assert np.array_equal(a.tokens(), bsel)
     assert a.chunk_ids.tolist() == [3, 7] and a.chunk_bounds.tolist() == [0, 1, 3]
     assert a.tokens()[:, 0, :].tolist() == [[4, 1], [0, 1], [2, 1]]
 
@@ -525,17 +568,22 @@ def test_contract_tc_count_above_the_stated_bound_raises():
 
 
 @pytest.mark.parametrize("shape", [R1, B16, (2, 4, 1), (1, 256, 3)])
-def test_device_writer_matches_host_writer(tmp_path, shape):
+def test_device_writer_matches_oracle_writer(tmp_path, shape):
+    from oracle.textio import write_text
     L, E, K = shape
     m = mt.ModelSpec(L, E, K)
     tr = mt.generate_trace(m, 1.2, 1234, 11, 3)
-    mt.write_trace(tr, tmp_path / "d.txt", engine="cuda")
-    mt.write_trace(tr, tmp_path / "h.txt", engine="host")
+    mt.write_trace(tr, tmp_path / "d.txt")
+    write_text(tmp_path / "h.txt", (L, E, K), tr.tokens(), tr.token_chunk_ids())
     assert (tmp_path / "d.txt").read_bytes() == (tmp_path / "h.txt").read_bytes()
     v = tr.view(2, 7)
-    mt.write_trace(v, tmp_path / "dv.txt", engine="cuda")
-    mt.write_trace(v, tmp_path / "hv.txt", engine="host")
+    mt.write_trace(v, tmp_path / "dv.txt")
+    write_text(tmp_path / "hv.txt", (L, E, K), v.tokens(), v.token_chunk_ids())
     assert (tmp_path / "dv.txt").read_bytes() == (tmp_path / "hv.txt").read_bytes()
+    # a host-resident trace (pinned planes or token-major) is written through the device too
+    mt.write_trace(v.to_host(pin=True), tmp_path / "dh.txt")
+    mt.write_trace(tr.to_host(pin=True, layout="tokens").view(2, 7), tmp_path / "dt.txt")
+    assert (tmp_path / "dh.txt").read_bytes() == (tmp_path / "dt.txt").read_bytes() == (tmp_path / "hv.txt").read_bytes()
     back = mt.parse_trace(tmp_path / "d.txt")
     assert np.array_equal(back.tokens(), tr.tokens())
 

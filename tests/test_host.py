@@ -323,46 +323,84 @@ def test_brute_force_guard():
         sv.brute_force_optimum(_inst(np.ones((3, 4, 5)), 1, 4))
 
 
-# ---------------- trace text format (host side) ----------------
+# ---------------- trace text format: the oracle's restatement (the product parses on the device) ----
 
 def _write(path, lines):
     path.write_text("\n".join(lines) + "\n")
 
 
-def test_parse_trace_errors(tmp_path):
+def test_oracle_text_parser_errors(tmp_path):
+    from oracle.textio import TextParseError, parse_text
     f = tmp_path / "t.txt"
     _write(f, ["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,3", "0\tlayer0:0,4\tlayer1:2,3"])
-    with pytest.raises(TraceParseError) as e:
-        mt.parse_trace(f, engine="host")  # expert index E -> error at that line
+    with pytest.raises(TextParseError) as e:
+        parse_text(f)  # expert index E -> error at that line
     assert e.value.line_no == 3
     _write(f, ["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1"])
-    with pytest.raises(TraceParseError) as e:
-        mt.parse_trace(f, engine="host")
+    with pytest.raises(TextParseError) as e:
+        parse_text(f)
     assert e.value.line_no == 2
     _write(f, ["#moeplace-trace v1 L=2 E=4 K=2", "0\tlayer0:0,1\tlayer1:2,2"])
-    with pytest.raises(TraceParseError):
-        mt.parse_trace(f, engine="host")
+    with pytest.raises(TextParseError):
+        parse_text(f)
     _write(f, ["garbage"])
-    with pytest.raises(TraceParseError) as e:
-        mt.parse_trace(f, engine="host")
+    with pytest.raises(TextParseError) as e:
+        parse_text(f)
     assert e.value.line_no == 1
     f.write_text("")
-    assert mt.parse_trace(f, engine="host").n_tokens == 0
+    assert parse_text(f)[1].shape[0] == 0
 
 
-def test_parse_write_roundtrip_host(tmp_path):
+def test_oracle_text_roundtrip(tmp_path):
+    from oracle.textio import parse_text, regroup, write_text
     f = tmp_path / "t.txt"
     lines = ["#moeplace-trace v1 L=2 E=5 K=2", "0\tlayer0:0,1\tlayer1:2,3", "0\tlayer0:4,1\tlayer1:0,3",
              "3\tlayer0:2,1\tlayer1:2,4"]
     _write(f, lines)
-    tr = mt.parse_trace(f, engine="host")
-    assert tr.n_tokens == 3 and tr.chunk_ids.tolist() == [0, 3] and tr.chunk_bounds.tolist() == [0, 2, 3]
+    shape, sel, cid = parse_text(f)
+    sel2, ids, bounds = regroup(sel, cid)
+    assert sel.shape[0] == 3 and ids.tolist() == [0, 3] and bounds.tolist() == [0, 2, 3]
     g = tmp_path / "u.txt"
-    mt.write_trace(tr, g)
+    write_text(g, shape, sel2, np.repeat(ids, np.diff(bounds)))
     assert g.read_text() == f.read_text()
-    # prefix-less fields are accepted
+    _write(f, ["#moeplace-trace v1 L=1 E=3 K=1", "1\t0:2"])  # prefix-less fields are accepted
+    assert parse_text(f)[1].tolist() == [[[2]]]
+
+
+def test_product_has_no_host_text_engine(tmp_path):
+    """The product parses and writes traces on the device only (no CPU fallback): asking for a
+    host engine is a configuration error, not a silent CPU path."""
+    f = tmp_path / "t.txt"
     _write(f, ["#moeplace-trace v1 L=1 E=3 K=1", "1\t0:2"])
-    assert mt.parse_trace(f, engine="host").tokens().tolist() == [[[2]]]
+    with pytest.raises(ConfigError):
+        mt.parse_trace(f, engine="host")
+    tr = mt.ActivationTrace(mt.ModelSpec(1, 3, 1), None, 0, 0, np.zeros(0, np.int64), np.zeros(1, np.int64))
+    with pytest.raises(ConfigError):
+        mt.write_trace(tr, tmp_path / "u.txt", engine="host")
+
+
+def test_cli_config_and_placement_errors_map_to_exit_codes(tmp_path):
+    """an invalid or non-object --config exits 2 (config error), a malformed placement
+    CSV row raises TraceParseError with its line number (exit 4)."""
+    import moeplace.cli as cli
+    bad = tmp_path / "bad.json"
+    bad.write_text("{not json")
+    assert cli.main(["topo", "build", "--config", str(bad), "--out", str(tmp_path / "g.json")]) == 2
+    bad.write_text("[1, 2]")
+    assert cli.main(["topo", "build", "--config", str(bad), "--out", str(tmp_path / "g.json")]) == 2
+    ok = tmp_path / "ok.json"
+    ok.write_text('{"L": 2, "E": 4, "K": 2, "c_exp": 4, "topology": "FatTree", "num_leaf_switches": 2, '
+                  '"num_nodes_per_leaf": 1, "num_gpus_per_server": 2}')
+    assert cli.main(["topo", "build", "--config", str(ok), "--out", str(tmp_path / "g.json")]) == 0
+    csvf = tmp_path / "p.csv"
+    csvf.write_text("layer,expert,device\n0,0,1\n0,1\n")
+    with pytest.raises(TraceParseError) as e:
+        mpl.read_placement(csvf, mt.ModelSpec(1, 2, 1))
+    assert e.value.line_no == 3 and exit_code(e.value) == 4
+    csvf.write_text("layer,expert,device\n0,x,1\n")
+    with pytest.raises(TraceParseError) as e:
+        mpl.read_placement(csvf, mt.ModelSpec(1, 2, 1))
+    assert e.value.line_no == 2
 
 
 def test_split_trace_host():
