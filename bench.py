@@ -17,11 +17,14 @@ owns a contiguous 10M-token shard of one N*10M-token trace (weak scaling) and th
 [counts | hop sums] buffer is combined with one NCCL all_reduce inside the timed step.
 
 value  = token-layers scored x placements per second, whole job: N*10M*58*4 / step time.
-e2e    = the same metric through the public API (moeplace.eval.evaluate_with_stats) on a trace
-         held in pinned HOST memory: the H2D copy (streamed in slices, overlapped with the
-         kernels), the kernels and the D2H of counts + sums are all inside the timed region.
---impl reference: the CPU restatement of the reference path (oracle/, numba, all host cores)
-         on a bounded sample of the same workload; rank 0 only.
+e2e    = the same metric through the public API (moeplace.eval.evaluate_with_stats) on the SPEC's
+         token-major [N, L, K] selections held in pinned HOST memory: the H2D copy (streamed in
+         slices, overlapped with the kernels), the on-device transpose into layer planes, the
+         kernels and the D2H of counts + sums are all inside the timed region.
+--impl reference: the CPU restatement of the reference path (oracle/, numba, all host cores) on
+         the same trace (regenerated on the CPU by the oracle's sampler), the same placements and
+         the same topology (bench_data/placements_wl*.npz, written by this script's GPU arm with
+         --write-fixtures and checked by it on every run); rank 0 only.
 """
 from __future__ import annotations
 
@@ -42,20 +45,44 @@ L, E, K = 58, 256, 8
 ZIPF_S, SEED = 1.2, 0
 TOK_PER_GPU = 10_000_000
 CHUNKS_PER_GPU = 150
-P = 4
 METRIC = "token-layers scored/sec (x placements) and achieved HBM GB/s"
 UNIT = "token-layers*placements/s"
+FIXTURES = ROOT / "bench_data"
+CPU_BLOCK = 1_000_000  # the CPU legs stream the trace in 1M-token blocks
+CONFIG3_KINDS = (("FatTree", 16), ("FatTreeHier", 16), ("Dragonfly", 16), ("DragonflySparse", 16),
+                 ("DragonflyPlus", 16), ("SlimFly", 18))
 
 
-def workload(n_gpus: int, tok: int, mode: str) -> dict:
-    return {"workload": "config2: DeepSeek-R1 shape (L=58, E=256, K=8), Zipf(1.2) synthetic trace, "
-                        f"{tok} tokens/GPU, {CHUNKS_PER_GPU} chunks/GPU, FatTree 8 leaves x 4 servers x 8 GPUs "
-                        "(256 devices), c_layer=1, c_exp=64; per step: load histogram + hop sums of P=4 "
-                        "placements (RR, Greedy, ILP, ILPLoad) over every token",
-            "tokens_per_gpu": tok, "tokens_total": tok * n_gpus, "placements": P, "kernel_mode": mode,
-            "l2": f"inputs larger than L2: {tok * L * K / 1e9:.2f} GB trace per GPU vs 126 MB L2, no flush needed",
-            "parallelism": f"token shards x{n_gpus} + 1 NCCL all_reduce of int64 counts|sums" if n_gpus > 1
-            else "single GPU"}
+def shape_of(wl: int, n_gpus: int, tokens_arg):
+    """(tokens per GPU, total tokens, total chunks, scaling) of a workload."""
+    if wl == 5:
+        n_total = tokens_arg or 100_000_000
+        return n_total // n_gpus, n_total, 1500, "strong"
+    per = tokens_arg or (1_000_000 if wl == 4 else TOK_PER_GPU)
+    return per, per * n_gpus, CHUNKS_PER_GPU * n_gpus, "weak"
+
+
+def workload(wl: int, n_gpus: int, tok: int, n_total: int, P: int) -> dict:
+    """The `config` object: identical for the GPU arm and the reference arm (same workload)."""
+    desc = {
+        2: "config2: DeepSeek-R1 shape (L=58, E=256, K=8), Zipf(1.2) synthetic trace, "
+           f"{tok} tokens/GPU, {CHUNKS_PER_GPU} chunks/GPU, FatTree 8 leaves x 4 servers x 8 GPUs "
+           "(256 devices), c_layer=1, c_exp=64; per step: load histogram + hop sums of P=4 "
+           "placements (RR, Greedy, ILP, ILPLoad) over every token",
+        3: f"config3: DeepSeek-R1 shape, {tok} Zipf(1.2) tokens/GPU, {CHUNKS_PER_GPU} chunks, 24 placements (RR, "
+           "Greedy, ILP, ILPLoad) x 6 topologies (FatTree, FatTreeHier, Dragonfly, DragonflySparse, DragonflyPlus "
+           "16x4x4 = 256 devices; SlimFly 18x4x4 = 288 devices), c_layer=1, c_exp=64; per step: hop sums of all 24",
+        4: f"config4: DeepSeek-R1 shape, {tok} Zipf(1.2) tokens/GPU, Dragonfly 16x4x4, 4096 candidate placements "
+           "(ILPLoad + 64 within-layer swaps each, seeds 1000+i); per step: per-chunk hop sums of all 4096",
+        5: f"config5: DeepSeek-R1 shape, {n_total} Zipf(1.2) tokens total sharded over {n_gpus} GPU(s), 1500 chunks, "
+           "FatTree 8x4x8; per step: load histogram + hop sums of P=4 placements (RR, Greedy, ILP, ILPLoad)",
+    }[wl]
+    by = tok * L * K
+    return {"workload": desc, "tokens_per_gpu": tok, "tokens_total": n_total, "placements": P,
+            "l2": (f"inputs larger than L2: {by / 1e9:.2f} GB trace per GPU vs 126 MB L2, no flush needed" if by > 126e6
+                   else f"trace {by / 1e6:.0f} MB < 126 MB L2 (reused across the step's passes)"),
+            "parallelism": (f"token shards x{n_gpus} + 1 NCCL all_reduce of int64 counts|sums" if n_gpus > 1
+                            else "single GPU")}
 
 
 def measured_peak():
@@ -100,6 +127,7 @@ class ClockSampler:
             self.th.start()
         except Exception:
             self.th = None
+        return self
 
     def stop(self) -> dict:
         self._stop.set()
@@ -113,25 +141,81 @@ class ClockSampler:
                 "window": "warm-up + timed steps (+ identical untimed steps until >= 8 samples)"}
 
 
-def cpu_sample(trace, n_sample: int):
-    """Token-major host copy of the first n_sample tokens of the device trace (same bytes)."""
-    import torch
-    v = trace.planes[:, trace.tok_begin * K:(trace.tok_begin + n_sample) * K].cpu().numpy()
-    return np.ascontiguousarray(v.reshape(L, n_sample, K).transpose(1, 0, 2))
+# ------------------------------ CPU legs (oracle; test infrastructure) ------------------------------
+
+def load_fixture(wl: int):
+    """Placements and cost matrices the GPU arm scores (written by `bench.py --write-fixtures`):
+    (labels, [assign int32 [L, E]], [p uint8 [L, S]] per placement)."""
+    key = {2: 2, 5: 2, 3: 3, 4: 4}[wl]
+    path = FIXTURES / f"placements_wl{key}.npz"
+    d = np.load(path)
+    labels = [str(x) for x in d["labels"]]
+    assigns = [d["assign"][i].astype(np.int32) for i in range(len(labels))]
+    costs = [d[f"p{int(t)}"] for t in d["topo_of"]]
+    return labels, assigns, costs, str(path.relative_to(ROOT))
 
 
-def time_oracle(sel, bounds, p, assigns, reps: int = 3, t0: int = 0):
-    """Seconds per pass of the CPU restatement: counts + per-chunk hop sums of every placement
-    in one token-block-parallel pass over the trace (oracle.evaluate.fused_pass)."""
+def perturb_swaps_np(base: np.ndarray, n: int, n_swaps: int, seed0: int) -> np.ndarray:
+    """Config-4 candidates, restated for the CPU leg (placement.perturb_swaps):
+    candidate i = `n_swaps` within-layer swaps of `base` drawn with seed seed0 + i."""
+    Lb, Eb = base.shape
+    out = np.repeat(base[None], n, axis=0).astype(np.int32)
+    for i in range(n):
+        rng = np.random.default_rng(seed0 + i)
+        ls, a, b = rng.integers(0, Lb, n_swaps), rng.integers(0, Eb, n_swaps), rng.integers(0, Eb, n_swaps)
+        c = out[i]
+        for l, x, y in zip(ls, a, b):
+            c[l, x], c[l, y] = c[l, y], c[l, x]
+    return out
+
+
+def cpu_setup(wl: int, n_tokens: int, n_chunks: int, a_tok: int, n_sample: int):
+    """The CPU legs' inputs: the oracle regenerates tokens [a_tok, a_tok + n_sample) of the SAME
+    trace in 1M-token blocks (parallel first touch, like any numba-parallel producer), and the
+    placements / cost matrices come from the committed fixture.  Returns (blocks [(t0, sel)],
+    bounds, pes, labels, fixture path)."""
     from oracle import evaluate as oe
-    pes = [oe.pe_table(p, a) for a in assigns]
-    oe.fused_pass(sel[:64], pes, bounds, E, t0)  # numba compile outside timing
-    best = float("inf")
-    for _ in range(reps):
+    from oracle import gen as og
+    labels, assigns, costs, fx = load_fixture(wl)
+    if wl == 4:
+        base = assigns[0]
+        assigns = list(perturb_swaps_np(base, 4096, 64, 1000))
+        costs = costs * len(assigns)
+        labels = [f"cand{i}" for i in range(len(assigns))]
+    pes = [oe.pe_table(p, a) for p, a in zip(costs, assigns)]
+    blocks = []
+    for s0 in range(a_tok, a_tok + n_sample, CPU_BLOCK):
+        s1 = min(s0 + CPU_BLOCK, a_tok + n_sample)
+        sel, bounds = og.generate(L, E, K, ZIPF_S, n_tokens, n_chunks, SEED, tok_range=(s0, s1))
+        blocks.append((s0, sel))
+    bounds = np.array([(c * n_tokens + n_chunks - 1) // n_chunks for c in range(n_chunks + 1)], dtype=np.int64)
+    return blocks, bounds, pes, labels, fx
+
+
+def cpu_pass(blocks, pes, bounds):
+    """One pass of the CPU restatement over the blocks: load counts [L, E] and per-chunk hop sums
+    [P, C] (oracle.evaluate.fused_pass: token blocks on all numba threads, private partials,
+    integer merge), summed over the blocks."""
+    from oracle import evaluate as oe
+    cnt, sums = None, None
+    for t0, sel in blocks:
+        c, s = oe.fused_pass(sel, pes, bounds, E, t0)
+        cnt = c if cnt is None else cnt + c
+        sums = s if sums is None else sums + s
+    return cnt, sums
+
+
+def time_cpu(blocks, pes, bounds, steps: int, warmup: int):
+    from oracle import evaluate as oe
+    oe.fused_pass(blocks[0][1][:64], pes, bounds, E, blocks[0][0])  # numba compile outside timing
+    for _ in range(warmup):
+        cpu_pass(blocks, pes, bounds)
+    ts = []
+    for _ in range(steps):
         t_a = time.perf_counter()
-        oe.fused_pass(sel, pes, bounds, E, t0)
-        best = min(best, time.perf_counter() - t_a)
-    return best
+        res = cpu_pass(blocks, pes, bounds)
+        ts.append(time.perf_counter() - t_a)
+    return float(np.mean(ts)), res
 
 
 def host_info(run_1thread) -> dict:
@@ -164,45 +248,48 @@ def cpu_threads() -> int:
         return len(os.sched_getaffinity(0))
 
 
+def cpu_leg(wl, n_total, c_total, a_tok, n_sample, steps, warmup):
+    """Shared by the reference arm and the GPU arm's cpu_baseline: the same code, input and
+    timing rule (mean over `steps` passes after `warmup`), so the two CPU numbers agree."""
+    blocks, bounds, pes, labels, fx = cpu_setup(wl, n_total, c_total, a_tok, n_sample)
+    t, res = time_cpu(blocks, pes, bounds, steps, warmup)
+    P = len(pes)
+    n1 = min(n_sample, 100_000 if wl != 4 else 500)
+    b1 = [(blocks[0][0], blocks[0][1][:n1])]
+
+    def one_thread():
+        t1, _ = time_cpu(b1, pes, bounds, 1, 0)
+        return n1 * L * P / t1
+
+    info = host_info(one_thread)
+    thr = cpu_threads()
+    d = {"value": n_sample * L * P / t, "unit": UNIT, "cores": thr, "kind": "port",
+         "sample": (f"tokens [{a_tok}, {a_tok + n_sample}) of the workload's trace, regenerated on the CPU by the "
+                    f"oracle sampler in {len(blocks)} block(s) of <= {CPU_BLOCK} tokens; counts + per-chunk hop sums "
+                    f"of the same {P} placements (fixture {fx}) in one oracle pass per block, numba parallel, "
+                    f"{thr} threads; mean of {steps} passes after {warmup} warm-up"),
+         "ms_per_pass": t * 1e3, **info, "sample_1thread": f"first {n1} tokens, 1 numba thread"}
+    return d, res, labels, bounds
+
+
 def run_reference(args, rank: int, world: int) -> None:
     """--impl reference: the reference path's CPU implementation (our oracle restatement of
-    SPEC.md; the reference ships no code) on the host cores, bounded sample per step."""
+    SPEC.md; the reference ships no code) on the host cores: the same trace (regenerated by the
+    oracle sampler), placements and topology as the GPU arm; configs 2 and 3 time all 10M tokens
+    streamed in 1M-token blocks, configs 4 and 5 a bounded sample."""
     if rank != 0:
         return
-    import numba
-    from oracle import gen as og
-    from oracle import topology as ot
-    n_sample = args.ref_tokens
-    sel, _ = og.generate(L, E, K, ZIPF_S, TOK_PER_GPU, CHUNKS_PER_GPU, SEED, tok_range=(0, n_sample))
-    bounds = np.minimum(np.array([(c * TOK_PER_GPU + CHUNKS_PER_GPU - 1) // CHUNKS_PER_GPU
-                                  for c in range(CHUNKS_PER_GPU + 1)]), n_sample)
-    # FatTree 8x4x8 server graph: servers 0..31, leaves 32..39, spines 40..43
-    links = [(s, 32 + s // 4) for s in range(32)] + [(32 + l, 40 + sp) for l in range(8) for sp in range(4)]
-    dsrv = ot.server_hops(44, links, 32)
-    dev_srv = np.repeat(np.arange(32), 8)
-    disp = np.array([(l * 256) // L for l in range(L)])
-    coll = np.concatenate([disp[1:], disp[-1:]])
-    p = ot.cost_matrix(dsrv, dev_srv, disp, coll)
-    rng = np.random.default_rng(0)
-    assigns = [np.stack([rng.permutation(256) for _ in range(L)]).astype(np.int32) for _ in range(P)]
-    threads = numba.get_num_threads()
-    time_oracle(sel[:1000], bounds, p, assigns, reps=1)
-    for _ in range(args.warmup):
-        time_oracle(sel, bounds, p, assigns, reps=1)
-    times = [time_oracle(sel, bounds, p, assigns, reps=1) for _ in range(args.steps)]
-    t = float(np.mean(times))
-    value = n_sample * L * P / t
-    n1 = min(n_sample, 100_000)
-    b1 = np.minimum(bounds, n1)
-    host = host_info(lambda: n1 * L * P / time_oracle(sel[:n1], b1, p, assigns, reps=2))
-    sample = (f"{n_sample} tokens (first {n_sample} of the config-2 trace, regenerated on the CPU), counts + "
-              f"hop sums of {P} placements per step; numba parallel, {threads} threads")
+    wl = args.workload
+    tok, n_total, c_total, scaling = shape_of(wl, world, args.tokens)
+    default = {2: tok, 3: tok, 4: 5_000, 5: 10_000_000}[wl]
+    n_sample = min(args.ref_tokens or default, tok if wl != 5 else n_total)
+    cb, _, labels, _ = cpu_leg(wl, n_total, c_total, 0, n_sample, args.steps, args.warmup)
+    P = len(labels)
+    value = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": workload(world, TOK_PER_GPU, "cpu-oracle"),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
-                             **host, "sample_1thread": f"first {n1} tokens, 1 numba thread"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_pass"], "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
+            "config": workload(wl, world, tok, n_total, P), "cpu_baseline": cb,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -242,20 +329,27 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", type=int, choices=[2, 3, 4, 5], default=2,
-                    help="BASELINE config: 2 (default, the metric's config), 3 multi-topology, 4 4096 candidates, "
-                         "5 100M tokens strong scaling")
+                    help="BASELINE config: 2 (default, the metric's config), 3 six topologies x 4 methods, 4 4096 "
+                         "candidates, 5 100M tokens strong scaling")
     ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
-    ap.add_argument("--algo", choices=["auto", "gather", "count", "factorized"], default="auto",
+    ap.add_argument("--algo", choices=["auto", "gather", "count", "seg", "token", "factorized"], default="auto",
                     help="hop-sum algorithm (include/moeplace_cuda.h MP_ALGO_*); auto = the library's choice "
                          "(config 4: factorized, as evaluate_many(method='auto') picks for P > 16)")
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (configs 2-4) / total (config 5)")
+    ap.add_argument("--chunks", type=int, default=None,
+                    help="chunks per GPU (default 150; e.g. 71429 = ~140 tokens per chunk, the paper's dialog length)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-tokens", type=int, default=None, help="cpu_baseline sample (tokens)")
-    ap.add_argument("--ref-tokens", type=int, default=1_000_000, help="--impl reference sample per step")
+    ap.add_argument("--ref-tokens", type=int, default=None, help="--impl reference sample per step")
+    ap.add_argument("--sustained-s", type=float, default=0.6, help="seconds of back-to-back steps for the sustained figure")
+    ap.add_argument("--write-fixtures", default=None, help="directory: save the placements the CPU legs use")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    global CHUNKS_PER_GPU
+    if args.chunks:
+        CHUNKS_PER_GPU = args.chunks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -312,35 +406,34 @@ def main():
         return out
 
     # ---------------- setup (untimed): trace shard, statistics, placements, tables ----------------
+    n, n_total, c_total, scaling = shape_of(wl, world, args.tokens)
+    a_tok, b_tok = rank * n, (rank + 1) * n
     if wl == 5:
-        n_total = args.tokens or 100_000_000
-        c_total = 1500
         a_tok, b_tok = (rank * n_total) // world, ((rank + 1) * n_total) // world
-        scaling = "strong"
+        n = b_tok - a_tok
     else:
-        per = args.tokens or (1_000_000 if wl == 4 else TOK_PER_GPU)
-        n_total, c_total = per * world, CHUNKS_PER_GPU * world
-        a_tok, b_tok = rank * per, (rank + 1) * per
-        scaling = "weak"
-    n = b_tok - a_tok
+        c_total = CHUNKS_PER_GPU * world
     trace = mt.generate_trace(model, ZIPF_S, n_total, c_total, SEED, tok_range=(a_tok, b_tok))
     counts0 = mt.trace_counts(trace)
     if world > 1:
         dist.all_reduce(counts0)
     freq = mt.frequencies_from_counts(counts0.cpu().numpy(), n_total, K)
+    topo_costs = []  # distinct cost matrices, in fixture order
     if wl in (2, 5):
         g, d, order, attn, cost = topology("FatTree", 8, 4, 8, {"spines": 4})
         placements = methods(freq, g, order, attn, cost)
         costs = [cost] * len(placements)
         kinds = ["FatTree 8x4x8"]
+        topo_costs = [cost]
     elif wl == 3:
         placements, costs, kinds = [], [], []
-        for kind in ("FatTree", "FatTreeHier", "Dragonfly", "DragonflySparse"):
-            g, d, order, attn, cost = topology(kind, 16, 4, 4)
+        for kind, leaves in CONFIG3_KINDS:
+            g, d, order, attn, cost = topology(kind, leaves, 4, 4)
             pls = methods(freq, g, order, attn, cost)
             placements += pls
             costs += [cost] * len(pls)
-            kinds.append(f"{kind} 16x4x4")
+            kinds.append(f"{kind} {leaves}x4x4")
+            topo_costs.append(cost)
     else:
         g, d, order, attn, cost = topology("Dragonfly", 16, 4, 4)
         base = methods(freq, g, order, attn, cost, which=("ilpload",))[0]
@@ -348,7 +441,27 @@ def main():
         placements = [mpl.Placement(cand[i], c, f"cand{i}") for i in range(cand.shape[0])]
         costs = [cost] * len(placements)
         kinds = ["Dragonfly 16x4x4"]
+        topo_costs = [cost]
     P_ = len(placements)
+
+    # the CPU legs score the same placements: save / check the committed fixture
+    fx_src = [base] if wl == 4 else placements
+    fx_topo = [0] if wl == 4 else [next(i for i, u in enumerate(topo_costs) if u is cs) for cs in costs]
+    fx = {"labels": np.array([p.label or "" for p in fx_src]),
+          "assign": np.stack([p.assign for p in fx_src]).astype(np.int16), "topo_of": np.array(fx_topo, np.int32)}
+    for i, cs in enumerate(topo_costs):
+        fx[f"p{i}"] = cs.numpy().astype(np.uint8)
+    fx_key = {2: 2, 5: 2, 3: 3, 4: 4}[wl]
+    if args.write_fixtures and rank == 0 and not (wl == 5 or args.tokens or args.chunks):
+        os.makedirs(args.write_fixtures, exist_ok=True)
+        np.savez_compressed(Path(args.write_fixtures) / f"placements_wl{fx_key}.npz", **fx)
+    fixture_match = None
+    try:
+        ref = np.load(FIXTURES / f"placements_wl{fx_key}.npz")
+        fixture_match = bool(all(np.array_equal(ref[k], fx[k]) for k in fx if k != "labels"))
+    except Exception:  # noqa: BLE001
+        fixture_match = None
+
     C = trace.n_chunks
     planes, stride = trace.planes, trace.planes.shape[1]
     t0, t1 = trace.tok_begin, trace.tok_end
@@ -376,10 +489,8 @@ def main():
     for W, _, _, _ in groups:
         views.append(sums_all[off:off + 4 * W * C])
         off += 4 * W * C
-    kev = [_events() for _ in range(2)]
-    kernel_ms = [[], []]
 
-    algo = {"auto": 0, "gather": 1, "count": 2, "factorized": 0}[args.algo]
+    algo = {"auto": 0, "gather": 1, "count": 2, "token": 3, "seg": 4, "factorized": 0}[args.algo]
     # config 4 (4096 candidates): the product path is evaluate_many(method="auto") -> factorized (one per-chunk
     # histogram pass + exact tensor-core contraction); the streaming passes are timed beside it
     fact = wl == 4 and args.algo in ("auto", "factorized")
@@ -391,103 +502,94 @@ def main():
         out_f4 = torch.zeros((P_, C), dtype=torch.int64, device=dev)
         max_chunk = int(np.max(trace.chunk_token_counts()))
         max_pe4 = max(cs.max_p for cs in costs)
-        kev_f = [_events() for _ in range(2)]
 
-    def fstep(timed: bool):
+    def fstep(hi=None):
         cnt_c4.zero_()
-        if timed:
-            kev_f[0][0].record(stream)
-        _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+        _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, hi or t1, L, K, E, _lib.ptr(bounds), C,
                   _lib.ptr(cnt_c4), _lib.ptr(err), sh)
-        if timed:
-            kev_f[0][1].record(stream)
-            kev_f[1][0].record(stream)
         out_f4.copy_(ev.contract_tc(cnt_c4, pe_all4, max_count=max_chunk, max_pe=max_pe4, err=err))
-        if timed:
-            kev_f[1][1].record(stream)
         if world > 1:
             dist.all_reduce(out_f4)
 
-    def algo_used(hist: bool, W: int) -> str:  # mirrors choose_algo in csrc/stream.cu
-        if args.algo not in ("auto", "factorized"):
-            return {"gather": "gather", "count": "count-contract"}[args.algo]
-        return "count-contract" if (hist or W > 1) else "gather"
-
-    def step(timed: bool):
+    def step(hi=None):
+        hi = hi or t1
         buf.zero_()
         if with_hist and fused:
-            if timed:
-                kev[0][0].record(stream)
             W, tables, max_p, _ = groups[0]
-            _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+            _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, hi, L, K, E, _lib.ptr(bounds), C,
                       _lib.ptr(tables), W, max_p, _lib.ptr(counts), _lib.ptr(views[0]), _lib.ptr(err), algo, sh)
-            if timed:
-                kev[0][1].record(stream)
         else:
             if with_hist:
-                if timed:
-                    kev[1][0].record(stream)
-                _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(counts), _lib.ptr(err), sh)
-                if timed:
-                    kev[1][1].record(stream)
-            if timed:
-                kev[0][0].record(stream)
+                _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, hi, L, K, E, _lib.ptr(counts), _lib.ptr(err), sh)
             for (W, tables, max_p, _), v in zip(groups, views):
-                _lib.call("mp_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C,
+                _lib.call("mp_score_ex_u8", _lib.ptr(planes), stride, t0, hi, L, K, _lib.ptr(bounds), C,
                           _lib.ptr(tables), W, max_p, _lib.ptr(v), algo, sh)
-            if timed:
-                kev[0][1].record(stream)
         if world > 1:
             dist.all_reduce(buf)
 
-    # ---------------- CPU baseline (rank 0, N=1 only) ----------------
-    cpu = None
+    def main_kernel():
+        """The step's dominant kernel alone (no zeroing, no collective): the roofline numerator."""
+        if fact:
+            _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+                      _lib.ptr(cnt_c4), _lib.ptr(err), sh)
+        elif fused:
+            W, tables, max_p, _ = groups[0]
+            _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(counts), _lib.ptr(views[0]), _lib.ptr(err), algo, sh)
+        else:
+            W, tables, max_p, _ = groups[0]
+            _lib.call("mp_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C,
+                      _lib.ptr(tables), W, max_p, _lib.ptr(views[0]), algo, sh)
+
+    def algo_used(hist: bool, W: int) -> str:
+        if fact:
+            return "factorized"
+        if args.algo != "auto":
+            return {"gather": "gather", "count": "count-contract", "seg": "segmented gather",
+                    "token": "token-tiled"}[args.algo]
+        # mirrors choose_algo in csrc/stream.cu (K = 8, max_p <= 31 here)
+        tpc = n / max(1, C)
+        seg_hi = (5000 if W == 1 else 3000 if W == 2 else 1800) if hist else (4000 if W == 1 else 6000 if W == 2 else 2500)
+        tok_lo = (70 if W == 1 else 0) if hist else (170 if W == 1 else 0)
+        if tpc < tok_lo:
+            return "token-tiled"
+        if tpc < seg_hi:
+            return "segmented gather"
+        return "count-contract" if (hist or W > 1) else "gather"
+
+    run = fstep if fact else step
+
+    # ---------------- CPU baseline + parity sample (rank 0, N=1 only; before any GPU timing) ----------------
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
         default_ns = {2: 1_000_000, 3: 250_000, 4: 2_000, 5: 1_000_000}[wl]
         ns = min(args.cpu_tokens or default_ns, n)
-        sel = cpu_sample(trace, ns)
-        bnd = np.minimum(np.asarray(trace.chunk_bounds, dtype=np.int64), ns)
-        from oracle import evaluate as oe
-        pes = []
-        cache = {}
-        for pl, cs in zip(placements, costs):
-            key = id(cs)
-            if key not in cache:
-                cache[key] = cs.numpy()
-            pes.append(oe.pe_table(cache[key], pl.assign))
-        oe.fused_pass(sel[:16], pes, bnd, E)
-        t_cpu = float("inf")
-        for _ in range(5):
-            t_a = time.perf_counter()
-            oe.fused_pass(sel, pes, bnd, E)
-            t_cpu = min(t_cpu, time.perf_counter() - t_a)
-        thr = cpu_threads()
-        cpu = {"value": ns * L * P_ / t_cpu, "unit": UNIT, "cores": thr, "kind": "port",
-               "sample": f"first {ns} tokens of the same trace (D2H copy), counts + hop sums of the same {P_} "
-                         f"placements in one pass, oracle/ numba parallel, best of 5, measured before any GPU timing",
-               "ms_per_sample": t_cpu * 1e3}
-        n1 = min(ns, 100_000 if wl != 4 else 500)
-        b1 = np.minimum(bnd, n1)
+        try:
+            cpu, (c_cnt, c_sums), _, _ = cpu_leg(wl, n_total, c_total, a_tok, ns, 3, 1)
+        except FileNotFoundError as e:  # no fixture yet (first run): nothing to compare against
+            cpu = {"value": None, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": f"unavailable: {e}"}
+        if cpu.get("value"):
+            # the same token range on the GPU, through the benched kernels (untimed): parity of the step
+            run(t0 + ns)
+            torch.cuda.synchronize()
+            if fact:
+                g_sums = out_f4.cpu().numpy()
+                ok = bool(np.array_equal(g_sums, c_sums))
+            else:
+                g_sums = np.concatenate([v.view(4 * W, C)[:np_].cpu().numpy()
+                                         for v, (W, _, _, np_) in zip(views, groups)])
+                ok = bool(np.array_equal(g_sums, c_sums))
+                if with_hist:
+                    ok = ok and bool(np.array_equal(counts.view(L, E).cpu().numpy(), c_cnt))
+            parity = {"ok": ok and fixture_match is not False, "tokens": ns, "fixture_match": fixture_match,
+                      "what": (f"{'counts + ' if with_hist else ''}per-chunk hop sums of all {P_} placements over tokens "
+                               f"[{a_tok}, {a_tok + ns}): the benched GPU kernels vs the CPU oracle on the same tokens "
+                               f"(regenerated independently on the CPU), bit-exact")}
 
-        def one_thread():
-            best = float("inf")
-            for _ in range(2):
-                t_a = time.perf_counter()
-                oe.fused_pass(sel[:n1], pes, b1, E)
-                best = min(best, time.perf_counter() - t_a)
-            return n1 * L * P_ / best
-
-        cpu.update(host_info(one_thread))
-        cpu["sample_1thread"] = f"first {n1} tokens, 1 numba thread"
-
-    launches_per_step = 1 if (fused or fact) else len(groups) + (1 if with_hist else 0)
-    run = fstep if fact else step
     # the clock poller starts before the warm-up so it is already sampling when timing begins
-    sampler = ClockSampler(local) if rank == 0 else None
-    if sampler:
-        sampler.start()
+    sampler = ClockSampler(local).start() if rank == 0 else None
     for _ in range(args.warmup):
-        run(False)
+        run()
     torch.cuda.synchronize()
     if with_hist and not torch.equal(counts.view(L, E), counts0):
         raise SystemExit("bench: histogram of the timed pass differs from the setup histogram")
@@ -497,24 +599,25 @@ def main():
     ev_a, ev_b = _events()
     ev_a.record(stream)
     for _ in range(args.steps):
-        run(False)
+        run()
     ev_b.record(stream)
     torch.cuda.synchronize()
-    for _ in range(args.steps):  # per-kernel shares with launch-bracketing events on the same stream
-        run(True)
-        torch.cuda.synchronize()
-        ke = kev_f if fact else kev
-        kernel_ms[0].append(ke[0][0].elapsed_time(ke[0][1]))
-        if fact or (with_hist and not fused):
-            kernel_ms[1].append(ke[1][0].elapsed_time(ke[1][1]))
     if world > 1:
         dist.barrier()
+    # the dominant kernel alone, back to back on the same stream (per-launch time for the roofline)
+    ka, kb = _events()
+    ka.record(stream)
+    for _ in range(args.steps):
+        main_kernel()
+    kb.record(stream)
+    torch.cuda.synchronize()
+    k_ms = ka.elapsed_time(kb) / args.steps
     if sampler and world == 1:
         # a short timed region can end before the poller has a handful of samples: keep the GPU on
         # the identical (untimed) step until it has >= 8, so the reported clocks are under this load
         extra = 0
         while len(sampler.sm) < 8 and extra < 2000:
-            run(False)
+            run()
             extra += 1
             if extra % 50 == 0:
                 torch.cuda.synchronize()
@@ -529,224 +632,141 @@ def main():
 
     # ---------------- roofline of the dominant kernel ----------------
     peak, peak_src = measured_peak()
-    k_main = float(np.mean(kernel_ms[0]))
     if fused:
-        kname, tkey, launches = ("mp_hist_score_u8 (fused hist+score of 4 placements; count-contract: histogram "
-                                 "+ per-(layer,chunk) contraction with the cost tables)"), "fused", 1
+        kname, tkey = ("mp_hist_score_u8 (fused hist+score of 4 placements; " + algo_used(True, 1) + ")"), "fused"
     elif fact:
-        kname, tkey, launches = ("mp_hist_chunks_u8 (factorized evaluator: per-chunk histogram int64 [C][L][E]; "
-                                 "the exact contraction with the 4096 pe rows runs after it as cuBLASLt int8 GEMMs)"), \
-            "hist_chunks", 1
+        kname, tkey = "mp_hist_chunks_u8 (factorized evaluator: per-chunk histogram int64 [C][L][E])", "hist_chunks"
     else:
-        Ws = sorted({W for W, _, _, _ in groups})
-        kname = f"mp_score_u8 (W={'/'.join(map(str, Ws))}, {len(groups)} launch(es) per step)"
-        tkey, launches = ("score" if Ws == [1] else f"score_w{Ws[-1]}"), len(groups)
-        if with_hist and np.mean(kernel_ms[1]) > k_main:
-            k_main, kname, tkey, launches = float(np.mean(kernel_ms[1])), "mp_hist_u8", "hist", 1
+        W0 = groups[0][0]
+        kname = f"mp_score_u8 (W={W0}, first of {len(groups)} launch(es) per step; {algo_used(False, W0)})"
+        tkey = "score" if W0 == 1 else f"score_w{W0}"
     alg_bytes = n * L * K  # one u8 id per (token, layer, pick), per launch
-    per_launch_ms = k_main / launches
-    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
     traffic = None
     try:
         tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())
         ent = tr.get(tkey, {})
-        if ent.get("tokens"):
+        if ent.get("tokens") and C == ent.get("chunks", C):
             traffic = ent["dram_bytes_per_launch"] * n / ent["tokens"]  # scaled to this launch's tokens
     except Exception:
         traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": kname, "kernel_ms_per_launch": per_launch_ms,
-                "kernel_share_of_step": k_main / ms if world == 1 else None, "alg_bytes_per_launch": alg_bytes,
-                "peak_source": peak_src}
-    if with_hist and not fused:
-        roofline["hist_ms"] = float(np.mean(kernel_ms[1]))
-    if fact:
-        roofline["contraction_ms"] = float(np.mean(kernel_ms[1]))
-    if wl in (3, 4) and not fact and algo_used(False, 4) == "gather":
-        # shared-memory roofline for the W=4 gather: 4 LDS.128 wavefronts per 32 lookups + 4 LDG wavefronts
-        # per 512 B, at 1 wavefront / SM / clock (sm_max_mhz)
-        mhz = (clocks or {}).get("sm_mhz") or 1965.0
-        lookups = n * L * K
-        wf = lookups / 32 * 4 * 4 / 4 + n * L * K / 512 * 4  # per launch group of 16 placements
-        roofline["smem_bound_ms_per_launch"] = wf / 148 / (mhz * 1e6) * 1e3
+                "traffic": traffic, "kernel": kname, "kernel_ms_per_launch": k_ms,
+                "kernel_ms_source": f"{args.steps} back-to-back launches of the kernel alone, CUDA events on its stream",
+                "kernel_share_of_step": (k_ms * (1 if fused or fact else len(groups)) / ms) if world == 1 else None,
+                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
 
-    # ---------------- each streaming kernel alone on the same trace (context for the roofline) ----------
-    kernels_alone = None
-    if wl in (2, 5) and rank == 0:
-        scratch = torch.zeros_like(buf)
-        alone = {
-            "mp_score_u8 (W=1, 4 placements)": lambda: _lib.call(
-                "mp_score_u8", _lib.ptr(planes), stride, t0, t1, L, K, _lib.ptr(bounds), C,
-                _lib.ptr(groups[0][1]), 1, groups[0][2], _lib.ptr(scratch[L * E:]), sh),
-            "mp_hist_u8": lambda: _lib.call(
-                "mp_hist_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(scratch[:L * E]), _lib.ptr(err), sh),
-            # the same fused step with the per-byte GATHER algorithm (one LDS per lookup + ATOMS), for comparison
-            "mp_hist_score_ex_u8 (GATHER, 4 placements)": lambda: _lib.call(
-                "mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
-                _lib.ptr(groups[0][1]), 1, groups[0][2], _lib.ptr(scratch[:L * E]), _lib.ptr(scratch[L * E:]),
-                _lib.ptr(err), 1, sh),
-        }
-        kernels_alone = {}
-        for nm, fn in alone.items():
-            for _ in range(3):
-                fn()
-            xa, xb = _events()
-            xa.record(stream)
-            for _ in range(10):
-                fn()
-            xb.record(stream)
-            torch.cuda.synchronize()
-            kms_ = xa.elapsed_time(xb) / 10
-            gbs = n * L * K / (kms_ / 1e3) / 1e9
-            kernels_alone[nm] = {"ms": kms_, "GBps": gbs, "frac": gbs / peak}
-        # L1TEX model (the SM's L1TEX/shared pipe moves one wavefront per clock): the step's wavefronts per
-        # launch are the shared-memory wavefronts ncu counted for the same kernel on the same trace
-        # (profiles/traffic.json, from the committed --set full capture; ATOMS + flush reads) plus one per
-        # 128 B of coalesced LDG.128; bound = wavefronts / (148 SMs x SM clock).
-        mhz = (clocks or {}).get("sm_mhz") or 1965.0
-        clk = mhz * 1e6
-        if fused:
-            try:
-                ent = json.loads((ROOT / "profiles" / "traffic.json").read_text())["fused"]
-                shw = ent["shared_wavefronts_per_launch"] * n / ent["tokens"]
-            except Exception:
-                shw = None
-            if shw:
-                ldg = n * L * K / 128
-                bound = (shw + ldg) / 148 / clk * 1e3
-                roofline["l1tex_model"] = {
-                    "shared_wavefronts_per_launch": shw, "ldg_wavefronts_per_launch": ldg,
-                    "wavefronts_per_512B": (shw + ldg) / (n * L * K / 512), "sm_mhz": mhz, "bound_ms": bound,
-                    "frac_of_l1tex_bound": bound / per_launch_ms,
-                    "shared_wavefronts_per_atoms_instr": shw / (n * L * K / 32),
-                    "source": "ncu --set full capture (profiles/r1_ncu_summary.md): "
-                              "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"}
+    # ---------------- sustained: the same step back to back for >= --sustained-s ----------------
+    sustained = None
+    if world == 1 and args.sustained_s > 0:
+        n_sus = max(args.steps, int(args.sustained_s * 1e3 / ms))
+        smp = ClockSampler(local).start()
+        sa, sb = _events()
+        sa.record(stream)
+        for i in range(n_sus):
+            run()
+            if i % 200 == 199:
+                torch.cuda.synchronize()  # bound the launch queue; the events still bracket the whole run
+        sb.record(stream)
+        torch.cuda.synchronize()
+        sclk = smp.stop()
+        s_ms = sa.elapsed_time(sb) / n_sus
+        sustained = {"steps": n_sus, "seconds": s_ms * n_sus / 1e3, "ms_per_step": s_ms,
+                     "value": n_total * L * P_ / (s_ms / 1e3),
+                     "hbm_frac": alg_bytes * (1 if fused or fact else len(groups)) / (s_ms / 1e3) / 1e9 / peak
+                     if not fact else None,
+                     "sm_mhz": sclk.get("sm_mhz"), "sm_min_mhz": sclk.get("sm_min_mhz"), "reasons": sclk.get("reasons")}
+        roofline["frac_sustained"] = sustained["hbm_frac"]
 
-    # ------- configs 2/4: the factorized evaluator beside the measured gather (not the headline) -------
-    factorized = None
+    # ------- config 4: the 256 streaming passes beside the factorized step (bit-identical check) -------
     passes = None
     if fact:
-        # the same 4096 hop sums by 256 streaming passes of 16 placements (count-contract), for comparison
         for _ in range(2):
-            step(False)
+            step()
+        torch.cuda.synchronize()
+        run()
         torch.cuda.synchronize()
         ok = torch.equal(out_f4, sums_all[:P_ * C].view(P_, C))
         pa, pb = _events()
         n_p = max(3, args.steps // 4)
         pa.record(stream)
         for _ in range(n_p):
-            step(False)
+            step()
         pb.record(stream)
         torch.cuda.synchronize()
         p_ms = pa.elapsed_time(pb) / n_p
-        passes = {"ms_per_step": p_ms, "launches_per_step": len(groups), "algorithm": algo_used(False, 4),
+        passes = {"ms_per_step": p_ms, "launches_per_step": len(groups), "algorithm": "count-contract",
                   "value": n_total * L * P_ / (p_ms / 1e3), "bit_identical_to_step": ok,
-                  "hbm_frac_per_pass": n * L * K / (p_ms / len(groups) / 1e3) / 1e9 / peak,
                   "note": "evaluate_many(method='count'): 256 mp_score_u8 W=4 passes over the resident trace"}
-    if wl == 2 or (wl == 4 and not fact):
-        cnt_c = torch.zeros((C, L * E), dtype=torch.int64, device=dev)
-        pe_all = ev.pe_matrix(placements, costs, model)
-        out_f = torch.zeros((P_, C), dtype=torch.int64, device=dev)
-
-        def fstep():
-            cnt_c.zero_()
-            _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, t1, L, K, E, _lib.ptr(bounds), C,
-                      _lib.ptr(cnt_c), _lib.ptr(err), sh)
-            out_f.copy_(ev.contract_tc(cnt_c, pe_all))
-            if with_hist:
-                torch.sum(cnt_c, 0, out=cnt_tot)  # the load histogram is the sum of the per-chunk ones
-
-        cnt_tot = torch.zeros(L * E, dtype=torch.int64, device=dev)
-        for _ in range(3):
-            fstep()
-        torch.cuda.synchronize()
-        ok = torch.equal(out_f, sums_all[:P_ * C].view(P_, C)) if world == 1 else None
-        if ok and with_hist:
-            ok = torch.equal(cnt_tot.view(L, E), counts0)
-        fa, fb = _events()
-        fa.record(stream)
-        for _ in range(args.steps):
-            fstep()
-        fb.record(stream)
-        torch.cuda.synchronize()
-        f_ms = fa.elapsed_time(fb) / args.steps
-        factorized = {"ms_per_step": f_ms, "placements_evaluated_per_s": P_ / (f_ms / 1e3),
-                      "bit_identical_to_step": ok,
-                      "note": "cross-check: per-chunk histogram materialised in HBM (mp_hist_chunks_u8, int64 [C][L][E]) "
-                              "+ exact contraction on the tensor cores (7-bit digit int8 GEMMs, cuBLASLt, int32 "
-                              "accumulation) -- the out-of-kernel form of the step's count-contract; "
-                              "same per-chunk hop sums by linearity (SPEC.md:383)"}
 
     # ---------------- e2e through the public API, host buffers ----------------
     e2e = None
     if not args.no_e2e:
-        host = trace.to_host(pin=True)
+        host_tok = trace.to_host(pin=True, layout="tokens")   # the SPEC's token-major [N, L, K] selections
+        host_pl = trace.to_host(pin=True)                      # layer planes (binary sidecar form)
         cand_host = torch.from_numpy(cand).pin_memory() if fact else None
         steps_e = max(1, args.e2e_steps if wl != 5 else 1)
 
-        def api_call():
+        def api_call(host):
             if with_hist:
                 return ev.evaluate_with_stats(host, placements, costs[0])[0].counts
             if fact:  # the candidate batch as one pinned host array, as a search loop holds it
                 return ev.evaluate_batch(host, cand_host, costs[0])  # auto -> factorized for P > 16
             return ev.score_sums(host, placements, costs)
 
-        api_call()  # warm-up
-        evs = []
-        for _ in range(steps_e):
+        def time_api(host):
+            api_call(host)  # warm-up
+            evs = []
+            res = None
+            for _ in range(steps_e):
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                a, b = _events()
+                a.record(stream)
+                res = api_call(host)  # H2D (streamed, overlapped) + device transpose + kernels + D2H + floats
+                b.record(stream)
+                torch.cuda.synchronize()
+                evs.append(a.elapsed_time(b))
+            if with_hist and world == 1 and not np.array_equal(res, counts0.cpu().numpy()):
+                raise SystemExit("bench: e2e histogram differs")
+            t_e = torch.tensor([float(np.mean(evs))], dtype=torch.float64, device=dev)
             if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            a, b = _events()
-            a.record(stream)
-            res = api_call()  # H2D (streamed, overlapped) + kernels + D2H + host floats
-            b.record(stream)
-            torch.cuda.synchronize()
-            evs.append(a.elapsed_time(b))
-        if with_hist and world == 1 and not np.array_equal(res, counts0.cpu().numpy()):
-            raise SystemExit("bench: e2e histogram differs")
-        t_e = torch.tensor([float(np.mean(evs))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-        e_ms = float(t_e.item())
-        api = ("moeplace.eval.evaluate_with_stats(trace in pinned host memory, 4 placements, cost)" if with_hist
-               else f"moeplace.eval.evaluate_batch(trace and the int32 [{P_}, L, E] candidate batch in pinned host "
-                    f"memory, method='auto' -> factorized; pe tables, contraction and per-candidate floats inside "
-                    f"the call)" if fact
-               else f"moeplace.eval.score_sums(trace in pinned host memory, {P_} placements)")
+                dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+            return float(t_e.item())
+
+        e_ms = time_api(host_tok)
+        e_ms_planes = time_api(host_pl)
+        fn = ("moeplace.eval.evaluate_with_stats(4 placements, cost)" if with_hist
+              else f"moeplace.eval.evaluate_batch(int32 [{P_}, L, E] candidate batch in pinned host memory, "
+                   "method='auto' -> factorized)" if fact
+              else f"moeplace.eval.score_sums({P_} placements)")
         e2e = {"value": n_total * L * P_ / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(n * L * K * world + (cand.nbytes if fact else 0)),
-               "d2h_bytes_per_step": int(((L * E if with_hist else 0) + P_ * C) * 8 * world), "api": api}
-        del host
+               "d2h_bytes_per_step": int(((L * E if with_hist else 0) + P_ * C) * 8 * world),
+               "api": fn + " on ActivationTrace.from_host_tokens: token-major uint8 [N, L, K] selections in pinned "
+                           "host memory, streamed in 1M-token slices and transposed into layer planes on the device",
+               "layer_planes_input": {"value": n_total * L * P_ / (e_ms_planes / 1e3), "ms_per_step": e_ms_planes,
+                                      "api": fn + " on trace.to_host(pin=True) (layer planes, binary-sidecar form)"}}
+        del host_tok, host_pl
 
     if rank == 0:
-        cfg = workload(world, n, "fused" if fused else "separate")
-        if wl != 2:
-            cfg = {"workload": {3: "config3: DeepSeek-R1 shape, 10M Zipf(1.2) tokens/GPU, 16 placements (RR, Greedy, "
-                                   "ILP, ILPLoad) x 4 topologies (FatTree, FatTreeHier, Dragonfly, DragonflySparse, "
-                                   "16x4x4 = 256 devices) scored in one W=4 pass",
-                                4: "config4: DeepSeek-R1 shape, 1M Zipf(1.2) tokens/GPU, Dragonfly 16x4x4, 4096 candidate "
-                                   "placements (ILPLoad + 64 within-layer swaps each, seeds 1000+i) scored per step "
-                                   + ("(factorized: one per-chunk histogram pass + exact int8 tensor-core contraction, "
-                                      "what evaluate_many(method='auto') runs for P > 16)" if fact
-                                      else "(256 W=4 passes)"),
-                                5: f"config5: DeepSeek-R1 shape, {n_total} Zipf(1.2) tokens total sharded over "
-                                   f"{world} GPU(s), 1500 chunks, FatTree 8x4x8; hist + score of 4 placements"}[wl],
-                   "tokens_per_gpu": n, "tokens_total": n_total, "placements": P_, "topologies": kinds,
-                   "l2": f"inputs larger than L2 ({n * L * K / 1e9:.2f} GB/GPU vs 126 MB)" if n * L * K > 126e6
-                   else f"trace {n * L * K / 1e6:.0f} MB < 126 MB L2: each step streams it {len(groups)}x; "
-                        "first pass per step from HBM, reuse from L2",
-                   "parallelism": f"token shards x{world}" + (" + 1 NCCL all_reduce" if world > 1 else "")}
-        cfg["hop_sum_algorithm"] = (algo_used(True, 1) if fused else "factorized" if fact else
-                                    "/".join(sorted({algo_used(False, W) for W, _, _, _ in groups})))
+        cfg = workload(wl, world, n, n_total, P_)
+        if args.chunks:
+            cfg["workload"] += f" [--chunks {CHUNKS_PER_GPU}: {n / C:.0f} tokens per chunk]"
+        engine = {"kernel_mode": "fused" if fused else "factorized" if fact else "separate",
+                  "hop_sum_algorithm": (algo_used(True, 1) if fused else "factorized" if fact else
+                                        "/".join(sorted({algo_used(False, W) for W, _, _, _ in groups}))),
+                  "topologies": kinds, "chunks": C}
+        launches = 1 if (fused or fact) else len(groups) + (1 if with_hist else 0)
+        if fact:
+            launches = 4  # mp_hist_chunks_u8, mp_count_digits, the int8 contraction, mp_digit_combine
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
-                "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "factorized": factorized,
-                "passes": passes,
-                "kernels_alone": kernels_alone,
-                "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
+                "config": cfg, "engine": engine, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
+                "e2e": e2e, "gpu_launches": launches * args.steps, "clocks": clocks, "sustained": sustained,
+                "passes": passes, "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
         emit(line)
     if world > 1:
         dist.destroy_process_group()
