@@ -501,13 +501,13 @@ def main():
         pe_all4 = ev.pe_matrix(placements, costs, model)
         out_f4 = torch.zeros((P_, C), dtype=torch.int64, device=dev)
         max_chunk = int(np.max(trace.chunk_token_counts()))
-        max_pe4 = max(cs.max_p for cs in costs)
 
     def fstep(hi=None):
         cnt_c4.zero_()
         _lib.call("mp_hist_chunks_u8", _lib.ptr(planes), stride, t0, hi or t1, L, K, E, _lib.ptr(bounds), C,
                   _lib.ptr(cnt_c4), _lib.ptr(err), sh)
-        out_f4.copy_(ev.contract_tc(cnt_c4, pe_all4, max_count=max_chunk, max_pe=max_pe4, err=err))
+        out_f4.zero_()
+        ev.CountDigits(cnt_c4, max_chunk, err).contract(pe_all4, out_f4)  # 8-bit count digits + tcgen05 kind::i8 GEMM
         if world > 1:
             dist.all_reduce(out_f4)
 
@@ -760,7 +760,7 @@ def main():
                   "topologies": kinds, "chunks": C}
         launches = 1 if (fused or fact) else len(groups) + (1 if with_hist else 0)
         if fact:
-            launches = 4  # mp_hist_chunks_u8, mp_count_digits, the int8 contraction, mp_digit_combine
+            launches = 3  # mp_hist_chunks_u8, mp_count_digits_u8, mp_contract_tc_u8 (tcgen05 kind::i8)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",

@@ -111,17 +111,21 @@ int mp_hist_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, i
 int mp_hist_chunks_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end, int L, int K,
                       int E, const int64_t* chunk_bounds, int C, int64_t* counts, int64_t* err, void* stream);
 int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out, void* stream);
-/* Tensor-core form of the same contraction (eval.contract_tc; the GEMMs are cuBLASLt int8 with
- * int32 accumulation, exact while LE * 127^2 < 2^31):
- * mp_count_digits: out int8 [ndig*Cp][LEp], out[(a*Cp + c)*LEp + i] = (counts[c*LE + i] >> 7a) & 127
- *   for c < C, i < LE, 0 in the padding (Cp >= C, LEp >= LE).  A count < 0 or >= 2^(7*ndig) is
- *   written as 0 and raises MP_DATA_EXPERT_RANGE in err = {1, chunk, index, count}.
- * mp_digit_combine: out[q*C + c] += sum_{a<ndig} part[q*ldp + a*Cp + c] << (shift0 + 7a), where
- *   part = int32 [P][ldp] is pe_digit @ digits^T (ldp >= ndig*Cp).                               */
-int mp_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
-                    int64_t* err, void* stream);
-int mp_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0, int64_t* out,
-                     void* stream);
+/* Tensor-core form of the same contraction (5th-generation tensor cores, tcgen05 kind::i8; no library GEMM):
+ * mp_count_digits_u8: out uint8 [C*ndig][ldd], out[(c*ndig + a)*ldd + i] = byte a of counts[c*LE + i]
+ *   (ndig in {1, 2, 4}; columns [LE, ldd) zero).  A count < 0 or >= 2^(8*ndig) is written as 0 and
+ *   raises MP_DATA_EXPERT_RANGE in err = {1, chunk, index, count}.
+ * mp_contract_tc_u8: out[q*C + c] += sum_{i<LE} pe[q*ldpe + i] * counts[c][i], exactly (int64), from
+ *   the digit operand above: ONE u8 x u8 GEMM with int32 accumulators in TMEM (TMA-fed, 128-byte
+ *   swizzled K-major tiles), stream-K over every (128-row pe tile, 128-byte k-block) unit with runs
+ *   of <= 32768 K per accumulation so every int32 partial is exact, the digits recombined in the
+ *   epilogue and added with coalesced int64 atomics.  ldpe, ldd: multiples of 16; pe, digits:
+ *   16-byte aligned.  ctas = 0: one CTA per SM; else that many CTAs (per 512-row digit tile).  Together with mp_hist_chunks_u8 this is the
+ *   factorized evaluator for any number of placements.                                            */
+int mp_count_digits_u8(const int64_t* counts, int C, int64_t LE, int ndig, int64_t ldd, uint8_t* out, int64_t* err,
+                       void* stream);
+int mp_contract_tc_u8(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig, int64_t LE,
+                      int64_t ldd, int64_t* out, int ctas, void* stream);
 
 /* ---- placement tables: Placement -> per-expert round-trip hops ---------
  * tables[((l*256 + e)*W + w)] is a u32 whose byte j is pe_q[l][e] = cost[topo_of[q]][l][assign[q][l][e]]
@@ -249,6 +253,33 @@ int mp_comm_map(const int64_t* counts, const int32_t* assign, const int32_t* dev
  * trace through double-buffered device slices while the kernels run on the previous slice.   */
 int mp_copy_planes_h2d(void* dst, int64_t dst_stride, const void* src, int64_t src_stride, int64_t width, int rows,
                        void* stream);
+
+/* ---- batched-scoring operands and the device search loop (A18) --------------------
+ * mp_pe_gather_u8: pe[q*ldpe + l*E + e] = cost[topo_of[q]][l][assign[q][l][e]] (topo_of NULL = 0),
+ *   columns [L*E, ldpe) zero; an assignment outside [0, topo_S[t]) (topo_S NULL: [0, n_dev)) raises
+ *   MP_DATA_UNPLACED err = {4, placement, l*E + e, count}.  cost uint8 [T][L][n_dev] (topologies
+ *   zero-padded to the widest), topo_S int32 [T], assign int32 [P][L][E], topo_of int32 [P].
+ * mp_perturb_pe_u8: candidate b = pe_cur with n_swaps within-layer swaps (layer l, experts x, y drawn by
+ *   Philox4x32-10 keyed by `seed`, counter (b, iter, j, 'SWAP')) -> pe_out[b*ldpe ..], the swaps
+ *   (l, x, y) -> swaps int32 [B][n_swaps][3].  Swapping two experts' devices swaps their pe bytes.
+ * mp_batch_objective: obj[b] from int64 per-chunk hop sums [B][C] and tokens [C]: kind 0 = mean hops
+ *   per token (exact total / tokens), 1 = mean + lam * population std of the per-chunk means, 2 =
+ *   the worst per-chunk mean; empty chunks skipped.
+ * mp_search_accept: best = argmin obj (lowest index on ties); if obj[best] < *cur_obj, replay its swaps
+ *   on assign int32 [L][E] and pe_cur, *cur_obj = obj[best]; history[iter] = *cur_obj and
+ *   accepted[iter] = best or -1 (all device pointers: the loop never synchronises the host).
+ * mp_objective_f64: out[q] = sum_i f[i] * pe[q*ldpe + i] (float64 f [LE], fixed reduction order) --
+ *   objective_value for float frequencies; with integer counts the exact form is
+ *   mp_contract_counts with C = 1.                                                                */
+int mp_pe_gather_u8(const uint8_t* cost, int T, int L, int n_dev, const int32_t* topo_S, const int32_t* assign,
+                    const int32_t* topo_of, int P, int E, uint8_t* pe, int64_t ldpe, int64_t* err, void* stream);
+int mp_perturb_pe_u8(const uint8_t* pe_cur, int L, int E, int B, int n_swaps, uint64_t seed, int64_t iter,
+                     uint8_t* pe_out, int64_t ldpe, int32_t* swaps, void* stream);
+int mp_batch_objective(const int64_t* sums, const int64_t* tokens, int B, int C, int kind, double lam, double* obj,
+                       void* stream);
+int mp_search_accept(const double* obj, int B, const int32_t* swaps, int n_swaps, int E, int32_t* assign,
+                     uint8_t* pe_cur, double* cur_obj, double* history, int64_t iter, int64_t* accepted, void* stream);
+int mp_objective_f64(const double* f, const uint8_t* pe, int64_t ldpe, int64_t LE, int P, double* out, void* stream);
 
 /* ---- token-major ingestion (an ActivationTrace is per token) --------------------
  * planes[l][(tok_out + i)*K + k] = tokens[(i*L + l)*K + k] for i < n: the device transpose of a

@@ -7,6 +7,7 @@ operations raise ``RuntimeError`` instead of silently computing on the host.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
@@ -14,6 +15,8 @@ import numpy as np
 from .errors import ConfigError, MoeplaceError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmoeplace_cuda.so"
+if os.environ.get("MOEPLACE_EXPERIMENT_LIB"):  # tools/ only: an experimental build of the same sources
+    LIB_PATH = Path(os.environ["MOEPLACE_EXPERIMENT_LIB"])
 
 _p = C.c_void_p
 _i32, _i64, _u64, _dbl = C.c_int, C.c_int64, C.c_uint64, C.c_double
@@ -32,8 +35,8 @@ SIGNATURES = {
     "mp_hist_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p]),
     "mp_hist_chunks_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _p, _p]),
     "mp_contract_counts": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
-    "mp_count_digits": (_i32, [_p, _i32, _i64, _i32, _i32, _i64, _p, _p, _p]),
-    "mp_digit_combine": (_i32, [_p, _i32, _i64, _i32, _i32, _i32, _i32, _p, _p]),
+    "mp_count_digits_u8": (_i32, [_p, _i32, _i64, _i32, _i64, _p, _p, _p]),
+    "mp_contract_tc_u8": (_i32, [_p, _i32, _i64, _p, _i32, _i32, _i64, _i64, _p, _i32, _p]),
     "mp_pack_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _i32, _p, _p]),
     "mp_score_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p]),
     "mp_token_hops_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p]),
@@ -49,6 +52,11 @@ SIGNATURES = {
     "mp_coeffs": (_i32, [_p, _i64, _p, _i32, _i32, _i32, _dbl, _p, _p, _p]),
     "mp_comm_map": (_i32, [_p, _p, _p, _p, _i32, _p, _p, _i32, _i32, _i32, _p, _p, _p]),
     "mp_copy_planes_h2d": (_i32, [_p, _i64, _p, _i64, _i64, _i32, _p]),
+    "mp_pe_gather_u8": (_i32, [_p, _i32, _i32, _i32, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p]),
+    "mp_perturb_pe_u8": (_i32, [_p, _i32, _i32, _i32, _i32, _u64, _i64, _p, _i64, _p, _p]),
+    "mp_batch_objective": (_i32, [_p, _p, _i32, _i32, _i32, _dbl, _p, _p]),
+    "mp_search_accept": (_i32, [_p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i64, _p, _p]),
+    "mp_objective_f64": (_i32, [_p, _p, _i64, _i64, _i32, _p, _p]),
     "mp_tokens_to_planes_u8": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _i64, _p]),
     "mp_solve_mcf": (_i32, [_p, _p, _i32, _i32, _i32, _i32, _i32, _p, _p, _p]),
 }
@@ -118,6 +126,13 @@ def ptr(x):
         raise ConfigError("expected a CUDA tensor")
     if not x.is_contiguous():
         raise ConfigError("expected a contiguous tensor")
+    return C.c_void_p(x.data_ptr())
+
+
+def ptr_any(x):
+    """Device pointer of a CUDA tensor whose layout the callee describes itself (pitch argument)."""
+    if not x.is_cuda:
+        raise ConfigError("expected a CUDA tensor")
     return C.c_void_p(x.data_ptr())
 
 

@@ -39,10 +39,22 @@ cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0
                                const int64_t* bounds, int C, int64_t* counts, int64_t* err, cudaStream_t s);
 cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int P, int64_t LE, int64_t* out,
                             cudaStream_t s);
-cudaError_t launch_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
-                                int64_t* err, cudaStream_t s);
-cudaError_t launch_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0,
-                                 int64_t* out, cudaStream_t s);
+cudaError_t launch_count_digits_u8(const int64_t* counts, int C, int64_t LE, int ndig, int64_t ldd, uint8_t* out,
+                                   int64_t* err, cudaStream_t s);
+cudaError_t launch_contract_tc(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig,
+                               int64_t LE, int64_t ldd, int64_t* out, int ctas, cudaStream_t s);
+cudaError_t launch_pe_gather(const uint8_t* cost, int T, int L, int S, const int32_t* topo_S, const int32_t* assign,
+                             const int32_t* topo_of, int P, int E, uint8_t* pe, int64_t ldpe, int64_t* err,
+                             cudaStream_t s);
+cudaError_t launch_perturb_pe(const uint8_t* pe_cur, int L, int E, int B, int n_swaps, uint64_t seed, int64_t iter,
+                              uint8_t* pe_out, int64_t ldpe, int32_t* swaps, cudaStream_t s);
+cudaError_t launch_batch_objective(const int64_t* sums, const int64_t* tokens, int B, int C, int kind, double lam,
+                                   double* obj, cudaStream_t s);
+cudaError_t launch_accept(const double* obj, int B, const int32_t* swaps, int n_swaps, int E, int32_t* assign,
+                          uint8_t* pe_cur, double* cur_obj, double* history, int64_t iter, int64_t* accepted,
+                          cudaStream_t s);
+cudaError_t launch_objective_f64(const double* f, const uint8_t* pe, int64_t ldpe, int64_t LE, int P, double* out,
+                                 cudaStream_t s);
 cudaError_t launch_tokens_to_planes(const uint8_t* tok, int64_t n, int L, int K, uint8_t* planes, int64_t stride,
                                     int64_t t_out, cudaStream_t s);
 cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K,
@@ -122,18 +134,20 @@ int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, i
   return status(mp::launch_contract(counts, C, pe, P, LE, out, S(stream)));
 }
 
-int mp_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
-                    int64_t* err, void* stream) {
-  if (!counts || !out || !err || C <= 0 || LE <= 0 || Cp < C || LEp < LE || ndig < 1 || ndig > 8) return MP_ERR_ARG;
-  return status(mp::launch_count_digits(counts, C, LE, ndig, Cp, LEp, out, err, S(stream)));
+int mp_count_digits_u8(const int64_t* counts, int C, int64_t LE, int ndig, int64_t ldd, uint8_t* out, int64_t* err,
+                       void* stream) {
+  if (!counts || !out || !err || C <= 0 || C > 65535 || LE <= 0 || ldd < LE || (ldd & 15) || !aligned16(out) || (ndig != 1 && ndig != 2 && ndig != 4))
+    return MP_ERR_ARG;
+  return status(mp::launch_count_digits_u8(counts, C, LE, ndig, ldd, out, err, S(stream)));
 }
 
-int mp_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0, int64_t* out,
-                     void* stream) {
-  if (!part || !out || P <= 0 || C <= 0 || Cp < C || ndig < 1 || ldp < (int64_t)ndig * Cp || shift0 < 0 ||
-      shift0 + 7 * ndig > 63)
-    return MP_ERR_ARG;
-  return status(mp::launch_digit_combine(part, P, ldp, C, Cp, ndig, shift0, out, S(stream)));
+int mp_contract_tc_u8(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig, int64_t LE,
+                      int64_t ldd, int64_t* out, int ctas, void* stream) {
+  if (!pe || !digits || !out || P <= 0 || C <= 0 || LE <= 0 || ctas < 0) return MP_ERR_ARG;
+  if (ndig != 1 && ndig != 2 && ndig != 4) return MP_ERR_ARG;
+  if (ldpe < LE || ldd < LE || (ldpe & 15) || (ldd & 15) || !aligned16(pe) || !aligned16(digits)) return MP_ERR_ARG;
+  if ((int64_t)C * ndig > (1 << 24)) return MP_ERR_UNSUPPORTED;
+  return status(mp::launch_contract_tc(pe, P, ldpe, digits, C, ndig, LE, ldd, out, ctas, S(stream)));
 }
 
 int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P, int L, int E,
@@ -308,6 +322,41 @@ int mp_tokens_to_planes_u8(const uint8_t* tokens, int64_t n, int L, int K, uint8
   if (!tokens || !planes || n < 0 || L <= 0 || K <= 0 || tok_out < 0) return MP_ERR_ARG;
   if (!aligned16(planes) || (plane_stride & 15) != 0 || plane_stride < (tok_out + n) * (int64_t)K) return MP_ERR_ARG;
   return status(mp::launch_tokens_to_planes(tokens, n, L, K, planes, plane_stride, tok_out, S(stream)));
+}
+
+int mp_pe_gather_u8(const uint8_t* cost, int T, int L, int n_dev, const int32_t* topo_S, const int32_t* assign,
+                    const int32_t* topo_of, int P, int E, uint8_t* pe, int64_t ldpe, int64_t* err, void* stream) {
+  if (!cost || !assign || !pe || !err || T <= 0 || L <= 0 || n_dev <= 0 || P <= 0 || E <= 0 || P > 65535)
+    return MP_ERR_ARG;
+  if (ldpe < (int64_t)L * E) return MP_ERR_ARG;
+  return status(mp::launch_pe_gather(cost, T, L, n_dev, topo_S, assign, topo_of, P, E, pe, ldpe, err, S(stream)));
+}
+
+int mp_perturb_pe_u8(const uint8_t* pe_cur, int L, int E, int B, int n_swaps, uint64_t seed, int64_t iter,
+                     uint8_t* pe_out, int64_t ldpe, int32_t* swaps, void* stream) {
+  if (!pe_cur || !pe_out || !swaps || L <= 0 || E <= 0 || B <= 0 || n_swaps < 1 || iter < 0) return MP_ERR_ARG;
+  if (ldpe < (int64_t)L * E || (ldpe & 15) || !aligned16(pe_cur) || !aligned16(pe_out)) return MP_ERR_ARG;
+  return status(mp::launch_perturb_pe(pe_cur, L, E, B, n_swaps, seed, iter, pe_out, ldpe, swaps, S(stream)));
+}
+
+int mp_batch_objective(const int64_t* sums, const int64_t* tokens, int B, int C, int kind, double lam, double* obj,
+                       void* stream) {
+  if (!sums || !tokens || !obj || B <= 0 || C <= 0 || kind < 0 || kind > 2) return MP_ERR_ARG;
+  return status(mp::launch_batch_objective(sums, tokens, B, C, kind, lam, obj, S(stream)));
+}
+
+int mp_search_accept(const double* obj, int B, const int32_t* swaps, int n_swaps, int E, int32_t* assign,
+                     uint8_t* pe_cur, double* cur_obj, double* history, int64_t iter, int64_t* accepted, void* stream) {
+  if (!obj || !swaps || !assign || !pe_cur || !cur_obj || !history || !accepted || B <= 0 || n_swaps < 1 || E <= 0 ||
+      iter < 0)
+    return MP_ERR_ARG;
+  return status(mp::launch_accept(obj, B, swaps, n_swaps, E, assign, pe_cur, cur_obj, history, iter, accepted,
+                                  S(stream)));
+}
+
+int mp_objective_f64(const double* f, const uint8_t* pe, int64_t ldpe, int64_t LE, int P, double* out, void* stream) {
+  if (!f || !pe || !out || LE <= 0 || ldpe < LE || P <= 0) return MP_ERR_ARG;
+  return status(mp::launch_objective_f64(f, pe, ldpe, LE, P, out, S(stream)));
 }
 
 }  // extern "C"

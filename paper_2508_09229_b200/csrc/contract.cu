@@ -27,7 +27,6 @@ namespace {
 constexpr int kBM = 128;               // pe rows per tile (MMA M)
 constexpr int kBK = 128;               // K bytes per stage (one 128-byte swizzle row)
 constexpr int kMaxStages = 8;
-constexpr int kTcThreads = 128;
 constexpr int kSmemLimit = 232448;     // 227 KB opt-in per CTA
 constexpr int kMaxKPerSplit = 32768;   // int32 exactness bound: 65025 * 32768 < 2^31
 
@@ -82,40 +81,72 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+template <int ND>
+__device__ __forceinline__ void stage_values(const uint32_t (&v)[16], int64_t* row) {
+#pragma unroll
+  for (int j = 0; j < 16 / ND; ++j) {
+    int64_t val = 0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) val += (int64_t)v[j * ND + d] << (8 * d);
+    row[j] = val;
+  }
+}
+
 struct TcArgs {
   int P, C, ndig, n_cols;   // n_cols = C * ndig rows of the digit operand
   int NT;                   // digit rows per CTA (multiple of 16, <= 512)
-  int kblocks, kb_per_split, stages, box_rows, n_loads;
+  int kblocks, m_tiles;     // k-blocks of 128 B per row; 128-row tiles of pe
+  int64_t units;            // m_tiles * kblocks (unit = one k-block of one pe tile), split evenly over gridDim.x
+  int max_seg;              // k-blocks one accumulation may span (int32 exactness: 256)
+  int stages, box_rows, n_loads;
   uint32_t tmem_cols;
   int64_t* out;
 };
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+// Stream-K work split: CTA i owns units [i*U/G, (i+1)*U/G) of the (tile, k-block) sequence; a run of
+// units of one pe tile (at most max_seg long) accumulates in TMEM and is flushed by one epilogue.
+struct Seg {
+  int64_t u, end;
+  __device__ bool next(const TcArgs& a, int64_t u1, int64_t* s0, int64_t* s1) {
+    if (u >= u1) return false;
+    const int64_t tile_end = (u / a.kblocks + 1) * a.kblocks;
+    *s0 = u;
+    *s1 = min(min(u1, tile_end), u + a.max_seg);
+    u = *s1;
+    return true;
+  }
+};
+
+constexpr int kEpiWarps = 4;                  // warps 0-3: epilogue (TMEM lane quadrants 0-3)
+constexpr int kTcThreads2 = 32 * (kEpiWarps + 2);  // + warp 4: TMA producer, warp 5: MMA issuer
+constexpr int kEpiTileBytes = 32 * 17 * 8;    // per warp: 32 rows x <= 16 int64 values, pitch 17
+
+__global__ void __launch_bounds__(kTcThreads2, 1)
     contract_tc_kernel(const __grid_constant__ CUtensorMap tm_pe, const __grid_constant__ CUtensorMap tm_dig, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[2 * kMaxStages + 1];
+  __shared__ __align__(8) uint64_t bars[2 * kMaxStages + 2];
   __shared__ uint32_t tmem_slot;
   const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.stages;
-  const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)a.NT * kBK, stage_bytes = a_bytes + b_bytes;
-  const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[kMaxStages]), done = smem_addr(&bars[2 * kMaxStages]);
-  const int m0 = blockIdx.x * kBM;
-  const int n0 = blockIdx.y * a.NT;                          // first digit row of this CTA
-  const int kb0 = blockIdx.z * a.kb_per_split;
-  const int kb1 = min(a.kblocks, kb0 + a.kb_per_split);
+  const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)a.n_loads * a.box_rows * kBK, stage_bytes = a_bytes + b_bytes;
+  const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[kMaxStages]);
+  const uint32_t tmem_full = smem_addr(&bars[2 * kMaxStages]), tmem_empty = smem_addr(&bars[2 * kMaxStages + 1]);
+  const int n0 = blockIdx.y * a.NT;  // first digit row of this CTA's N tile
+  const int64_t u0 = blockIdx.x * a.units / gridDim.x, u1 = (blockIdx.x + 1) * a.units / gridDim.x;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 4 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(done, 1);
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_pe)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dig)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == 5) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
                  "r"(a.tmem_cols)
                  : "memory");
@@ -126,77 +157,127 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
 
-  if (warp == 0 && lane == 0) {  // ---- TMA producer ----
-    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-      const int s = i % S;
-      if (i >= S) mbar_wait(empty0 + 8 * s, ((i / S) - 1) & 1);
-      const uint32_t dst = base + (uint32_t)s * stage_bytes;
-      mbar_expect_tx(full0 + 8 * s, a_bytes + (uint32_t)a.n_loads * a.box_rows * kBK);
-      tma_load_2d(dst, &tm_pe, kb * kBK, m0, full0 + 8 * s);
-      for (int j = 0; j < a.n_loads; ++j)
-        tma_load_2d(dst + a_bytes + (uint32_t)j * a.box_rows * kBK, &tm_dig, kb * kBK, n0 + j * a.box_rows,
-                    full0 + 8 * s);
+  if (warp == 4) {  // ---- TMA producer ----
+    if (lane == 0) {
+      int i = 0;
+      for (int64_t u = u0; u < u1; ++u, ++i) {
+        const int s = i % S;
+        if (i >= S) mbar_wait(empty0 + 8 * s, ((i / S) - 1) & 1);
+        const int m0 = (int)(u / a.kblocks) * kBM, kb = (int)(u % a.kblocks);
+        const uint32_t dst = base + (uint32_t)s * stage_bytes;
+        mbar_expect_tx(full0 + 8 * s, stage_bytes);
+        tma_load_2d(dst, &tm_pe, kb * kBK, m0, full0 + 8 * s);
+        for (int j = 0; j < a.n_loads; ++j)
+          tma_load_2d(dst + a_bytes + (uint32_t)j * a.box_rows * kBK, &tm_dig, kb * kBK, n0 + j * a.box_rows,
+                      full0 + 8 * s);
+      }
     }
-  } else if (warp == 1 && lane == 0) {  // ---- MMA issuer (one thread) ----
-    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-      const int s = i % S;
-      mbar_wait(full0 + 8 * s, (i / S) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sa = base + (uint32_t)s * stage_bytes, sb = sa + a_bytes;
+  } else if (warp == 5) {  // ---- MMA issuer (one thread) ----
+    if (lane == 0) {
+      Seg sg{u0, u1};
+      int64_t s0, s1;
+      int i = 0, seg = 0;
+      while (sg.next(a, u1, &s0, &s1)) {
+        if (seg > 0) mbar_wait(tmem_empty, (seg - 1) & 1);  // the epilogue has drained the accumulators
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int64_t u = s0; u < s1; ++u, ++i) {
+          const int s = i % S;
+          mbar_wait(full0 + 8 * s, (i / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = base + (uint32_t)s * stage_bytes, sb = sa + a_bytes;
 #pragma unroll
-      for (int k = 0; k < kBK / 32; ++k) {
-        for (int j = 0; j * 256 < a.NT; ++j) {
-          const int nj = min(256, a.NT - 256 * j);
-          mma_i8(tmem + 256 * j, sw128_desc(sa + 32 * k), sw128_desc(sb + (uint32_t)j * 256 * kBK + 32 * k), idesc_i8(nj),
-                 (i > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < kBK / 32; ++k) {
+            for (int j = 0; j * 256 < a.NT; ++j) {
+              const int nj = min(256, a.NT - 256 * j);
+#ifdef MP_TC_EXPERIMENT_NO_MMA
+              if (u >= 0) continue;
+#endif
+              mma_i8(tmem + 256 * j, sw128_desc(sa + 32 * k), sw128_desc(sb + (uint32_t)j * 256 * kBK + 32 * k),
+                     idesc_i8(nj), (u > s0 || k > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(empty0 + 8 * s);  // the slot is free once these MMAs have read it
         }
+        mma_commit(tmem_full);
+        ++seg;
       }
-      mma_commit(empty0 + 8 * s);  // the slot is free once these MMAs have read it
     }
-    mma_commit(done);
-  }
-  __syncwarp();
-  // ---- epilogue: TMEM -> registers -> digit recombine -> int64 atomics ----
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + warp * 32 + lane;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const int nd = a.ndig;
-  for (int c0 = 0; c0 < a.NT; c0 += 16) {
-    uint32_t v[16];
-    tmem_ld16(trow + c0, v);
-    if (row < a.P) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j % nd) continue;  // nd in {1, 2, 4} divides 16: column j starts a chunk's digit group
-        const int n = n0 + c0 + j;
-        if (n >= a.n_cols) break;
-        int64_t val = 0;
-        for (int d = 0; d < nd; ++d) val += (int64_t)v[j + d] << (8 * d);
-        if (val) atomic_add_i64(a.out + (int64_t)row * a.C + n / nd, val);
+  } else {  // ---- epilogue warps 0-3: TMEM -> registers -> digit recombine -> coalesced int64 atomics ----
+    uint8_t* tile = smem_raw + (base - smem_addr(smem_raw)) + (uint32_t)S * stage_bytes + warp * kEpiTileBytes;
+    int64_t* t64 = reinterpret_cast<int64_t*>(tile);
+    const int nd = a.ndig, V = 16 / nd;  // chunk values per 16 columns
+    Seg sg{u0, u1};
+    int64_t s0, s1;
+    int seg = 0;
+    while (sg.next(a, u1, &s0, &s1)) {
+      mbar_wait(tmem_full, seg & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row0 = (int)(s0 / a.kblocks) * kBM + warp * 32;
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+      for (int c0 = 0; c0 < a.NT; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(trow + c0, v);
+        if (c0 + 16 >= a.NT) {  // last TMEM read of this segment: hand the accumulators back
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tmem_empty) : "memory");
+        }
+        // digit recombine: value j of this row = sum_d v[j*nd + d] << 8d, staged as tile[row][j]
+        if (nd == 1) stage_values<1>(v, t64 + lane * 17);
+        else if (nd == 2) stage_values<2>(v, t64 + lane * 17);
+        else stage_values<4>(v, t64 + lane * 17);
+        __syncwarp();
+        // write-out: instruction r covers rows 32/V * r .. and V consecutive chunks per row
+        const int cbase = (n0 + c0) / nd;
+        for (int r = 0; r < V; ++r) {
+          const int idx = r * 32 + lane;
+          const int rr = idx / V, j = idx % V;
+          const int row = row0 + rr, ch = cbase + j;
+          const int64_t val = t64[rr * 17 + j];
+#ifdef MP_TC_EXPERIMENT_NO_ATOMICS
+          if (val == 0x7fffffffffffll) a.out[0] = val;
+#else
+          if (val && row < a.P && ch < a.C && (n0 + c0) + j * nd < a.n_cols)
+            atomic_add_i64(a.out + (int64_t)row * a.C + ch, val);
+#endif
+        }
+        __syncwarp();
       }
+      ++seg;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 2)
+  if (warp == 5)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
 }
 
+// out[(c*ndig + a)*ldd + i] = byte a of counts[c*LE + i]; columns [LE, ldd) are zero.  One thread per
+// 8 consecutive columns of one chunk row (blockIdx.y = chunk): eight int64 loads, ndig u64 stores.
 __global__ void count_digits_u8_kernel(const int64_t* __restrict__ counts, int C, int64_t LE, int ndig, int64_t ldd,
                                        uint8_t* __restrict__ out, int64_t* err) {
-  // out[(c*ndig + a)*ldd + i] = byte a of counts[c*LE + i]; columns [LE, ldd) are zero
-  const int64_t n = (int64_t)C * ldd;
+  const int c = blockIdx.y;
   const int sh = 8 * ndig;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(j / ldd);
-    const int64_t i = j - (int64_t)c * ldd;
-    int64_t v = i < LE ? counts[(int64_t)c * LE + i] : 0;
-    if (v < 0 || (sh < 64 && (v >> sh) != 0)) {
-      report_err(err, MP_DATA_EXPERT_RANGE, c, i);
-      v = 0;
+  const int64_t* row = counts + (int64_t)c * LE;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i0 < ldd;
+       i0 += (int64_t)gridDim.x * blockDim.x * 8) {
+    uint64_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t i = i0 + k;
+      int64_t v = i < LE ? __ldg(row + i) : 0;
+      if (v < 0 || (sh < 64 && (v >> sh) != 0)) {
+        report_err(err, MP_DATA_EXPERT_RANGE, c, i);
+        v = 0;
+      }
+#pragma unroll
+      for (int d = 0; d < 4; ++d) w[d] |= (uint64_t)((v >> (8 * d)) & 0xff) << (8 * k);
     }
-    for (int d = 0; d < ndig; ++d) out[((int64_t)c * ndig + d) * ldd + i] = (uint8_t)(v >> (8 * d));
+    if (i0 + 8 <= ldd) {  // ldd is a multiple of 16: every 8-column group is whole
+#pragma unroll
+      for (int d = 0; d < 4; ++d)
+        if (d < ndig) *reinterpret_cast<uint64_t*>(out + ((int64_t)c * ndig + d) * ldd + i0) = w[d];
+    }
   }
 }
 
@@ -228,15 +309,14 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uin
 
 cudaError_t launch_count_digits_u8(const int64_t* counts, int C, int64_t LE, int ndig, int64_t ldd, uint8_t* out,
                                    int64_t* err, cudaStream_t s) {
-  const int64_t n = (int64_t)C * ldd;
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  count_digits_u8_kernel<<<grid, 256, 0, s>>>(counts, C, LE, ndig, ldd, out, err);
+  const int gx = (int)std::min<int64_t>((ldd / 8 + 127) / 128, 64);
+  count_digits_u8_kernel<<<dim3(gx, C), 128, 0, s>>>(counts, C, LE, ndig, ldd, out, err);
   return cudaGetLastError();
 }
 
-// splits: 0 = choose (fill the SMs), else the split-K factor
+// ctas: 0 = one CTA per SM (stream-K over every (pe tile, k-block) unit), else that many CTAs per N tile
 cudaError_t launch_contract_tc(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig,
-                               int64_t LE, int64_t ldd, int64_t* out, int splits, cudaStream_t s) {
+                               int64_t LE, int64_t ldd, int64_t* out, int ctas, cudaStream_t s) {
   if (P <= 0 || C <= 0 || LE <= 0) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -253,25 +333,24 @@ cudaError_t launch_contract_tc(const uint8_t* pe, int P, int64_t ldpe, const uin
   a.box_rows = ((a.NT + a.n_loads - 1) / a.n_loads + 7) / 8 * 8;
   a.tmem_cols = a.NT <= 32 ? 32 : a.NT <= 64 ? 64 : a.NT <= 128 ? 128 : a.NT <= 256 ? 256 : 512;
   a.kblocks = (int)((LE + kBK - 1) / kBK);
-  const int m_tiles = (P + kBM - 1) / kBM;
-  int sp = splits > 0 ? splits : std::max(1, sms / (m_tiles * n_tiles));
-  sp = std::min(sp, a.kblocks);
-  a.kb_per_split = (a.kblocks + sp - 1) / sp;
-  a.kb_per_split = std::min(a.kb_per_split, kMaxKPerSplit / kBK);
-  sp = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
+  a.m_tiles = (P + kBM - 1) / kBM;
+  a.units = (int64_t)a.m_tiles * a.kblocks;
+  a.max_seg = kMaxKPerSplit / kBK;
+  int64_t g = ctas > 0 ? ctas : std::max(1, sms / n_tiles);
+  g = std::min(g, a.units);
   const int stage_bytes = kBM * kBK + a.n_loads * a.box_rows * kBK;
-  a.stages = std::min(kMaxStages, (kSmemLimit - 1024) / stage_bytes);
+  const int epi_bytes = kEpiWarps * kEpiTileBytes;
+  a.stages = std::min(kMaxStages, (kSmemLimit - 2048 - epi_bytes) / stage_bytes);
   if (a.stages < 2) return cudaErrorInvalidValue;
   a.out = out;
   CUtensorMap tm_pe, tm_dig;
   if (!make_map(&tm_pe, pe, (uint64_t)LE, (uint64_t)P, (uint64_t)ldpe, kBM)) return cudaErrorInvalidValue;
   if (!make_map(&tm_dig, digits, (uint64_t)LE, (uint64_t)a.n_cols, (uint64_t)ldd, (uint32_t)a.box_rows))
     return cudaErrorInvalidValue;
-  const int smem = a.stages * stage_bytes + 1024;
+  const int smem = a.stages * stage_bytes + epi_bytes + 1024;
   cudaError_t e = cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  contract_tc_kernel<<<dim3((unsigned)m_tiles, (unsigned)n_tiles, (unsigned)sp), kTcThreads, smem, s>>>(tm_pe, tm_dig,
-                                                                                                       a);
+  contract_tc_kernel<<<dim3((unsigned)g, (unsigned)n_tiles), kTcThreads2, smem, s>>>(tm_pe, tm_dig, a);
   return cudaGetLastError();
 }
 

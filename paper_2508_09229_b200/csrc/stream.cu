@@ -676,56 +676,6 @@ cudaError_t launch_contract(const int64_t* counts, int C, const uint8_t* pe, int
   return cudaGetLastError();
 }
 
-// ---- tensor-core contraction operands (factorized evaluator, eval.contract_tc) ----
-// Digit planes of the per-chunk counts for exact int8 GEMMs: out is int8 [ndig * Cp][LEp], row
-// a*Cp + c holds digit a (7 bits) of counts[c][.], zero in the padding rows/columns, so one GEMM
-// against pe [P][LEp] yields every digit's partial sums side by side (N = ndig * Cp).  A count
-// that needs more than ndig digits (or is negative) is reported, never truncated silently.
-__global__ void count_digits_kernel(const int64_t* __restrict__ counts, int C, int64_t LE, int ndig, int Cp,
-                                    int64_t LEp, int8_t* __restrict__ out, int64_t* err) {
-  const int64_t n = (int64_t)Cp * LEp;
-  const int64_t lim = (int64_t)1 << (7 * ndig);
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(k / LEp);
-    const int64_t i = k - (int64_t)c * LEp;
-    int64_t v = (c < C && i < LE) ? __ldg(counts + (int64_t)c * LE + i) : 0;
-    if (v < 0 || v >= lim) {
-      report_err(err, MP_DATA_EXPERT_RANGE, c, (int)(i < 0x7fffffff ? i : 0x7fffffff), v);
-      v = 0;
-    }
-    for (int a = 0; a < ndig; ++a) out[((int64_t)a * Cp + c) * LEp + i] = (int8_t)((v >> (7 * a)) & 127);
-  }
-}
-
-// out[q*C + c] += sum_a part[q*ldp + a*Cp + c] << (shift0 + 7a): recombines the int32 digit GEMM
-// partials (exact: each partial < 2^31) into the int64 hop sums.
-__global__ void digit_combine_kernel(const int32_t* __restrict__ part, int P, int64_t ldp, int C, int Cp, int ndig,
-                                     int shift0, int64_t* __restrict__ out) {
-  const int64_t n = (int64_t)P * C;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(k / C), c = (int)(k - (int64_t)q * C);
-    int64_t v = 0;
-    for (int a = 0; a < ndig; ++a) v += (int64_t)__ldg(part + q * ldp + (int64_t)a * Cp + c) << (shift0 + 7 * a);
-    out[k] += v;
-  }
-}
-
-cudaError_t launch_count_digits(const int64_t* counts, int C, int64_t LE, int ndig, int Cp, int64_t LEp, int8_t* out,
-                                int64_t* err, cudaStream_t s) {
-  const int64_t n = (int64_t)Cp * LEp;
-  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  count_digits_kernel<<<grid, 256, 0, s>>>(counts, C, LE, ndig, Cp, LEp, out, err);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_digit_combine(const int32_t* part, int P, int64_t ldp, int C, int Cp, int ndig, int shift0,
-                                 int64_t* out, cudaStream_t s) {
-  const int64_t n = (int64_t)P * C;
-  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  digit_combine_kernel<<<grid, 256, 0, s>>>(part, P, ldp, C, Cp, ndig, shift0, out);
-  return cudaGetLastError();
-}
-
 // Which exact algorithm computes the hop sums: the per-byte gather costs one LDS per
 // lookup (1/2/4 wavefronts per 32 lookups for W = 1/2/4) on top of the histogram's ATOMS when both are
 // needed; count-contract costs only the histogram.  Measured (R1, 10M tokens): gather W=1 0.80 ms,

@@ -180,12 +180,7 @@ def _assign_to_device(placements: Sequence[Placement], costs: Sequence[CostMatri
                                     f"{costs[i].S} devices)")  # checked before narrowing to int32
             np.copyto(host[i], a, casting="unsafe")
         out = buf[:P * L * E].to(dev, non_blocking=True).view(P, L, E)
-        flat = out.view(P, -1)
-        S = t.as_tensor(np.asarray([c.S for c in costs], dtype=np.int32), device=dev)
-        bad = (flat.amin(1) < 0) | (flat.amax(1) >= S)
-        first = int(t.nonzero(bad)[0, 0]) if bool(bad.any()) else -1  # syncs: the staging buffer is free again
-    if first >= 0:
-        raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {first}, {costs[first].S} devices)")
+        t.cuda.current_stream().synchronize()  # the staging buffer is free again
     return out
 
 
@@ -267,83 +262,103 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, a
 
 def pe_matrix(placements: Sequence[Placement], costs, model: ModelSpec):
     """uint8 [P, L*E] per-expert round-trip costs pe_q[l, e] = p_q[l, assign_q[l, e]] on the device
-    (one batched gather per distinct cost matrix)."""
+    (``mp_pe_gather_u8``; rows padded to a 16-byte pitch, the returned tensor is the [P, L*E] view)."""
     placements = list(placements)
     costs = _as_costs(costs, len(placements))
-    return _pe_from_device_assign(_assign_to_device(placements, costs, model).long(), costs, model)
+    return _pe_from_device_assign(_assign_to_device(placements, costs, model), costs, model)
 
 
 def _pe_from_device_assign(assign, costs: Sequence[CostMatrix], model: ModelSpec):
-    """pe uint8 [P, L*E] from checked device assignments int64 [P, L, E]."""
+    """pe uint8 [P, L*E] (a view of a [P, ldpe] buffer, ldpe = L*E rounded up to 16) from device
+    assignments [P, L, E] (``mp_pe_gather_u8``, one launch for every topology of the batch); an
+    expert placed outside its placement's topology raises the SPEC error."""
     t = _lib.torch()
-    dev = assign.device
+    dev = _lib.require_cuda()
     uniq, topo_of = _unique_costs(costs)
-    topo_of = np.asarray(topo_of)
-    if len(uniq) == 1:  # one topology: a single gather, no index copies
-        P = assign.shape[0]
-        return t.gather(uniq[0].p.unsqueeze(0).expand(P, -1, -1), 2, assign).reshape(P, -1)
-    out = t.empty((assign.shape[0], model.L * model.E), dtype=t.uint8, device=dev)
-    for ti, c in enumerate(uniq):
-        idx = t.as_tensor(np.flatnonzero(topo_of == ti), device=dev)
-        sel = assign.index_select(0, idx)
-        out[idx] = t.gather(c.p.unsqueeze(0).expand(len(idx), -1, -1), 2, sel).reshape(len(idx), -1)
-    return out
+    cost, S = _padded_costs(uniq, model)
+    P, LE = assign.shape[0], model.L * model.E
+    ldpe = -(-LE // 16) * 16
+    a32 = assign.to(device=dev, dtype=t.int32).contiguous()
+    d_topo = _lib.to_dev(np.asarray(topo_of, dtype=np.int32), t.int32)
+    d_S = _lib.to_dev(np.asarray([c.S for c in uniq], dtype=np.int32), t.int32)
+    pe = t.empty((P, ldpe), dtype=t.uint8, device=dev)
+    err = _lib.new_err()
+    _lib.call("mp_pe_gather_u8", _lib.ptr(cost), len(uniq), model.L, S, _lib.ptr(d_S), _lib.ptr(a32), _lib.ptr(d_topo),
+              P, model.E, _lib.ptr(pe), ldpe, _lib.ptr(err), _lib.stream_handle())
+    code, q, _, _ = _lib.read_err(err)
+    if code:
+        raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {q}, {costs[q].S} devices)")
+    return pe[:, :LE]
 
 
-def _digits(x, bits: int = 7):
-    """Number of base-2^bits digits needed for non-negative integer tensor x."""
-    mx = int(x.max().item()) if x.numel() else 0
-    d = 1
-    while mx >= (1 << (bits * d)):
-        d += 1
-    return d
+def _pe_operand(pe):
+    """(tensor, row pitch) of a uint8 [P, LE] cost matrix as the contraction's A operand: rows with a
+    16-byte-multiple pitch (a padded copy only when the given rows do not have one)."""
+    t = _lib.torch()
+    P, LE = pe.shape
+    if pe.stride(1) == 1 and pe.stride(0) % 16 == 0 and pe.data_ptr() % 16 == 0:
+        return pe, pe.stride(0)
+    ldpe = -(-LE // 16) * 16
+    A = t.zeros((P, ldpe), dtype=t.uint8, device=pe.device)
+    A[:, :LE].copy_(pe)
+    return A, ldpe
+
+
+def _n_digits(max_count: int) -> int:
+    if max_count < 0:
+        raise ConfigError("contract_tc: negative count bound")
+    for nd in (1, 2, 4):
+        if max_count < (1 << (8 * nd)):
+            return nd
+    raise ConfigError("contract_tc: per-chunk counts of 2^32 or more are outside the digit format")
+
+
+class CountDigits:
+    """The contraction's B operand: per-chunk counts int64 [C, LE] split into 8-bit digits
+    (``mp_count_digits_u8``), uint8 [C*ndig, ldd], row c*ndig + a = digit a of chunk c.  Built once
+    per trace (the placement search reuses it every iteration)."""
+
+    def __init__(self, cnt, max_count: Optional[int] = None, err=None):
+        t = _lib.torch()
+        C, LE = cnt.shape
+        if max_count is None:
+            max_count = int(cnt.max().item()) if cnt.numel() else 0
+        self.C, self.LE, self.ndig = C, LE, _n_digits(int(max_count))
+        self.ldd = -(-LE // 16) * 16
+        self.buf = t.empty((C * self.ndig, self.ldd), dtype=t.uint8, device=cnt.device)
+        self.err = _lib.new_err() if err is None else err
+        self.own_err = err is None
+        _lib.call("mp_count_digits_u8", _lib.ptr(cnt.contiguous()), C, LE, self.ndig, self.ldd, _lib.ptr(self.buf),
+                  _lib.ptr(self.err), _lib.stream_handle())
+
+    def contract(self, pe, out=None, ctas: int = 0):
+        """out[P, C] += pe [P, LE] @ counts^T, exact int64, on the tensor cores (``mp_contract_tc_u8``;
+        ``ctas`` = 0: one CTA per SM)."""
+        t = _lib.torch()
+        A, ldpe = _pe_operand(pe)
+        P = A.shape[0]
+        if out is None:
+            out = t.zeros((P, self.C), dtype=t.int64, device=A.device)
+        _lib.call("mp_contract_tc_u8", _lib.ptr_any(A), P, ldpe, _lib.ptr(self.buf), self.C, self.ndig, self.LE,
+                  self.ldd, _lib.ptr(out), ctas, _lib.stream_handle())
+        return out
+
+    def check(self):
+        if self.own_err:
+            _lib.check_err(self.err, "contract_tc: per-chunk count outside its digit range")
 
 
 def contract_tc(cnt, pe, max_count: Optional[int] = None, max_pe: Optional[int] = None, err=None):
-    """Exact hop sums [P, C] = pe [P, LE] (uint8) @ cnt^T [LE, C] (int64 counts) on the tensor cores:
-    both operands are split into 7-bit digits (int8 >= 0) and every digit pair's products come from
-    int8 GEMMs with int32 accumulation (cuBLASLt; exact since LE * 127^2 < 2^31 for LE <= 133,000).
-    ``mp_count_digits`` writes all count digits as one stacked operand (rows a*Cp + c), so one GEMM
-    per pe digit (one in total when pe < 128) yields every digit's partials side by side, and
-    ``mp_digit_combine`` adds them into int64 with weights 128^(a+b).  ``max_count`` / ``max_pe``
-    bound the operands (no device reduction or sync when given; a count above the bound raises
-    rather than truncating); with ``err`` the caller checks that device error block itself."""
-    t = _lib.torch()
-    P, LE = pe.shape
-    C = cnt.shape[0]
-    if LE * 127 * 127 >= 2 ** 31:
-        raise ConfigError("contract_tc: L*E too large for exact int32 accumulation")
-    Pp, Cp = max(32, -(-P // 32) * 32), max(8, -(-C // 8) * 8)
-    LEp = max(16, -(-LE // 16) * 16)  # cuBLASLt int8: K a multiple of 16 (zero padding is exact)
-    out = t.zeros((P, C), dtype=t.int64, device=pe.device)
-    if max_count is None:
-        da = _digits(cnt)
-    else:
-        da = 1
-        while max_count >= (1 << (7 * da)):
-            da += 1
-    db = 1 if (max_pe if max_pe is not None else int(pe.max().item())) < 128 else 2
-    cnt = cnt.contiguous()
-
-    def pe_digit(b):
-        d = pe if db == 1 else ((pe & 127) if b == 0 else (pe >> 7))
-        if (Pp, LEp) == (P, LE):
-            return d.view(t.int8)  # values < 128: the uint8 bits are the int8 value
-        A = t.zeros((Pp, LEp), dtype=t.int8, device=pe.device)
-        A[:P, :LE].copy_(d.view(t.int8))
-        return A
-
-    own_err = err is None
-    if own_err:
-        err = _lib.new_err()
-    B = t.empty((da * Cp, LEp), dtype=t.int8, device=pe.device)  # B^T row-major == B column-major
-    sh = _lib.stream_handle()
-    _lib.call("mp_count_digits", _lib.ptr(cnt), C, LE, da, Cp, LEp, _lib.ptr(B), _lib.ptr(err), sh)
-    for b in range(db):
-        part = t._int_mm(pe_digit(b), B.t())  # int32 [Pp, da*Cp], exact
-        _lib.call("mp_digit_combine", _lib.ptr(part), P, part.shape[1], C, Cp, da, 7 * b, _lib.ptr(out), sh)
-    if own_err:
-        _lib.check_err(err, "contract_tc: per-chunk count outside its digit range")
+    """Exact hop sums [P, C] = pe [P, LE] (uint8) @ cnt^T [LE, C] (int64 per-chunk counts) on the 5th-
+    generation tensor cores: the counts are split into 8-bit digits (``mp_count_digits_u8``) and ONE
+    u8 x u8 GEMM (``mp_contract_tc_u8``: tcgen05 kind::i8, TMA-fed, int32 accumulators in TMEM, exact
+    split-K ranges) produces every digit's partials, recombined into int64 in its epilogue.
+    ``max_count`` bounds the counts (no device reduction or sync when given; a count above it raises
+    rather than truncating); ``max_pe`` is accepted for compatibility (pe is used as u8 as it is);
+    with ``err`` the caller checks that device error block itself."""
+    d = CountDigits(cnt, max_count, err)
+    out = d.contract(pe)
+    d.check()
     return out
 
 
@@ -366,11 +381,11 @@ def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement
     if contraction == "tc":
         # a per-chunk count is at most the chunk's token count (distinct picks per record)
         max_count = int(np.max(trace.chunk_token_counts()))
-        max_pe = max(c.max_p for c in _unique_costs(_as_costs(costs, len(placements)))[0])
-        out = contract_tc(cnt.view(C, -1), pe, max_count=max_count, max_pe=max_pe)
+        out = contract_tc(cnt.view(C, -1), pe, max_count=max_count)
     elif contraction == "cuda":
         out = t.zeros((pe.shape[0], C), dtype=t.int64, device=cnt.device)
-        _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe), pe.shape[0], m.L * m.E, _lib.ptr(out),
+        pe_c = pe.contiguous()
+        _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe_c), pe.shape[0], m.L * m.E, _lib.ptr(out),
                   _lib.stream_handle())
     else:
         raise ConfigError(f"unknown contraction {contraction!r}")
@@ -440,23 +455,21 @@ def evaluate_batch(trace: ActivationTrace, assign, costs, method: str = "auto") 
         raise ConfigError("assign batch must hold integer device ids")
     P = int(a.shape[0])
     costs = _as_costs(costs, P)
-    a = a.to(dev, non_blocking=a.is_pinned()).long()
-    S = t.as_tensor(np.asarray([c.S for c in costs], dtype=np.int64), device=dev)
-    flat = a.view(P, -1)
-    bad = (flat.amin(1) < 0) | (flat.amax(1) >= S)
-    if bool(bad.any()):
-        q = int(t.nonzero(bad)[0, 0])
-        raise MoeplaceError(f"evaluate: expert placed outside the topology (placement {q}, {costs[q].S} devices)")
+    if a.dtype != t.int32 and a.numel():  # range-check before narrowing to int32 (the gather checks the rest)
+        lo, hi = int(a.min()), int(a.max())
+        if lo < 0 or hi >= 2 ** 31:
+            raise MoeplaceError("evaluate: expert placed outside the topology")
+    a = a.to(dev, non_blocking=a.is_pinned())
     if method == "auto":
         fact_bytes = trace.n_chunks * m.L * m.E * 8
         method = "factorized" if P > MAX_LANES and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
     if method == "factorized":
+        pe = _pe_from_device_assign(a, costs, m)  # checks every assignment against its topology
         cnt = chunk_counts(trace)
-        pe = _pe_from_device_assign(a, costs, m)
-        max_pe = max(c.max_p for c in _unique_costs(costs)[0])
-        sums = contract_tc(cnt.view(trace.n_chunks, -1), pe, max_count=int(np.max(trace.chunk_token_counts())),
-                           max_pe=max_pe).cpu().numpy()
+        sums = contract_tc(cnt.view(trace.n_chunks, -1), pe,
+                           max_count=int(np.max(trace.chunk_token_counts()))).cpu().numpy()
     elif method in ("gather", "count", "token", "pass"):
+        _pe_from_device_assign(a, costs, m)  # same range check as the factorized path
         host = a.to(t.int32).cpu().numpy()
         pls = [Placement(host[q]) for q in range(P)]
         sums = score_sums(trace, pls, costs, algo="auto" if method == "pass" else method)
@@ -634,16 +647,33 @@ def token_hops(selections, placement: Placement, cost: CostMatrix) -> int:
 
 def objective_value(placement: Placement, freq: FrequencyTable, cost: CostMatrix) -> float:
     """sum_{l,e} f[l,e] * p[l, device(l,e)].  Equals evaluate(train).mean / K
-    for the trace f was estimated from."""
+    for the trace f was estimated from (SPEC.md:383).  On the device: pe by ``mp_pe_gather_u8``;
+    with the table's exact counts the sum is the integer contraction sum_{l,e} count * pe
+    (``mp_contract_counts``) over K * n_tokens, one correctly rounded division; float-only
+    frequencies are summed by ``mp_objective_f64``."""
+    t = _lib.torch()
     f = np.asarray(freq.f, dtype=np.float64)
-    a = placement.assign
+    a = np.asarray(placement.assign)
     if f.shape != a.shape:
         raise ConfigError(f"frequency table {f.shape} and placement {a.shape} differ")
-    p = cost.numpy()
-    if a.min() < 0 or a.max() >= p.shape[1]:
+    if a.size and (a.min() < 0 or a.max() >= cost.S):
         raise MoeplaceError("objective_value: expert placed outside the topology")
-    pe = p[np.arange(a.shape[0])[:, None], a].astype(np.float64)
-    return float(np.sum(f * pe))
+    L, E = a.shape
+    model = ModelSpec(L, E, max(1, int(freq.topk or 1)))
+    pe = _pe_from_device_assign(_lib.to_dev(a[None], t.int32), [cost], model)
+    LE = L * E
+    sh = _lib.stream_handle()
+    if freq.counts is not None and freq.n_tokens and freq.topk:
+        cnt = _lib.to_dev(np.asarray(freq.counts, dtype=np.int64).reshape(1, LE), t.int64)
+        out = t.zeros((1, 1), dtype=t.int64, device=cnt.device)
+        pe_c = pe.contiguous()
+        _lib.call("mp_contract_counts", _lib.ptr(cnt), 1, _lib.ptr(pe_c), 1, LE, _lib.ptr(out), sh)
+        return int(out.item()) / (int(freq.topk) * int(freq.n_tokens))
+    fd = _lib.to_dev(f.reshape(LE), t.float64)
+    out = t.empty(1, dtype=t.float64, device=fd.device)
+    A, ldpe = _pe_operand(pe)
+    _lib.call("mp_objective_f64", _lib.ptr(fd), _lib.ptr_any(A), ldpe, LE, 1, _lib.ptr(out), sh)
+    return float(out.item())
 
 
 def gain(baseline_hops: float, method_hops: float) -> float:

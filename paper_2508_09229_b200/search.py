@@ -3,15 +3,23 @@
 Local search over placements: every iteration perturbs the incumbent into a batch of candidates
 with random within-layer swaps (which keep every per-(device, layer) and per-device count, so
 constraints stay satisfied — SPEC.md:182-191), scores the whole batch at once with the factorized
-evaluator (per-chunk counts computed ONCE on the device, then one exact tensor-core contraction per
-batch, `eval.contract_tc`) and accepts the best candidate if it improves the objective.
+evaluator and accepts the best candidate if it improves the objective.  The whole iteration runs as
+device kernels with no host synchronisation:
+
+  * ``mp_perturb_pe_u8``   the candidates' per-expert cost rows: swapping two experts' devices swaps
+                           their pe bytes, so a candidate is the incumbent's u8 row with its swaps
+                           applied (the swap list is kept, the int32 assignments are never built);
+  * ``mp_contract_tc_u8``  exact per-chunk hop sums of the batch on the tensor cores (tcgen05 kind::i8)
+                           against the trace's per-chunk count digits, computed ONCE per search;
+  * ``mp_batch_objective`` the objective of every candidate from its exact sums;
+  * ``mp_search_accept``   argmin, and — if it improves — the winner's swaps replayed on the device
+                           assignment and cost row; the history is written on the device.
 
 Objectives are functions of the exact per-chunk hop sums, so they can be non-linear where the ILP
 of Eq. (1) is linear:
   * "mean"       token-weighted mean hops (= K * objective_value; ILPLoad is optimal)
   * "mean+std"   mean + lam * population std of per-chunk means (robustness across dialogs)
   * "max"        worst per-chunk mean
-Everything (perturbation, cost gather, contraction, objective, argmin) stays on the GPU.
 """
 from __future__ import annotations
 
@@ -21,9 +29,11 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, MoeplaceError
-from .eval import contract_tc
+from .eval import CountDigits, _pe_from_device_assign
 from .model_trace import ActivationTrace, chunk_counts
 from .placement import CostMatrix, Placement
+
+OBJECTIVES = {"mean": 0, "mean+std": 1, "max": 2}
 
 
 @dataclass
@@ -32,40 +42,7 @@ class SearchResult:
     objective: float
     history: list = field(default_factory=list)  # objective of the incumbent after each iteration
     evaluated: int = 0                          # candidates scored
-
-
-def _objective(sums, tokens, kind: str, lam: float):
-    """sums: int64 [B, C] (device), tokens: int64 [C] -> float64 [B]."""
-    t = _lib.torch()
-    keep = tokens > 0
-    s = sums[:, keep].to(t.float64)
-    n = tokens[keep].to(t.float64)
-    mean = s.sum(dim=1) / n.sum()
-    if kind == "mean":
-        return mean
-    means = s / n
-    if kind == "mean+std":
-        return mean + lam * means.std(dim=1, unbiased=False)
-    if kind == "max":
-        return means.max(dim=1).values
-    raise ConfigError(f"unknown objective {kind!r}")
-
-
-def perturb(assign, batch: int, n_swaps: int, gen):
-    """[B, L, E] candidates: `n_swaps` random within-layer swaps of `assign` each (device)."""
-    t = _lib.torch()
-    L, E = assign.shape
-    cand = assign.unsqueeze(0).repeat(batch, 1, 1)
-    b = t.arange(batch, device=assign.device)
-    for _ in range(n_swaps):
-        l = t.randint(0, L, (batch,), device=assign.device, generator=gen)
-        x = t.randint(0, E, (batch,), device=assign.device, generator=gen)
-        y = t.randint(0, E, (batch,), device=assign.device, generator=gen)
-        vx = cand[b, l, x].clone()
-        vy = cand[b, l, y].clone()
-        cand[b, l, x] = vy
-        cand[b, l, y] = vx
-    return cand
+    accepted: list = field(default_factory=list)  # per iteration: accepted candidate index or -1
 
 
 def improve_placement(trace: ActivationTrace, start: Placement, cost: CostMatrix, objective: str = "mean",
@@ -78,35 +55,42 @@ def improve_placement(trace: ActivationTrace, start: Placement, cost: CostMatrix
         raise MoeplaceError("improve_placement: empty trace")
     if start.assign.shape != (m.L, m.E):
         raise ConfigError("placement shape does not match the trace")
+    if objective not in OBJECTIVES:
+        raise ConfigError(f"unknown objective {objective!r}")
+    if batch < 1 or n_swaps < 1 or iters < 0:
+        raise ConfigError("batch and n_swaps must be >= 1, iters >= 0")
     dev = _lib.require_cuda()
-    C = trace.n_chunks
-    cnt = chunk_counts(trace).view(C, -1)          # once: [C, L*E]
-    tokens = t.as_tensor(trace.chunk_token_counts(), device=dev)
-    p = cost.p.to(t.int64)                          # [L, S]
-    gen = t.Generator(device=dev)
-    gen.manual_seed(seed)
-    cur = _lib.to_dev(start.assign, t.int64)
-    max_count = int(max(trace.chunk_token_counts().max(), 0))
+    C, LE = trace.n_chunks, m.L * m.E
     err = _lib.new_err()
+    digits = CountDigits(chunk_counts(trace).view(C, -1), int(max(trace.chunk_token_counts().max(), 0)), err)
+    tokens = _lib.to_dev(trace.chunk_token_counts(), t.int64)
+    cur = _lib.to_dev(start.assign, t.int32)
+    pe0 = _pe_from_device_assign(cur.unsqueeze(0), [cost], m)        # [1, LE] view of a padded row
+    ldpe = -(-LE // 16) * 16
+    pe_cur = t.zeros(ldpe, dtype=t.uint8, device=dev)
+    pe_cur[:LE].copy_(pe0[0])
+    pe_b = t.empty((batch, ldpe), dtype=t.uint8, device=dev)
+    swaps = t.empty((batch, n_swaps, 3), dtype=t.int32, device=dev)
+    sums = t.zeros((batch, C), dtype=t.int64, device=dev)
+    obj = t.empty(batch, dtype=t.float64, device=dev)
+    cur_obj = t.empty(1, dtype=t.float64, device=dev)
+    history = t.empty(iters + 1, dtype=t.float64, device=dev)
+    accepted = t.full((iters + 1,), -1, dtype=t.int64, device=dev)
+    sh = _lib.stream_handle()
+    kind = OBJECTIVES[objective]
 
-    def score(cands):
-        pe = t.gather(p.unsqueeze(0).expand(cands.shape[0], -1, -1), 2, cands)  # [B, L, E]
-        sums = contract_tc(cnt, pe.reshape(cands.shape[0], -1).to(t.uint8), max_count=max_count, max_pe=cost.max_p,
-                           err=err)
-        return _objective(sums, tokens, objective, lam)
-
-    best = float(score(cur.unsqueeze(0))[0].item())
-    hist = [best]
-    evaluated = 1
-    for _ in range(iters):
-        cands = perturb(cur, batch, n_swaps, gen)
-        obj = score(cands)
-        evaluated += batch
-        i = int(t.argmin(obj).item())
-        v = float(obj[i].item())
-        if v < best:
-            best, cur = v, cands[i].clone()
-        hist.append(best)
+    s0 = digits.contract(pe_cur.view(1, ldpe)[:, :LE], t.zeros((1, C), dtype=t.int64, device=dev))
+    _lib.call("mp_batch_objective", _lib.ptr(s0), _lib.ptr(tokens), 1, C, kind, float(lam), _lib.ptr(cur_obj), sh)
+    history[0:1].copy_(cur_obj)
+    for it in range(iters):
+        _lib.call("mp_perturb_pe_u8", _lib.ptr(pe_cur), m.L, m.E, batch, n_swaps, int(seed) & 0xFFFFFFFFFFFFFFFF, it,
+                  _lib.ptr(pe_b), ldpe, _lib.ptr(swaps), sh)
+        sums.zero_()
+        digits.contract(pe_b[:, :LE], sums)
+        _lib.call("mp_batch_objective", _lib.ptr(sums), _lib.ptr(tokens), batch, C, kind, float(lam), _lib.ptr(obj), sh)
+        _lib.call("mp_search_accept", _lib.ptr(obj), batch, _lib.ptr(swaps), n_swaps, m.E, _lib.ptr(cur),
+                  _lib.ptr(pe_cur), _lib.ptr(cur_obj), _lib.ptr(history), it + 1, _lib.ptr(accepted), sh)
     _lib.check_err(err, "improve_placement: per-chunk count outside its digit range")
-    out = Placement(cur.to(t.int32).cpu().numpy(), start.constraints, (start.label or "start") + f"+search[{objective}]")
-    return SearchResult(out, best, hist, evaluated)
+    hist = history.cpu().tolist()
+    out = Placement(cur.cpu().numpy(), start.constraints, (start.label or "start") + f"+search[{objective}]")
+    return SearchResult(out, hist[-1], hist, 1 + iters * batch, accepted[1:].cpu().tolist())

@@ -561,10 +561,10 @@ def test_contract_tc_count_above_the_stated_bound_raises():
     import torch
     from moeplace.errors import MoeplaceError
     pe = torch.ones((40, 64), dtype=torch.uint8, device="cuda")
-    cnt = torch.full((9, 64), 200, dtype=torch.int64, device="cuda")
-    assert ev.contract_tc(cnt, pe, max_count=200).sum().item() == 40 * 9 * 64 * 200
+    cnt = torch.full((9, 64), 300, dtype=torch.int64, device="cuda")
+    assert ev.contract_tc(cnt, pe, max_count=300).sum().item() == 40 * 9 * 64 * 300
     with pytest.raises(MoeplaceError):
-        ev.contract_tc(cnt, pe, max_count=100)  # one 7-bit digit cannot hold 200: raised, not truncated
+        ev.contract_tc(cnt, pe, max_count=100)  # one 8-bit digit cannot hold 300: raised, not truncated
 
 
 @pytest.mark.parametrize("shape", [R1, B16, (2, 4, 1), (1, 256, 3)])

@@ -77,11 +77,18 @@ def test_argument_validation_matrix():
         (L.mp_comm_map(P, P, P, P, 4, P, P, Lr, E, 8, P, None, None), ARG),
         (L.mp_pack_server_tables(P, 1, P, P, 5, Lr, E, 8, P, P, None), ARG),
         (L.mp_contract_counts(P, 65535 * 16 + 1, P, 1, 10, P, None), UNS),
-        (L.mp_count_digits(P, 4, 10, 2, 3, 16, P, P, None), ARG),           # Cp < C
-        (L.mp_count_digits(P, 4, 10, 2, 8, 16, P, None, None), ARG),        # err required
-        (L.mp_count_digits(P, 4, 10, 0, 8, 16, P, P, None), ARG),           # no digits
-        (L.mp_digit_combine(P, 4, 8, 3, 8, 2, 0, P, None), ARG),            # ldp < ndig*Cp
-        (L.mp_digit_combine(P, 4, 16, 3, 8, 2, 50, P, None), ARG),          # shift beyond int64
+        (L.mp_count_digits_u8(P, 4, 10, 2, 8, P, P, None), ARG),            # ldd < LE
+        (L.mp_count_digits_u8(P, 4, 10, 2, 16, P, None, None), ARG),        # err required
+        (L.mp_count_digits_u8(P, 4, 10, 3, 16, P, P, None), ARG),           # ndig not 1/2/4
+        (L.mp_contract_tc_u8(P, 8, 24, P, 4, 2, 20, 32, P, 0, None), ARG),  # ldpe not a multiple of 16
+        (L.mp_contract_tc_u8(P, 8, 32, P, 4, 3, 20, 32, P, 0, None), ARG),  # ndig not 1/2/4
+        (L.mp_contract_tc_u8(P, 8, 32, P, 4, 2, 20, 32, P, -1, None), ARG), # negative split
+        (L.mp_pe_gather_u8(P, 1, Lr, 8, None, P, None, 4, E, P, Lr * E, None, None), ARG),  # err required
+        (L.mp_pe_gather_u8(P, 1, Lr, 8, None, P, None, 4, E, P, Lr * E - 1, P, None), ARG),  # ldpe < L*E
+        (L.mp_perturb_pe_u8(P, Lr, E, 4, 2, 0, 0, P, Lr * E + 8, P, None), ARG),  # ldpe not 16-aligned
+        (L.mp_batch_objective(P, P, 4, 8, 3, 1.0, P, None), ARG),           # unknown objective kind
+        (L.mp_search_accept(P, 4, P, 2, E, P, P, P, P, 0, None, None), ARG),  # accepted[] required
+        (L.mp_objective_f64(P, P, 8, 16, 1, P, None), ARG),                 # ldpe < LE
         (L.mp_coeffs(P, 0, P, Lr, E, 8, 1e9, P, None, None), ARG),          # denom 0 with counts
         (L.mp_copy_planes_h2d(P, 8, P, 16, 16, 1, None), ARG),               # dst stride < width
         (L.mp_copy_planes_h2d(P, 16, P, 16, 0, 4, None), 0),                 # empty copy is a no-op
