@@ -16,6 +16,8 @@
 // into u32 every 64 windows and at each flush.  With HIST every byte also increments the
 // lane-replicated histogram (W = 1: in the table rows' free half, one PRMT per address; W = 2 / 4:
 // a separate region of 128-byte rows, PRMT byte extract + IMAD), flushed per segment.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace mp {
@@ -47,8 +49,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int E,
            const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
            int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
-  constexpr int K = 8;
   constexpr int P = 4 * W;
+  constexpr int U = seg_unroll<W>();
   // 256 rows x 256 B of tables (W = 1: bytes 128-255 of each row hold the histogram replicas);
   // W > 1 with HIST: + a 256 rows x 128 B histogram region; then a 128-byte trash row
   extern __shared__ __align__(128) uint8_t sm[];
@@ -57,50 +59,72 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t base = smem_addr(sm);
-  const uint32_t hbase = base + 128;
   const uint32_t slot = W == 4 ? (uint32_t)((lane & 7) << 4) : W == 2 ? (uint32_t)(lane << 3) : (uint32_t)(lane << 2);
   const uint32_t hslot = (uint32_t)(lane << 2);
   const uint32_t hreg = base + 256 * 256 + hslot;  // W > 1: bin e of this lane at hreg + e * 128
-  const uint32_t trash = base + 256 * 256 + (kHistRegion ? 256 * 128 : 0) + hslot;  // masked-out tokens (no branch)
-  // histogram address of byte b of `word` (lane replica)
-  auto haddr = [&](uint32_t word, int b) -> uint32_t {
-    if constexpr (kHistRegion) return prmt(word, 0u, 0x4440u | (uint32_t)b) * 128u + hreg;
-    else return hbase + prmt(word, hslot, sel_row(b));
-  };
+  const uint32_t trash = base + 256 * 256 + (kHistRegion ? 256 * 128 : 0) + hslot;  // masked-out tokens
 
-  uint32_t acc16[2 * W], acc32[P];
+  // running sums of the current chunk in u16 lanes (acc16[2w] = placements {4w, 4w+2}, acc16[2w+1] =
+  // {4w+1, 4w+3}); they are widened only inside a flush, which runs at every chunk boundary and
+  // at least every 128 windows (128 x 2 tokens x 248 < 2^16), so no u32 sums stay live
+  uint32_t acc16[2 * W];
 #pragma unroll
   for (int i = 0; i < 2 * W; ++i) acc16[i] = 0;
-#pragma unroll
-  for (int i = 0; i < P; ++i) acc32[i] = 0;
-  auto widen = [&]() {
+  // two tokens' u8-lane sums into the u16 lanes: one PRMT per half and word, one IADD3 each
+  auto add2 = [&](const uint32_t (&a)[W], const uint32_t (&b)[W]) {
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      acc32[4 * w + 0] += acc16[2 * w] & 0xffffu;
-      acc32[4 * w + 2] += acc16[2 * w] >> 16;
-      acc32[4 * w + 1] += acc16[2 * w + 1] & 0xffffu;
-      acc32[4 * w + 3] += acc16[2 * w + 1] >> 16;
+      acc16[2 * w] += prmt(a[w], 0u, 0x7270u) + prmt(b[w], 0u, 0x7270u);      // bytes 0, 2
+      acc16[2 * w + 1] += prmt(a[w], 0u, 0x7371u) + prmt(b[w], 0u, 0x7371u);  // bytes 1, 3
+    }
+  };
+  int64_t* hp = nullptr;  // &hop_sums[q][c] of this lane's reduce-scatter slot q (set per warp range)
+  auto flush = [&]() {  // warp-uniform: running sums of the current chunk -> hop_sums[.][c]
+    uint32_t v[P];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      v[4 * w + 0] = acc16[2 * w] & 0xffffu;
+      v[4 * w + 2] = acc16[2 * w] >> 16;
+      v[4 * w + 1] = acc16[2 * w + 1] & 0xffffu;
+      v[4 * w + 3] = acc16[2 * w + 1] >> 16;
       acc16[2 * w] = 0;
       acc16[2 * w + 1] = 0;
     }
+    int q = 0;
+    const uint32_t tot = warp_reduce_scatter<P>(v, lane, &q);
+    if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hp, (int64_t)tot);
   };
-  auto add_token = [&](const uint32_t (&s)[W]) {
+  // the 8 lookups (+ histogram increments) of one token record: u8-lane sums per table word
+  auto record = [&](uint32_t w0, uint32_t w1, bool valid, uint32_t (&sum)[W]) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      acc16[2 * w] += s[w] & 0x00ff00ffu;
-      acc16[2 * w + 1] += (s[w] >> 8) & 0x00ff00ffu;
+    for (int w = 0; w < W; ++w) sum[w] = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      const uint32_t word = k < 4 ? w0 : w1;
+      const uint32_t a0 = base + prmt(word, slot, sel_row(k & 3));
+      const uint32_t a1 = base + prmt(word, slot, sel_row((k + 1) & 3));
+      uint32_t x0[W], x1[W];
+      seg_lookup<W>(a0, x0);
+      seg_lookup<W>(a1, x1);
+#pragma unroll
+      for (int w = 0; w < W; ++w) sum[w] = sum[w] + x0[w] + x1[w];
+      if constexpr (HIST) {
+        if constexpr (kHistRegion) {
+          atoms_inc(valid ? prmt(word, 0u, 0x4440u | (uint32_t)(k & 3)) * 128u + hreg : trash);
+          atoms_inc(valid ? prmt(word, 0u, 0x4440u | (uint32_t)((k + 1) & 3)) * 128u + hreg : trash);
+        } else {  // W = 1: the lane's replica sits 128 bytes after its table slot in the same row
+          atoms_inc(valid ? a0 + 128u : trash);
+          atoms_inc(valid ? a1 + 128u : trash);
+        }
+      }
+    }
+    if (!valid) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) sum[w] = 0;
     }
   };
-  auto flush = [&](int c) {  // warp-uniform: running sums of chunk c -> hop_sums[.][c]
-    widen();
-    int q = 0;
-    const uint32_t tot = warp_reduce_scatter<P>(acc32, lane, &q);
-    if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + c, (int64_t)tot);
-#pragma unroll
-    for (int i = 0; i < P; ++i) acc32[i] = 0;
-  };
 
-  Flat f(t0 * K, t1 * K, L);
+  Flat f(t0 * 8, t1 * 8, L);
   for (int64_t g = f.g0; g < f.g1;) {
     const int l = (int)(g / f.nb);
     const int64_t off_in = g - (int64_t)l * f.nb;
@@ -124,13 +148,16 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
     __syncthreads();
 
     // tokens [ta, tb) of this segment; vector (token pair) m covers tokens 2m, 2m+1
-    const int64_t ta = x0 / K, tb = x1 / K;
+    const int64_t ta = x0 / 8, tb = x1 / 8;
     const int64_t m0 = ta >> 1, m1 = (tb + 1) >> 1;
     const int64_t per = (m1 - m0 + kSegWarps - 1) / kSegWarps;
     const int64_t wm0 = min(m1, m0 + per * warp), wm1 = min(m1, wm0 + per);
     if (wm0 < wm1) {
-      // the warp's tokens [wt0, wt1)
+      // the warp's tokens [wt0, wt1); 32-bit offsets from its first pair (pair r = tokens T0+2r, +1)
       const int64_t wt0 = max(ta, 2 * wm0), wt1 = min(tb, 2 * wm1);
+      const int64_t T0 = 2 * wm0;
+      const int npairs = (int)(wm1 - wm0);
+      const int ra = (int)(wt0 - T0), rb = (int)(wt1 - T0);  // valid relative tokens [ra, rb)
       int c = 0;
       {
         int lo = 0, hi = C;
@@ -140,80 +167,80 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
         }
         c = lo;
       }
-      int64_t nb = __ldg(bounds + c + 1);  // first token of the next chunk
-      // 32-bit offsets from the warp's first pair: pair r covers tokens T0 + 2r, T0 + 2r + 1
-      const int64_t T0 = 2 * wm0;
-      const int npairs = (int)(wm1 - wm0);
-      const int ra = (int)(wt0 - T0), rb = (int)(wt1 - T0);  // valid relative tokens [ra, rb)
-      auto rel = [&](int64_t t) { return (int)min(t - T0, (int64_t)0x7fffffff); };
-      int nbr = rel(nb);
+      // relative chunk starts: 32-bit differences (a GPU's token range is far below 2^31), low words only
+      const uint32_t T0lo = (uint32_t)T0;
+      auto next_start = [&](int cc) {
+        return (int)(__ldg(reinterpret_cast<const uint32_t*>(bounds + cc)) - T0lo);
+      };
+      int nbr = next_start(c + 1);  // first token of the next chunk
+      // this lane's reduce-scatter slot (warp_reduce_scatter: q = lane >> (5 - log2 P))
+      hp = hop_sums + (int64_t)(lane >> (P == 4 ? 3 : P == 8 ? 2 : 1)) * C + c;
       const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane) + wm0;
-      int since = 0;  // windows since the last widen
-      for (int rw = 0; rw < npairs; rw += 32 * seg_unroll<W>()) {
-        constexpr int kSegU = seg_unroll<W>();
-        int4 x[kSegU];
-#pragma unroll
-        for (int u = 0; u < kSegU; ++u) {
-          const int r = rw + u * 32 + lane;
-          x[u] = r < npairs ? ldg_stream(pv + r) : make_int4(0, 0, 0, 0);
+
+      // one 64-token window: pairs [rfirst, rfirst + 32).  EDGE: it may hold tokens outside
+      // [ra, rb) (the warp's first window when ra = 1, the last ones); interior windows carry no
+      // per-lane validity logic at all.
+      auto window = [&](const int4& x, int rfirst, auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
+        bool vA = true, vB = true;
+        if constexpr (EDGE) {
+          const int tA = 2 * (rfirst + lane);
+          vA = tA >= ra && tA < rb;
+          vB = tA + 1 >= ra && tA + 1 < rb;
         }
+        uint32_t sA[W], sB[W];
+        record((uint32_t)x.x, (uint32_t)x.y, vA, sA);
+        record((uint32_t)x.z, (uint32_t)x.w, vB, sB);
+        const int wlast = EDGE ? min(2 * rfirst + 63, rb - 1) : 2 * rfirst + 63;  // last valid token
+        if (nbr <= wlast) {  // chunk boundaries inside the window (warp-uniform)
+          const int tA = 2 * (rfirst + lane);
+          do {
+            const bool inA = tA < nbr, inB = tA + 1 < nbr;  // tokens of chunk c not yet added
+            uint32_t pA[W], pB[W];
 #pragma unroll
-        for (int u = 0; u < kSegU; ++u) {
-          const int rfirst = rw + u * 32;
-          if (rfirst >= npairs) break;  // warp-uniform
-          const int r = rfirst + lane;
-          const int tA = 2 * r, tB = tA + 1;
-          const bool vA = r < npairs && tA >= ra && tA < rb;
-          const bool vB = r < npairs && tB >= ra && tB < rb;
-          const uint32_t wd[4] = {(uint32_t)x[u].x, (uint32_t)x[u].y, (uint32_t)x[u].z, (uint32_t)x[u].w};
-          uint32_t sA[W], sB[W];
-#pragma unroll
-          for (int w = 0; w < W; ++w) sA[w] = sB[w] = 0;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t word = wd[k >> 2];
-            const uint32_t off = prmt(word, slot, sel_row(k & 3));
-            uint32_t t[W];
-            seg_lookup<W>(base + off, t);
-#pragma unroll
-            for (int w = 0; w < W; ++w) sA[w] += t[w];
-            if constexpr (HIST) atoms_inc(vA ? haddr(word, k & 3) : trash);
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t word = wd[2 + (k >> 2)];
-            const uint32_t off = prmt(word, slot, sel_row(k & 3));
-            uint32_t t[W];
-            seg_lookup<W>(base + off, t);
-#pragma unroll
-            for (int w = 0; w < W; ++w) sB[w] += t[w];
-            if constexpr (HIST) atoms_inc(vB ? haddr(word, k & 3) : trash);
-          }
-          // last valid token of this window (warp-uniform)
-          const int wlast = min(2 * (rfirst + 31) + 1, rb - 1);
-          if (nbr > wlast) {  // no boundary in the window (the common case for long chunks)
-            if (vA) add_token(sA);
-            if (vB) add_token(sB);
-          } else {
-            bool dA = !vA, dB = !vB;
-            while (nbr <= wlast) {  // boundary inside the window: tokens < nb belong to chunk c
-              if (!dA && tA < nbr) { add_token(sA); dA = true; }
-              if (!dB && tB < nbr) { add_token(sB); dB = true; }
-              flush(c);
-              since = 0;
-              ++c;
-              nbr = rel(__ldg(bounds + c + 1));  // c < C - 1 here: bounds[C] >= t1 > the window
+            for (int w = 0; w < W; ++w) {
+              pA[w] = inA ? sA[w] : 0u;
+              pB[w] = inB ? sB[w] : 0u;
+              sA[w] -= pA[w];
+              sB[w] -= pB[w];
             }
-            if (!dA) add_token(sA);
-            if (!dB) add_token(sB);
-          }
-          if (++since == 64) {  // u16 lanes: <= 64 windows x 2 tokens x 248 < 2^16
-            widen();
-            since = 0;
-          }
+            add2(pA, pB);
+            flush();
+            ++c;  // c < C - 1 here: bounds[C] >= the trace end > the window
+            ++hp;
+            nbr = next_start(c + 1);
+          } while (nbr <= wlast);
+        }
+        add2(sA, sB);
+      };
+      using Interior = std::integral_constant<bool, false>;
+      using Edge = std::integral_constant<bool, true>;
+
+      // pairs [0, full) have both tokens valid when ra = 0; the first window is an edge when ra = 1
+      const int full = rb == 2 * npairs ? npairs : npairs - 1;
+      int rw = 0, nwin = 0;
+      if (ra != 0) {
+        const int4 x = lane < npairs ? ldg_stream(pv + lane) : make_int4(0, 0, 0, 0);
+        window(x, 0, Edge{});
+        rw = 32;
+      }
+      for (; rw + 32 * U <= full; rw += 32 * U) {  // interior batches: unpredicated loads
+        int4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = ldg_stream(pv + rw + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < U; ++u) window(x[u], rw + u * 32, Interior{});
+        if ((nwin += U) >= 128) {  // u16 headroom: flush into the same chunk
+          flush();
+          nwin = 0;
         }
       }
-      flush(c);
+      for (; rw < npairs; rw += 32) {  // the rest, one window at a time (< U + 1 per warp range)
+        const int r = rw + lane;
+        const int4 x = r < npairs ? ldg_stream(pv + r) : make_int4(0, 0, 0, 0);
+        window(x, rw, Edge{});
+      }
+      flush();
     }
 
     if constexpr (HIST) {
