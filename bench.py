@@ -547,15 +547,9 @@ def main():
         if args.algo != "auto":
             return {"gather": "gather", "count": "count-contract", "seg": "segmented gather",
                     "token": "token-tiled"}[args.algo]
-        # mirrors choose_algo in csrc/stream.cu (K = 8, max_p <= 31 here)
-        tpc = n / max(1, C)
-        seg_hi = (5000 if W == 1 else 3000 if W == 2 else 1800) if hist else (4000 if W == 1 else 6000 if W == 2 else 2500)
-        tok_lo = (70 if W == 1 else 0) if hist else (170 if W == 1 else 0)
-        if tpc < tok_lo:
-            return "token-tiled"
-        if tpc < seg_hi:
-            return "segmented gather"
-        return "count-contract" if (hist or W > 1) else "gather"
+        mp_ = max(g[2] for g in groups)
+        a = _lib.choose_algo(hist, W, n, C, L, K, mp_)  # the library's own AUTO rule
+        return {"gather": "gather", "count": "count-contract", "token": "token-tiled", "seg": "segmented gather"}[a]
 
     run = fstep if fact else step
 

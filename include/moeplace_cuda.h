@@ -171,9 +171,9 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
  *     down sharply for short chunks.  Requires L*K*max_p <= 65535 (else MP_ERR_UNSUPPORTED);
  *     with a histogram it is mp_hist_u8 + the token pass;
  *   MP_ALGO_AUTO:   the faster one for the shape, by average tokens per chunk (measured
- *     crossovers): when SEG applies (K = 8, max_p <= 31) SEG below 5000 / 3000 / 1800 (with a
- *     histogram, W = 1 / 2 / 4) and 4000 / 6000 / 2500 (score-only) tokens per chunk, TOKEN
- *     below 70 (histogram, W = 1) / 170 (score-only W = 1); otherwise TOKEN below MP_TOKEN_CHUNK_TOKENS (W = 1 with
+ *     crossovers, mp_choose_algo): when SEG applies (K = 8, max_p <= 31) SEG below 5500 / 3000 /
+ *     1800 (with a histogram, W = 1 / 2 / 4) and 20000 / 7000 / 2400 (score-only) tokens per
+ *     chunk, TOKEN below 80 (score-only W = 1); otherwise TOKEN below MP_TOKEN_CHUNK_TOKENS (W = 1 with
  *     a histogram; half of it for W = 2, 700 for W = 4; score-only 4096 / 1600 / 800) when the
  *     limit above holds; else GATHER for score-only W = 1 and COUNT otherwise.  This is what
  *     mp_score_u8 / mp_hist_score_u8 use.
@@ -195,6 +195,9 @@ int mp_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begi
 int mp_hist_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
                         int L, int K, int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int W,
                         int max_p, int64_t* counts, int64_t* hop_sums, int64_t* err, int algo, void* stream);
+/* The algorithm MP_ALGO_AUTO resolves to for a call over `tokens` tokens in C chunks (hist != 0: the
+ * fused histogram + score pass).  Host-only, no device work. */
+int mp_choose_algo(int hist, int W, int64_t tokens, int C, int L, int K, int max_p);
 
 /* ---- unique-destination scoring (extension A17; not a SPEC metric) ------------------------
  * For up to 4 placements (W = 1 tables) and per chunk c:

@@ -44,6 +44,7 @@ SIGNATURES = {
     "mp_score_ex_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _i32, _p]),
     "mp_hist_score_ex_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _i32,
                                    _p]),
+    "mp_choose_algo": (_i32, [_i32, _i32, _i64, _i32, _i32, _i32, _i32]),
     "mp_score_dedup_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "mp_pack_server_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _p, _p]),
     "mp_apsp_bfs": (_i32, [_p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),
@@ -95,6 +96,12 @@ def call(name: str, *args) -> int:
     if st in (MP_ERR_ARG, MP_ERR_UNSUPPORTED):
         raise ConfigError(msg)
     raise RuntimeError(msg)
+
+
+def choose_algo(hist: bool, W: int, tokens: int, C: int, L: int, K: int, max_p: int) -> str:
+    """The hop-sum algorithm MP_ALGO_AUTO resolves to for this shape (mp_choose_algo; host-only)."""
+    code = load().mp_choose_algo(int(hist), W, tokens, C, L, K, max_p)
+    return {1: "gather", 2: "count", 3: "token", 4: "seg"}[code]
 
 
 # ---- torch device plumbing -----------------------------------------------------------------

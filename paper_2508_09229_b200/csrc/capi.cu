@@ -6,6 +6,7 @@ namespace mp {
 cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1,
                           int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                           int64_t* hop_sums, int64_t* err, cudaStream_t s, int algo);
+int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K, int max_p);
 cudaError_t launch_gen(uint64_t seed, int64_t t0, int64_t t1, int L, int K, int E, const uint32_t* cdf,
                        const uint8_t* perm, uint8_t* planes, int64_t stride, cudaStream_t s);
 cudaError_t launch_validate(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
@@ -211,6 +212,10 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
                      int64_t* hop_sums, int64_t* err, void* stream) {
   return mp_hist_score_ex_u8(planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C, tables, 1, max_p,
                              counts, hop_sums, err, MP_ALGO_AUTO, stream);
+}
+
+int mp_choose_algo(int hist, int W, int64_t tokens, int C, int L, int K, int max_p) {
+  return mp::choose_algo(hist != 0, W, MP_ALGO_AUTO, tokens, C, L, K, max_p);
 }
 
 int mp_apsp_bfs(const int32_t* row_ptr, const int32_t* col, int n_nodes, const int32_t* src_nodes, int n_src,

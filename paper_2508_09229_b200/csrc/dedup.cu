@@ -59,45 +59,173 @@ constexpr int kDedupThreads = 512;
 #define MP_DEDUP_U 2  // 32-pair windows in flight per warp (K = 8 warp-range path)
 #endif
 
-// Fast K = 8 record for pe bytes <= 31 and server ids < 128 (checked per layer by the CTA).  Row
-// layout of the fast path: slot lane*8 holds {pe word, server word} (one LDS.64 per pick), and bit 7
-// of each server byte flags "this is the source server of the layer for that placement".  With the
-// server id in bits 0-6, t = ((a ^ b) | 0x80808080) - 0x01010101 has bit 7 of a byte set iff the
-// ids differ (each byte of (a^b)|0x80 is >= 0x80, so subtracting 1 never borrows across bytes; the
-// flag bit is ignored), so "new server" = AND of t over the earlier picks, read from bit 7 directly
-// (PRMT's sign-replicate turns it into the dedup mask); a record's hop and dedup sums fit u8 lanes
-// (8 * 31 < 256); the source server is removed once per record (distinct servers - [src in set],
-// the latter the OR of the flag bits).
-__device__ __forceinline__ uint32_t bytes_ne7(uint32_t a, uint32_t b) {
-  return ((a ^ b) | 0x80808080u) - 0x01010101u;
-}
-__device__ __forceinline__ void dedup_record8_fast(uint2 v, uint32_t base, uint32_t slot8,
-                                                   uint32_t (&hop16)[2], uint32_t& uq8, uint32_t (&dd16)[2]) {
-  const uint32_t wv[2] = {v.x, v.y};
-  uint32_t sw[8], pw[8];
+// One record's contributions as u16 lane pairs ({q0, q2}, {q1, q3}): SPEC hops, distinct remote
+// destination servers, deduplicated hops.
+struct DedupRec {
+  uint32_t h[2], u[2], d[2];
+};
+
+// Fast K = 8 record (pe bytes <= 31, server ids < 128; slot lane*8 holds {pe word, server word} with
+// bit 7 of each server byte flagging the layer's source server).  Per pick k the byte-parallel
+// "differs from every earlier pick" test is AND_j ((s_k ^ s_j) | 0x80808080) - 0x01010101 (bit 7 per
+// byte, no borrow between bytes); PRMT's sign-replicate mode turns it into a 0x00/0xff byte mask.
+// Each pick's loads are consumed at once, so only the 8 server words stay live.
+__device__ __forceinline__ void dedup_rec_fast(uint32_t w0, uint32_t w1, uint32_t base, uint32_t slot8, DedupRec& r) {
+  uint32_t sw[8];
+  uint32_t h8 = 0, d8 = 0, n8 = 0, srcany = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const uint2 r = lds64(base + prmt(wv[k >> 2], slot8, sel_row(k & 3)));
-    pw[k] = r.x;
-    sw[k] = r.y;
-  }
-  uint32_t h8 = pw[0], d8 = pw[0], n8 = 0x01010101u, srcany = sw[0];
+    const uint2 e = lds64(base + prmt(k < 4 ? w0 : w1, slot8, sel_row(k & 3)));
+    sw[k] = e.y;
+    uint32_t m = 0xffffffffu;
+    if (k > 0) {
+      uint32_t nw = 0xffffffffu;
 #pragma unroll
-  for (int k = 1; k < 8; ++k) {
-    uint32_t nw = bytes_ne7(sw[k], sw[0]);
-#pragma unroll
-    for (int j = 1; j < k; ++j) nw &= bytes_ne7(sw[k], sw[j]);
-    const uint32_t f = (nw >> 7) & 0x01010101u;  // 1 in bytes whose server is new in the record
-    h8 += pw[k];
-    d8 += pw[k] & (f * 0xffu);                    // byte mask by IMAD: keeps the ALU pipe free
-    n8 += f;
-    srcany |= sw[k];
+      for (int j = 0; j < k; ++j) nw &= ((e.y ^ sw[j]) | 0x80808080u) - 0x01010101u;
+      m = prmt(nw, 0u, 0xBA98u);  // byte = 0xff iff its bit 7 is set (the server is new)
+    }
+    h8 += e.x;
+    d8 += e.x & m;
+    n8 += m & 0x01010101u;
+    srcany |= e.y;
   }
-  uq8 += n8 - ((srcany >> 7) & 0x01010101u);  // distinct remote destination servers per lane
-  hop16[0] += h8 & 0x00ff00ffu;
-  hop16[1] += (h8 >> 8) & 0x00ff00ffu;
-  dd16[0] += d8 & 0x00ff00ffu;
-  dd16[1] += (d8 >> 8) & 0x00ff00ffu;
+  n8 -= (srcany >> 7) & 0x01010101u;  // distinct remote destination servers per placement byte
+  r.h[0] = prmt(h8, 0u, 0x7270u);
+  r.h[1] = prmt(h8, 0u, 0x7371u);
+  r.d[0] = prmt(d8, 0u, 0x7270u);
+  r.d[1] = prmt(d8, 0u, 0x7371u);
+  r.u[0] = prmt(n8, 0u, 0x7270u);
+  r.u[1] = prmt(n8, 0u, 0x7371u);
+}
+
+template <bool FAST>
+__device__ __forceinline__ void dedup_warp_range(const uint8_t* __restrict__ plane, int64_t wm0, int64_t wm1,
+                                                 int64_t r0, int64_t r1, const int64_t* __restrict__ bounds, int C,
+                                                 uint32_t base, uint32_t slot, uint32_t slot8, uint32_t src, int lane,
+                                                 int64_t* __restrict__ hop_sums, int64_t* __restrict__ uniq_sums,
+                                                 int64_t* __restrict__ dedup_sums) {
+  constexpr int U = MP_DEDUP_U;
+  const int64_t wt0 = max(r0, 2 * wm0), wt1 = min(r1, 2 * wm1);
+  int c = 0;
+  {
+    int lo = 0, hi = C;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(bounds + mid) <= wt0) lo = mid; else hi = mid;
+    }
+    c = lo;
+  }
+  const int64_t T0 = 2 * wm0;
+  const int npairs = (int)(wm1 - wm0);
+  const int ra = (int)(wt0 - T0), rb = (int)(wt1 - T0);  // valid relative tokens [ra, rb)
+  const uint32_t T0lo = (uint32_t)T0;                      // 32-bit relative chunk starts
+  auto next_start = [&](int cc) { return (int)(__ldg(reinterpret_cast<const uint32_t*>(bounds + cc)) - T0lo); };
+  int nbr = next_start(c + 1);
+  // reduce-scatter<16> slot q = lane >> 1: values 0-3 hops, 4-7 unique servers, 8-11 dedup hops
+  const int qs = lane >> 1;
+  int64_t* hp = (qs < 4 ? hop_sums : qs < 8 ? uniq_sums : dedup_sums) + (int64_t)(qs & 3) * C + c;
+  uint32_t h16[2] = {0, 0}, u16[2] = {0, 0}, d16[2] = {0, 0};  // running sums of chunk c, u16 lanes
+  auto flush = [&]() {
+    uint32_t v[16] = {h16[0] & 0xffffu, h16[1] & 0xffffu, h16[0] >> 16, h16[1] >> 16,
+                      u16[0] & 0xffffu, u16[1] & 0xffffu, u16[0] >> 16, u16[1] >> 16,
+                      d16[0] & 0xffffu, d16[1] & 0xffffu, d16[0] >> 16, d16[1] >> 16, 0u, 0u, 0u, 0u};
+    h16[0] = h16[1] = u16[0] = u16[1] = d16[0] = d16[1] = 0;
+    int q = 0;
+    const uint32_t tot = warp_reduce_scatter<16>(v, lane, &q);
+    if ((lane & 1) == 0 && tot && q < 12) atomic_add_i64(hp, (int64_t)tot);
+  };
+  auto rec = [&](uint32_t w0, uint32_t w1, DedupRec& r) {
+    if constexpr (FAST) {
+      dedup_rec_fast(w0, w1, base, slot8, r);
+    } else {
+      uint32_t hh[2] = {0, 0}, dd[2] = {0, 0}, uq = 0;
+      dedup_record8(make_uint2(w0, w1), base, slot, src, hh, uq, dd);
+      r.h[0] = hh[0]; r.h[1] = hh[1]; r.d[0] = dd[0]; r.d[1] = dd[1];
+      r.u[0] = prmt(uq, 0u, 0x7270u);
+      r.u[1] = prmt(uq, 0u, 0x7371u);
+    }
+  };
+  auto mask = [&](DedupRec& r, bool keep) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      r.h[i] = keep ? r.h[i] : 0u;
+      r.u[i] = keep ? r.u[i] : 0u;
+      r.d[i] = keep ? r.d[i] : 0u;
+    }
+  };
+  auto add2 = [&](const DedupRec& a, const DedupRec& b) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      h16[i] += a.h[i] + b.h[i];
+      u16[i] += a.u[i] + b.u[i];
+      d16[i] += a.d[i] + b.d[i];
+    }
+  };
+  const uint4* __restrict__ pv = reinterpret_cast<const uint4*>(plane) + wm0;
+  auto window = [&](const uint4& x, int rfirst, bool edge) {
+    const int tA = 2 * (rfirst + lane);
+    DedupRec A, B;
+    rec(x.x, x.y, A);
+    rec(x.z, x.w, B);
+    if (edge) {
+      mask(A, tA >= ra && tA < rb);
+      mask(B, tA + 1 >= ra && tA + 1 < rb);
+    }
+    const int wlast = edge ? min(2 * rfirst + 63, rb - 1) : 2 * rfirst + 63;
+    while (nbr <= wlast) {  // boundary inside the window (warp-uniform): tokens < nbr are chunk c's
+      DedupRec pa = A, pb = B;
+      const bool inA = tA < nbr, inB = tA + 1 < nbr;
+      mask(pa, inA);
+      mask(pb, inB);
+      mask(A, !inA);
+      mask(B, !inB);
+      add2(pa, pb);
+      flush();
+      ++c;  // c < C - 1 here: bounds[C] >= the trace end > the window
+      ++hp;
+      nbr = next_start(c + 1);
+    }
+    add2(A, B);
+  };
+  // pairs [0, full) have both tokens valid when ra = 0; u16 headroom: 2 records x 2040 per window for
+  // the general path, so flush every 16 windows there and every 128 on the fast path (2 x 248)
+  constexpr int kFlushWin = FAST ? 128 : 16;
+  const int full = rb == 2 * npairs ? npairs : npairs - 1;
+  int rw = 0, nwin = 0;
+  if (ra != 0) {
+    const uint4 x = lane < npairs ? pv[lane] : make_uint4(0, 0, 0, 0);
+    window(x, 0, true);
+    rw = 32;
+    ++nwin;
+  }
+  for (; rw + 32 * U <= full; rw += 32 * U) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int4 v = ldg_stream(pv + rw + u * 32 + lane);
+      x[u] = make_uint4((uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) window(x[u], rw + u * 32, false);
+    if ((nwin += U) >= kFlushWin) {
+      flush();
+      nwin = 0;
+    }
+  }
+  for (; rw < npairs; rw += 32) {
+    const int r = rw + lane;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (r < npairs) {
+      const int4 v = ldg_stream(pv + r);
+      x = make_uint4((uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w);
+    }
+    window(x, rw, true);
+    if (++nwin >= kFlushWin) {
+      flush();
+      nwin = 0;
+    }
+  }
+  flush();
 }
 
 __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0,
@@ -148,112 +276,18 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
     __syncthreads();
     if (K == 8) {
       // Warp ranges (as in the segmented gather, csrc/seg.cu): the segment's token pairs are split
-      // into 16 contiguous warp ranges; a warp streams 32-pair windows (4 in flight), computes each
+      // into 16 contiguous warp ranges; a warp streams 32-pair windows (U in flight), computes each
       // record's contribution separately, keeps running sums of its current chunk and reduces them
-      // at every chunk boundary it crosses -- so short chunks cost one warp reduction per boundary
-      // instead of a pass of the whole CTA over every (layer, chunk) piece.
+      // at every chunk boundary it crosses; interior windows carry no per-lane validity logic.
       const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
       const int64_t m0 = r0 >> 1, m1 = (r1 + 1) >> 1;
       const int64_t perw = (m1 - m0 + nwarps - 1) / nwarps;
       const int64_t wm0 = min(m1, m0 + perw * warp), wm1 = min(m1, wm0 + perw);
       if (wm0 < wm1) {
-        const int64_t wt0 = max(r0, 2 * wm0), wt1 = min(r1, 2 * wm1);
-        int c = 0;
-        {
-          int lo = 0, hi = C;
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (__ldg(bounds + mid) <= wt0) lo = mid; else hi = mid;
-          }
-          c = lo;
-        }
-        const int64_t T0 = 2 * wm0;
-        const int npairs = (int)(wm1 - wm0);
-        const int ra = (int)(wt0 - T0), rb = (int)(wt1 - T0);
-        auto rel = [&](int64_t x) { return (int)min(x - T0, (int64_t)0x7fffffff); };
-        int nbr = rel(__ldg(bounds + c + 1));
-        uint32_t h16[2] = {0, 0}, d16[2] = {0, 0}, u8 = 0;          // running, narrow lanes
-        uint32_t hop[4] = {0, 0, 0, 0}, uq[4] = {0, 0, 0, 0}, dd[4] = {0, 0, 0, 0};  // running, u32
-        int since = 0, recs = 0;
-        auto widen = [&]() {
-          hop[0] += h16[0] & 0xffffu; hop[2] += h16[0] >> 16; hop[1] += h16[1] & 0xffffu; hop[3] += h16[1] >> 16;
-          dd[0] += d16[0] & 0xffffu; dd[2] += d16[0] >> 16; dd[1] += d16[1] & 0xffffu; dd[3] += d16[1] >> 16;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) uq[q] += (u8 >> (8 * q)) & 0xffu;
-          h16[0] = h16[1] = d16[0] = d16[1] = u8 = 0;
-        };
-        auto flush = [&](int cc) {  // warp-uniform: running sums of chunk cc -> the three outputs
-          widen();
-          uint32_t v[16] = {hop[0], hop[1], hop[2], hop[3], uq[0], uq[1], uq[2], uq[3],
-                            dd[0], dd[1], dd[2], dd[3], 0u, 0u, 0u, 0u};
-          int q = 0;
-          const uint32_t tot = warp_reduce_scatter<16>(v, lane, &q);
-          if ((lane & 1) == 0 && tot && q < 12) {
-            int64_t* dst = q < 4 ? hop_sums : q < 8 ? uniq_sums : dedup_sums;
-            atomic_add_i64(dst + (int64_t)(q & 3) * C + cc, (int64_t)tot);
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) hop[i] = uq[i] = dd[i] = 0;
-          recs = 0;
-        };
-        auto rec = [&](uint2 w, uint32_t (&h_)[2], uint32_t& u_, uint32_t (&d_)[2]) {
-          if (fast) dedup_record8_fast(w, base, slot8, h_, u_, d_);
-          else dedup_record8(w, base, slot, src, h_, u_, d_);
-        };
-        auto add_rec = [&](const uint32_t (&h_)[2], uint32_t u_, const uint32_t (&d_)[2]) {
-          h16[0] += h_[0]; h16[1] += h_[1]; d16[0] += d_[0]; d16[1] += d_[1]; u8 += u_;
-        };
-        const uint4* __restrict__ pv = reinterpret_cast<const uint4*>(plane) + wm0;
-        for (int rw = 0; rw < npairs; rw += 32 * MP_DEDUP_U) {
-          uint4 x[MP_DEDUP_U];
-#pragma unroll
-          for (int u = 0; u < MP_DEDUP_U; ++u) {
-            const int r = rw + u * 32 + lane;
-            if (r < npairs) {
-              const int4 vv = ldg_stream(pv + r);
-              x[u] = make_uint4((uint32_t)vv.x, (uint32_t)vv.y, (uint32_t)vv.z, (uint32_t)vv.w);
-            } else {
-              x[u] = make_uint4(0, 0, 0, 0);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < MP_DEDUP_U; ++u) {
-            const int rfirst = rw + u * 32;
-            if (rfirst >= npairs) break;  // warp-uniform
-            const int r = rfirst + lane;
-            const int tA = 2 * r, tB = tA + 1;
-            const bool vA = r < npairs && tA >= ra && tA < rb;
-            const bool vB = r < npairs && tB >= ra && tB < rb;
-            uint32_t hA[2] = {0, 0}, dA[2] = {0, 0}, uA = 0, hB[2] = {0, 0}, dB[2] = {0, 0}, uB = 0;
-            rec(make_uint2(x[u].x, x[u].y), hA, uA, dA);
-            rec(make_uint2(x[u].z, x[u].w), hB, uB, dB);
-            const int wlast = min(2 * (rfirst + 31) + 1, rb - 1);
-            if (nbr > wlast) {
-              if (vA) add_rec(hA, uA, dA);
-              if (vB) add_rec(hB, uB, dB);
-            } else {
-              bool doneA = !vA, doneB = !vB;
-              while (nbr <= wlast) {  // boundary inside the window: records < nb belong to chunk c
-                if (!doneA && tA < nbr) { add_rec(hA, uA, dA); doneA = true; }
-                if (!doneB && tB < nbr) { add_rec(hB, uB, dB); doneB = true; }
-                flush(c);
-                since = 0;
-                ++c;  // c < C - 1 here: bounds[C] >= the trace end > the window
-                nbr = rel(__ldg(bounds + c + 1));
-              }
-              if (!doneA) add_rec(hA, uA, dA);
-              if (!doneB) add_rec(hB, uB, dB);
-            }
-            // narrow lanes: u16 hop/dedup sums take 8 records (8 x 8 x 255 < 2^16), u8 unique counts 31
-            if (++since == 4) {
-              widen();
-              since = 0;
-              // u32 running sums: a warp's total over 32 lanes x 2^15 records x 2040 stays below 2^32
-              if ((recs += 8) >= (1 << 15)) flush(c);
-            }
-          }
-        }
-        flush(c);
+        if (fast) dedup_warp_range<true>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
+                                         hop_sums, uniq_sums, dedup_sums);
+        else dedup_warp_range<false>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
+                                     hop_sums, uniq_sums, dedup_sums);
       }
       g += r1 - r0;
       continue;
