@@ -112,13 +112,15 @@ struct Flat {
   int64_t nb;     // bytes per plane in range
   int64_t b0;     // first byte (within a plane)
   int64_t g0, g1; // this CTA's flattened range
-  __device__ Flat(int64_t b0_, int64_t b1_, int L) {
+  __device__ Flat(int64_t b0_, int64_t b1_, int L) : Flat(b0_, b1_, L, (int)blockIdx.x, (int)gridDim.x) {}
+  // range `idx` of `n` (a kernel whose CTAs hold several independent workers)
+  __device__ Flat(int64_t b0_, int64_t b1_, int L, int idx, int n) {
     b0 = b0_;
     nb = b1_ - b0_;
     int64_t total = nb * (int64_t)L;
-    int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    int64_t per = (total + n - 1) / n;
     per = (per + 15) & ~(int64_t)15;
-    g0 = min(total, (int64_t)blockIdx.x * per);
+    g0 = min(total, (int64_t)idx * per);
     g1 = min(total, g0 + per);
   }
 };

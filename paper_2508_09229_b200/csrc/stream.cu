@@ -430,9 +430,23 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
 #ifndef MP_PIPE_GTAIL4
 #define MP_PIPE_GTAIL4 1  // guarded 4-vector tail batches (C = 3000: hist_chunks 1.905 -> 1.472, W = 4 pass 2.10 -> 1.80 ms)
 #endif
+// MP_PIPE_SPLIT (default): one CTA of 1024 threads per SM made of two independent 512-thread halves
+// whose sets interleave in 256-byte rows (half h at bytes h*128..h*128+127 of row e), so the bins of
+// one warp's ATOMS are 256 B apart and share address bit 7.  microbench9 (i.i.d. Zipf bytes,
+// profiles/r2_microbench9_atoms_pitch.txt): 128-byte pitch 0.763 ms per 4.64 GB, 256-byte pitch
+// 0.731 ms.  In this kernel the gain is smaller (fused step 0.854 -> 0.846 ms, W = 4 at C = 1500
+// 1.329 -> 1.238; hist+8 placements at C = 150 0.870 -> 0.901), and ncu's aggregate ATOMS conflict
+// counter stays at ~18 % of ATOMS while the per-instruction source view shows ideal wavefronts.
+// Occupancy is unchanged (32 warps per SM).  MP_PIPE_SPLIT=0 builds the 2 x 512-thread CTA kernel.
+#ifndef MP_PIPE_SPLIT
+#define MP_PIPE_SPLIT 1
+#endif
 constexpr int kPipeSets = 3;
-constexpr int kPipeSetBytes = 256 * 128;
+constexpr int kPipeHalves = MP_PIPE_SPLIT ? 2 : 1;
+constexpr int kPipeRow = 128 * kPipeHalves;                 // bytes per expert row of one set
+constexpr int kPipeSetBytes = 256 * kPipeRow;
 constexpr int kPipeSmem = kPipeSets * kPipeSetBytes;
+constexpr int kPipeThreads = kThreads * kPipeHalves;
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -447,14 +461,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
       : "memory");
 }
 
-// ATOMS increments for bytes [xa, xb) of one plane into the set at shared address sb (= set base + lane*4)
+// ATOMS increments for bytes [xa, xb) of one plane; sb = shared address of this lane's replica of bin 0 in the piece's set (bin e at sb + e * kPipeRow)
 template <int UNROLL>
-__device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb, uint32_t sb) {
-  const uint32_t tid = threadIdx.x, T = blockDim.x;
+__device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb, uint32_t sb,
+                                           uint32_t tid) {
+  constexpr uint32_t T = kThreads;  // threads of one (half-)CTA
   const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
   const int64_t tb = max(ha, xb & ~(int64_t)15);
-  for (int64_t x = xa + tid; x < ha; x += T) atoms_inc(sb + ((uint32_t)plane[x] << 7));
-  for (int64_t x = tb + tid; x < xb; x += T) atoms_inc(sb + ((uint32_t)plane[x] << 7));
+  for (int64_t x = xa + tid; x < ha; x += T) atoms_inc(sb + (uint32_t)plane[x] * (uint32_t)kPipeRow);
+  for (int64_t x = tb + tid; x < xb; x += T) atoms_inc(sb + (uint32_t)plane[x] * (uint32_t)kPipeRow);
   const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
   const uint32_t nv = (uint32_t)((tb - ha) >> 4);
   auto vec = [&](const int4& x) {
@@ -462,7 +477,7 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) atoms_inc(prmt(wd[q], 0u, 0x4440u | (uint32_t)b) * 128u + sb);
+      for (int b = 0; b < 4; ++b) atoms_inc(prmt(wd[q], 0u, 0x4440u | (uint32_t)b) * (uint32_t)kPipeRow + sb);
   };
   uint32_t v = tid;
   for (; v + (UNROLL - 1) * T < nv; v += UNROLL * T) {
@@ -497,24 +512,26 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
 // WC == 0: per-chunk histogram, counts is int64 [C][L][E].  WC > 0: count-contract with WC-word
 // tables; counts (nullable) is int64 [L][E] and hop_sums int64 [4*WC][C].
 template <int WC, int UNROLL>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kPipeThreads, 2 / kPipeHalves)
 pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
             const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
             int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
-  extern __shared__ __align__(128) uint8_t sm[];  // kPipeSets x 256 rows x 128 B
-  __shared__ __align__(8) uint64_t bar[kPipeSets];
+  extern __shared__ __align__(128) uint8_t sm[];  // kPipeSets x 256 rows x kPipeRow B
+  __shared__ __align__(8) uint64_t bar[kPipeHalves][kPipeSets];
   constexpr int PC = 4 * (WC > 0 ? WC : 1);
   const int lane = threadIdx.x & 31;
-  const uint32_t base = smem_addr(sm);
-  const uint32_t bar0 = smem_addr(bar);
-  uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
-  for (int i = threadIdx.x; i < kPipeSmem / 4; i += blockDim.x) smw[i] = 0;
-  if (threadIdx.x == 0)
-    for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, blockDim.x);
+  const int half = kPipeHalves > 1 ? (int)(threadIdx.x >> 9) : 0;  // independent 512-thread halves
+  const uint32_t tid = threadIdx.x & (kThreads - 1);
+  const uint32_t base0 = smem_addr(sm);
+  const uint32_t bar0 = smem_addr(&bar[half][0]);
+  uint32_t* smw = reinterpret_cast<uint32_t*>(sm) + half * 32;
+  for (int i = threadIdx.x; i < kPipeSmem / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (tid == 0)
+    for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, kThreads);
   __syncthreads();
 
   // flush roles: two threads per bin (16 replicas each, rotated: a warp's 32 loads hit 32 banks)
-  const int fe = threadIdx.x >> 1, fh = threadIdx.x & 1;
+  const int fe = (int)(tid >> 1), fh = (int)(tid & 1);
   uint32_t snap[kPipeSets] = {0u, 0u, 0u};
   // piece k-1 awaiting its flush
   int pk = -1, pl = 0, pc = 0;
@@ -524,7 +541,7 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
     mbar_wait(bar0 + 8 * set, (uint32_t)((pk / kPipeSets) & 1));  // every thread finished counting piece pk
     uint32_t part = 0;
     if (fe < 256) {
-      const uint32_t* row = smw + set * (kPipeSetBytes / 4) + fe * 32;
+      const uint32_t* row = smw + set * (kPipeSetBytes / 4) + fe * (kPipeRow / 4);
 #pragma unroll
       for (int i = 0; i < 16; ++i) part += row[(fh * 16 + i + fe) & 31];
     }
@@ -561,8 +578,8 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
     }
   };
 
-  int k = 0;  // this CTA's piece counter
-  Flat f(t0 * K, t1 * K, L);
+  int k = 0;  // this (half-)CTA's piece counter
+  Flat f(t0 * K, t1 * K, L, (int)blockIdx.x * kPipeHalves + half, (int)gridDim.x * kPipeHalves);
   for (int64_t g = f.g0; g < f.g1;) {
     const int l = (int)(g / f.nb);
     const int64_t off_in = g - (int64_t)l * f.nb;
@@ -580,7 +597,7 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
       while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
       const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
       const int set = k % kPipeSets;
-      pipe_count<UNROLL>(plane, x, xe, base + (uint32_t)(set * kPipeSetBytes) + (uint32_t)(lane << 2));
+      pipe_count<UNROLL>(plane, x, xe, base0 + (uint32_t)(set * kPipeSetBytes + half * 128 + (lane << 2)), tid);
       if (pk >= 0) flush_prev();
       mbar_arrive(bar0 + 8 * set);  // counted piece k, flushed piece k-1
       pk = k++;
@@ -607,15 +624,15 @@ static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kPipeSmem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, kPipeSmem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t total = (t1 - t0) * (int64_t)K * L;
   int64_t grid = (int64_t)nsm * per_sm;
-  const int64_t min_bytes_per_cta = 64 * 1024;
+  const int64_t min_bytes_per_cta = 64 * 1024 * kPipeHalves;
   grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
-  kern<<<(unsigned)grid, kThreads, kPipeSmem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
-                                                    hop_sums, err);
+  kern<<<(unsigned)grid, kPipeThreads, kPipeSmem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
+                                                        hop_sums, err);
   return cudaGetLastError();
 }
 
