@@ -35,6 +35,29 @@ __global__ void fill_kernel(uint8_t* t, int64_t n, const uint32_t* cdf, uint32_t
     reinterpret_cast<uint32_t*>(t)[i] = out;
   }
 }
+// 8 distinct Zipf draws per aligned 8-byte record (as the trace generator produces), in draw order
+// (mode 1) or sorted by expert id (mode 2)
+__global__ void fill_records_kernel(uint8_t* t, int64_t n, const uint32_t* cdf, uint32_t total, int mode) {
+  __shared__ uint32_t s_cdf[257];
+  for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdf[i] = cdf[i];
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n / 8; r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t e[8]; int got = 0; uint32_t ctr = 0;
+    while (got < 8) {
+      uint32_t x = mix32((uint32_t)(r * 64 + ctr++) * 0x9e3779b9U ^ (uint32_t)(r >> 26)) % total;
+      int lo = 0, hi = 256;
+      while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_cdf[mid] <= x) lo = mid; else hi = mid; }
+      uint32_t v = (uint32_t)(lo * 167) & 255u; bool dup = false;
+      for (int j = 0; j < got; ++j) dup |= e[j] == v;
+      if (!dup) e[got++] = v;
+    }
+    if (mode == 2)
+      for (int i = 1; i < 8; ++i) for (int j = i; j > 0 && e[j - 1] > e[j]; --j) { uint32_t tmp = e[j]; e[j] = e[j - 1]; e[j - 1] = tmp; }
+    uint2 w = make_uint2(0, 0);
+    for (int j = 0; j < 4; ++j) { w.x |= e[j] << (8 * j); w.y |= e[4 + j] << (8 * j); }
+    reinterpret_cast<uint2*>(t)[r] = w;
+  }
+}
 __device__ __forceinline__ int4 ldg_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
@@ -107,13 +130,17 @@ int main(int argc, char** argv) {
   uint8_t* t; uint32_t* dc; unsigned long long* out;
   CK(cudaMalloc(&t, n)); CK(cudaMalloc(&dc, 257 * 4)); CK(cudaMalloc(&out, 8));
   CK(cudaMemcpy(dc, cdf.data(), 257 * 4, cudaMemcpyHostToDevice));
-  fill_kernel<<<148 * 8, 256>>>(t, n, dc, T); CK(cudaDeviceSynchronize());
+  const int mode = argc > 2 ? atoi(argv[2]) : 0;  // 0 i.i.d. bytes, 1 distinct records, 2 sorted records
+  if (mode == 0) fill_kernel<<<148 * 8, 256>>>(t, n, dc, T);
+  else fill_records_kernel<<<148 * 8, 256>>>(t, n, dc, T, mode);
+  CK(cudaDeviceSynchronize());
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = nsm * 2; const int64_t nvec = n / 16;
   const char* names[] = {"pitch128 (pipe_kernel)", "pitch256 lower half", "pitch256 upper half (seg W=1)",
                          "pitch128 lane^e rotated", "pitch128 alt arithmetic"};
   float ms[5] = {run<0>((int4*)t, nvec, out, grid), run<1>((int4*)t, nvec, out, grid), run<2>((int4*)t, nvec, out, grid),
                  run<3>((int4*)t, nvec, out, grid), run<4>((int4*)t, nvec, out, grid)};
-  for (int i = 0; i < 5; ++i) printf("zipf %.1f  %-32s %.3f ms  %.1f GB/s\n", s, names[i], ms[i], n / (ms[i] * 1e6));
+  const char* modes[] = {"iid bytes", "distinct records", "sorted records"};
+  for (int i = 0; i < 5; ++i) printf("zipf %.1f %-17s %-32s %.3f ms  %.1f GB/s\n", s, modes[mode], names[i], ms[i], n / (ms[i] * 1e6));
   return 0;
 }
