@@ -9,9 +9,10 @@
  *
  * Conventions (all functions):
  *   - Plain pointers and sizes only.  Device pointers are CUDA global-memory addresses; the
- *     caller owns every buffer (inputs, outputs, scratch).  The library never allocates,
- *     frees, or keeps global mutable state, and is safe to call concurrently on different
- *     streams.
+ *     caller owns every buffer (inputs, outputs, scratch).  The library never allocates or
+ *     frees device memory; its only global state is a mutex-guarded cache of per-device launch
+ *     facts (SM count, each kernel's resident CTAs, its shared-memory attribute), filled on a
+ *     device's first launch.  Safe to call concurrently on different streams.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
  *     function only ENQUEUES work; nothing synchronises the host.
  *   - Integer outputs are ACCUMULATED (`+=`): the caller zeroes them.  This makes sharded

@@ -1,6 +1,9 @@
 // Shared device helpers for the moeplace sm_100a kernels.
 #pragma once
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cuda_runtime.h>
 #include "../../include/moeplace_cuda.h"
 
@@ -124,5 +127,46 @@ struct Flat {
     g1 = min(total, g0 + per);
   }
 };
+
+// ---- host-side launch facts, queried once per device (and kernel) instead of on every launch:
+// the streamed end-to-end path launches once per 1M-token slice.  The cache holds only device
+// properties and occupancy results; it never owns device memory.
+inline int device_sm_count() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cache[64] = {0};  // benign race: every writer stores the same value
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
+}
+
+// cudaFuncSetAttribute(max dynamic shared memory) once per (device, kernel, size); *per_sm = resident
+// CTAs per SM at (threads, smem), from cudaOccupancyMaxActiveBlocksPerMultiprocessor (cached).
+inline cudaError_t prepare_kernel(const void* kern, int threads, int smem, int* per_sm) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, kern, threads, smem);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end()) {
+      *per_sm = it->second;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int n = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = n;
+  *per_sm = n;
+  return cudaSuccess;
+}
 
 }  // namespace mp

@@ -319,9 +319,7 @@ cudaError_t launch_count_digits_u8(const int64_t* counts, int C, int64_t LE, int
 cudaError_t launch_contract_tc(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig,
                                int64_t LE, int64_t ldd, int64_t* out, int ctas, cudaStream_t s) {
   if (P <= 0 || C <= 0 || LE <= 0) return cudaSuccess;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sm_count();
   TcArgs a;
   a.P = P;
   a.C = C;
@@ -354,7 +352,8 @@ cudaError_t launch_contract_tc(const uint8_t* pe, int P, int64_t ldpe, const uin
   if (!make_map(&tm_dig, digits, (uint64_t)LE, (uint64_t)a.n_cols, (uint64_t)ldd, (uint32_t)a.box_rows))
     return cudaErrorInvalidValue;
   const int smem = a.stages * stage_bytes + epi_bytes + 1024;
-  cudaError_t e = cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaError_t e = prepare_kernel((const void*)contract_tc_kernel, kTcThreads2, smem, &per_sm);
   if (e != cudaSuccess) return e;
   contract_tc_kernel<<<dim3((unsigned)g, (unsigned)n_tiles), kTcThreads2, smem, s>>>(tm_pe, tm_dig, a);
   return cudaGetLastError();

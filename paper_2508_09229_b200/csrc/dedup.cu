@@ -350,12 +350,10 @@ cudaError_t launch_dedup(const uint8_t* planes, int64_t stride, int64_t t0, int6
                          const uint8_t* src_srv, int64_t* hop_sums, int64_t* uniq_sums, int64_t* dedup_sums,
                          cudaStream_t s) {
   const int smem = 256 * 256;
-  cudaError_t e = cudaFuncSetAttribute(dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaError_t e = prepare_kernel((const void*)dedup_kernel, kDedupThreads, smem, &per_sm);
   if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dedup_kernel, kDedupThreads, smem);
+  const int nsm = device_sm_count();
   const int64_t records = (t1 - t0) * (int64_t)L;
   int64_t grid = (int64_t)nsm * max(1, per_sm);
   grid = max((int64_t)1, min(grid, (records + 4095) / 4096));

@@ -177,9 +177,7 @@ cudaError_t launch_gen(uint64_t seed, int64_t t0, int64_t t1, int L, int K, int 
                        const uint8_t* perm, uint8_t* planes, int64_t stride, cudaStream_t s) {
   const int64_t n = t1 - t0;
   if (n <= 0) return cudaSuccess;
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   const int64_t want = (n + 255) / 256;
   const unsigned gx = (unsigned)max((int64_t)1, min(want, (int64_t)nsm * 16 / max(1, L) + 1));
   dim3 grid(gx, L);
@@ -220,9 +218,7 @@ cudaError_t launch_validate(const uint8_t* planes, int64_t stride, int64_t t0, i
                             int64_t* err, cudaStream_t s) {
   const int64_t n = t1 - t0;
   if (n <= 0) return cudaSuccess;
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   const unsigned gx = (unsigned)max((int64_t)1, min((n + 255) / 256, (int64_t)nsm * 16 / max(1, L) + 1));
   validate_kernel<<<dim3(gx, L), 256, 0, s>>>(planes, stride, t0, t1, L, K, E, err);
   return cudaGetLastError();

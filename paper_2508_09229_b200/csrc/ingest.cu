@@ -60,15 +60,12 @@ __global__ void tok2planes_any(const uint8_t* __restrict__ tok, int64_t n, int L
 cudaError_t launch_tokens_to_planes(const uint8_t* tok, int64_t n, int L, int K, uint8_t* planes, int64_t stride,
                                     int64_t t_out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sm_count();
   if (K == 8 && ((uintptr_t)tok & 7) == 0) {
     const size_t smem = (size_t)kTT * (L | 1) * 8;
-    if (smem > 48 * 1024) {
-      const cudaError_t e = cudaFuncSetAttribute(tok2planes_k8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
+    int per_sm = 0;
+    const cudaError_t e = prepare_kernel((const void*)tok2planes_k8, kIngestThreads, (int)smem, &per_sm);
+    if (e != cudaSuccess) return e;
     const int64_t tiles = (n + kTT - 1) / kTT;
     const int grid = (int)std::min(tiles, (int64_t)sms * 6);
     tok2planes_k8<<<grid, kIngestThreads, smem, s>>>(reinterpret_cast<const uint64_t*>(tok), n, L,

@@ -174,9 +174,7 @@ cudaError_t launch_find_nl(const uint8_t* text, int64_t n, const int64_t* offset
 cudaError_t launch_parse(const uint8_t* text, const int64_t* ends, int64_t first_start, int64_t n_lines, int L, int K,
                          int E, uint8_t* planes, int64_t stride, int64_t* chunk_ids, int64_t* err, cudaStream_t s) {
   if (n_lines <= 0) return cudaSuccess;
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   const int64_t want = (n_lines + 255) / 256;
   parse_kernel<<<(unsigned)min(want, (int64_t)nsm * 8), 256, 0, s>>>(text, ends, first_start, n_lines, L, K, E, planes,
                                                                       stride, chunk_ids, err);
@@ -237,9 +235,7 @@ cudaError_t launch_format(bool write, const uint8_t* planes, int64_t stride, int
                           const int64_t* cids, int64_t* lens_or_offsets, uint8_t* out, cudaStream_t s) {
   const int64_t n = t1 - t0;
   if (n <= 0) return cudaSuccess;
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   const unsigned grid = (unsigned)min((n + 255) / 256, (int64_t)nsm * 16);
   if (write) format_kernel<true><<<grid, 256, 0, s>>>(planes, stride, t0, n, L, K, cids, lens_or_offsets, out);
   else format_kernel<false><<<grid, 256, 0, s>>>(planes, stride, t0, n, L, K, cids, lens_or_offsets, out);

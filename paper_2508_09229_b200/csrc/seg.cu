@@ -266,13 +266,10 @@ static cudaError_t launch_seg_t(const uint8_t* planes, int64_t stride, int64_t t
                                 int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   auto kern = seg_kernel<W, HIST>;
   const int smem = 256 * 256 + ((HIST && W > 1) ? 256 * 128 : 0) + 128;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaError_t e = prepare_kernel((const void*)kern, kThreads, smem, &per_sm);
   if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-  if (e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
   const int64_t total = (t1 - t0) * 8 * (int64_t)L;
   int64_t grid = (int64_t)nsm * max(1, per_sm);
   grid = max((int64_t)1, min(grid, (total + 65535) / 65536));

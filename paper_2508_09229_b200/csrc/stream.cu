@@ -397,13 +397,10 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
                             int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   constexpr int UNROLL = W == 0 ? MP_COUNT_UNROLL : MP_GATHER_UNROLL;  // vectors per thread per iteration
   auto kern = stream_kernel<HIST, W, WIDEN, UNROLL, CHUNKED, WC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  int per_sm = 0;
+  cudaError_t e = prepare_kernel((const void*)kern, kThreads, kSmemBytes, &per_sm);
   if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmemBytes);
-  if (e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
   if (per_sm < 1) per_sm = 1;
   // grid: persistent, one wave of resident CTAs; small inputs get fewer CTAs
   const int64_t total = (t1 - t0) * (int64_t)K * L;
@@ -619,13 +616,10 @@ static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0
                                const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                                int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   auto kern = pipe_kernel<WC, MP_COUNT_UNROLL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmem);
+  int per_sm = 0;
+  cudaError_t e = prepare_kernel((const void*)kern, kPipeThreads, kPipeSmem, &per_sm);
   if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, kPipeSmem);
-  if (e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
   if (per_sm < 1) per_sm = 1;
   const int64_t total = (t1 - t0) * (int64_t)K * L;
   int64_t grid = (int64_t)nsm * per_sm;

@@ -255,9 +255,8 @@ static cudaError_t run_score_tok(int nsm, const uint8_t* planes, int64_t stride,
                                  cudaStream_t s) {
   const int smem = 256 * 256;
   int per_sm = 0;
-  cudaError_t e = cudaFuncSetAttribute(score_tok_kernel<K8, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const cudaError_t e = prepare_kernel((const void*)score_tok_kernel<K8, ACC>, kTokThreads, smem, &per_sm);
   if (e != cudaSuccess) return e;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_tok_kernel<K8, ACC>, kTokThreads, smem);
   const int64_t tiles = (n + (int64_t)kTPT * kTokThreads - 1) / ((int64_t)kTPT * kTokThreads);
   const int64_t grid = max((int64_t)1, min(tiles, (int64_t)nsm * max(1, per_sm)));
   for (int w = 0; w < W; ++w)  // one pass per table word (4 placements each)
@@ -271,9 +270,7 @@ cudaError_t launch_score_tok(const uint8_t* planes, int64_t stride, int64_t t0, 
                              cudaStream_t s) {
   const int64_t n = t1 - t0;
   if (n <= 0) return cudaSuccess;
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   if (K == 8 && max_p <= 31) return run_score_tok<true, 8>(nsm, planes, stride, t0, n, L, K, bounds, C, tables, W, hop_sums, s);
   if (K == 8 && max_p <= 63) return run_score_tok<true, 4>(nsm, planes, stride, t0, n, L, K, bounds, C, tables, W, hop_sums, s);
   if (K == 8) return run_score_tok<true, 1>(nsm, planes, stride, t0, n, L, K, bounds, C, tables, W, hop_sums, s);
@@ -285,8 +282,7 @@ static void run_token_hops(int64_t tiles, int nsm, const uint8_t* planes, int64_
                            int L, int K, const uint32_t* rep, uint32_t* hops, cudaStream_t s) {
   const int smem = 256 * 256;  // two interleaved table buffers
   int per_sm = 0;
-  cudaFuncSetAttribute(token_hops_kernel<K8, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, token_hops_kernel<K8, ACC>, kTokThreads, smem);
+  prepare_kernel((const void*)token_hops_kernel<K8, ACC>, kTokThreads, smem, &per_sm);
   const int64_t grid = max((int64_t)1, min(tiles, (int64_t)nsm * max(1, per_sm)));
   token_hops_kernel<K8, ACC><<<(unsigned)grid, kTokThreads, smem, s>>>(planes, stride, t0, n, L, K, rep, hops);
 }
@@ -296,9 +292,7 @@ cudaError_t launch_token_hops(const uint8_t* planes, int64_t stride, int64_t t0,
                               cudaStream_t s) {
   const int64_t n = t1 - t0;
   if (n <= 0) return cudaSuccess;
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   const int64_t nrep = (int64_t)L * 256 * 32;
   replicate_kernel<<<(unsigned)min((nrep + 255) / 256, (int64_t)4096), 256, 0, s>>>(tables, L, replicated);
   const int64_t tiles = (n + (int64_t)kTPT * kTokThreads - 1) / ((int64_t)kTPT * kTokThreads);
