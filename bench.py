@@ -760,7 +760,13 @@ def main():
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based Zipf generator, seed 0)",
                 "config": cfg, "engine": engine, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
                 "e2e": e2e, "gpu_launches": launches * args.steps, "clocks": clocks, "sustained": sustained,
-                "passes": passes, "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9}
+                "passes": passes, "hbm_gbs_step": n * L * K / (ms / 1e3) / 1e9,
+                # `value` counts token-layers x placements as BASELINE.json's metric names it; with
+                # count-contract / factorized scoring a placement costs O(C*L*E) per (layer, chunk)
+                # piece, not per token, so the per-byte rate is value / placements (and hbm_gbs_step)
+                "token_layers_per_s": n_total * L / (ms / 1e3), "placements": P_,
+                "value_note": "value = token-layers x placements per second (BASELINE metric); the trace "
+                              "bytes processed per second are token_layers_per_s x K = hbm_gbs_step x N GPUs"}
         emit(line)
     if world > 1:
         dist.destroy_process_group()
