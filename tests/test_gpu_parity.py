@@ -388,7 +388,10 @@ def test_token_major_host_streaming_matches_device(monkeypatch, shape):
     (R1, "FatTree", (4, 2, 4)), (B16, "Dragonfly", (4, 2, 4)), ((3, 16, 5), "DragonflySparse", (4, 2, 4)),
     # K = 8 general path: pe bytes up to 36 in some layers (fast and general layers mixed), and
     # 130 servers (ids >= 128)
-    (R1, "DragonflySparse", (64, 1, 1)), (R1, "FatTree", (65, 2, 1))])
+    (R1, "DragonflySparse", (64, 1, 1)), (R1, "FatTree", (65, 2, 1)),
+    # one-hot path (every server id < 32, costs <= 15): config 2's 32-server FatTree; 32 servers of a
+    # sparse dragonfly whose larger costs send some layers back to the pairwise path
+    (R1, "FatTree", (8, 4, 8)), (R1, "DragonflySparse", (32, 1, 1))])
 def test_dedup_matches_oracle(shape, kind, size):
     """Extension A17: unique destination servers and deduplicated hops, bit-exact vs the oracle;
     the SPEC hop sums produced alongside equal mp_score_u8's."""

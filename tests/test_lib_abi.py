@@ -123,3 +123,23 @@ def test_integration_stub_matches_the_abi():
     for name, args in found:
         got = [names[a.strip()] for a in args.split(",")]
         assert got == list(_lib.SIGNATURES[name][1]), name
+
+
+def test_auto_algorithm_rule():
+    """mp_choose_algo (host-only) is the rule MP_ALGO_AUTO applies: the crossovers measured for R1
+    (profiles/r2_chunk_granularity.txt) -- count-contract / gather for long chunks, the segmented
+    gather for dialog-length ones, the token walk only for the shortest score-only chunks."""
+    N, L, K = 10_000_000, 58, 8
+    tpc = {150: 66_667, 1500: 6667, 2000: 5000, 71_429: 140, 150_000: 67}
+    want = {  # (hist, W): algorithm per chunk count
+        (True, 1): {150: "count", 1500: "count", 2000: "seg", 71_429: "seg", 150_000: "seg"},
+        (False, 1): {150: "gather", 1500: "seg", 2000: "seg", 71_429: "seg", 150_000: "token"},
+        (False, 4): {150: "count", 1500: "count", 2000: "count", 71_429: "seg", 150_000: "seg"},
+        (True, 4): {150: "count", 1500: "count", 2000: "count", 71_429: "seg", 150_000: "seg"},
+    }
+    for (hist, W), row in want.items():
+        for C, algo in row.items():
+            assert _lib.choose_algo(hist, W, N, C, L, K, 8) == algo, (hist, W, C, tpc[C])
+    # SEG needs K = 8 and costs <= 31; otherwise the token walk / streaming algorithms apply
+    assert _lib.choose_algo(False, 1, N, 71_429, L, K, 40) in ("token", "gather")
+    assert _lib.choose_algo(True, 1, N, 150, L, 6, 8) == "count"
