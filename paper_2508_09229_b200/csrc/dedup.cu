@@ -55,6 +55,13 @@ __device__ __forceinline__ void dedup_record8(uint2 v, uint32_t base, uint32_t s
 }
 
 constexpr int kDedupThreads = 512;
+// One-hot server masks for layers whose server ids are < 32 and costs <= 15, built
+// and measured against the pairwise tests: 3.587 vs 3.420 ms at 150 chunks, 3.70 vs 3.56 at 15k,
+// 5.03 vs 4.98 at 150k (R1 10M, FatTree 8x4x8; ncu: L1TEX 85 %, 833M shared wavefronts -- the 4
+// LDS.128 wavefronts per pick -- and ALU 71 %), so it is off by default (-DMP_DEDUP_ONEHOT=1 builds it).
+#ifndef MP_DEDUP_ONEHOT
+#define MP_DEDUP_ONEHOT 0
+#endif
 #ifndef MP_DEDUP_U
 #define MP_DEDUP_U 2  // 32-pair windows in flight per warp (K = 8 warp-range path)
 #endif
@@ -98,13 +105,60 @@ __device__ __forceinline__ void dedup_rec_fast(uint32_t w0, uint32_t w1, uint32_
   r.u[1] = prmt(n8, 0u, 0x7371u);
 }
 
-template <bool FAST>
+// One-hot K = 8 record (every server id < 32 and pe byte <= 31 in the layer; the variant VERDICT r1
+// asked to be built and measured).  Row e: bytes 0-127 hold {onehot_q0 .. onehot_q3} (1 << server of
+// expert e under placement q) at slot (lane & 7) * 16 -- one LDS.128 per pick, a quarter-warp per
+// wavefront -- and bytes 128-255 the pe word at 128 + lane * 4.  The record's server sets are the OR
+// of its 8 masks; distinct remote servers = popc(set & ~source); deduplicated hops =
+// sum_b popc(set & plane_b) << b with plane_b = the servers whose cost has bit b (per layer and
+// placement, built by the CTA).
+struct __align__(16) OnehotLayer {
+  uint32_t plane[4][4];  // [q][bit]: costs <= 15 (a layer with a larger cost takes the pairwise path)
+  uint32_t src;          // byte q = source server of the layer under placement q
+  int nb;                // cost bits in use (<= 4)
+};
+// The planes stay in shared memory (one broadcast LDS.128 per placement and record): holding the 16
+// plane words in registers spilled at the 64-register budget of 2 CTAs per SM.
+__device__ __forceinline__ void dedup_rec_onehot(uint32_t w0, uint32_t w1, uint32_t base, uint32_t slot16,
+                                                 uint32_t slotpe, const OnehotLayer* ol, uint32_t srcw, DedupRec& r) {
+  uint32_t M[4] = {0u, 0u, 0u, 0u}, h8 = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t word = k < 4 ? w0 : w1;
+    const uint4 m = lds128(base + prmt(word, slot16, sel_row(k & 3)));
+    h8 += lds32(base + prmt(word, slotpe, sel_row(k & 3)));
+    M[0] |= m.x;
+    M[1] |= m.y;
+    M[2] |= m.z;
+    M[3] |= m.w;
+  }
+  uint32_t u[4], d[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    u[q] = __popc(M[q]) - ((M[q] >> ((srcw >> (8 * q)) & 31u)) & 1u);
+    const uint4 pl = *reinterpret_cast<const uint4*>(ol->plane[q]);  // zero planes beyond the layer's bits
+    d[q] = __popc(M[q] & pl.x) + ((uint32_t)__popc(M[q] & pl.y) << 1) + ((uint32_t)__popc(M[q] & pl.z) << 2) +
+           ((uint32_t)__popc(M[q] & pl.w) << 3);
+  }
+  r.h[0] = prmt(h8, 0u, 0x7270u);
+  r.h[1] = prmt(h8, 0u, 0x7371u);
+  r.u[0] = u[0] | (u[2] << 16);
+  r.u[1] = u[1] | (u[3] << 16);
+  r.d[0] = d[0] | (d[2] << 16);
+  r.d[1] = d[1] | (d[3] << 16);
+}
+
+// MODE 0: general pairwise record (any server id <= 255, pe <= 255); 1: fast pairwise (ids < 128,
+// pe <= 31); 2: one-hot masks (ids < 32, pe <= 31)
+template <int MODE>
 __device__ __forceinline__ void dedup_warp_range(const uint8_t* __restrict__ plane, int64_t wm0, int64_t wm1,
                                                  int64_t r0, int64_t r1, const int64_t* __restrict__ bounds, int C,
                                                  uint32_t base, uint32_t slot, uint32_t slot8, uint32_t src, int lane,
                                                  int64_t* __restrict__ hop_sums, int64_t* __restrict__ uniq_sums,
-                                                 int64_t* __restrict__ dedup_sums) {
+                                                 int64_t* __restrict__ dedup_sums, const OnehotLayer* s_ol) {
   constexpr int U = MP_DEDUP_U;
+  constexpr bool FAST = MODE != 0;
+  const uint32_t slot16 = (uint32_t)((lane & 7) << 4), slotpe = 128u + (uint32_t)(lane << 2);
   const int64_t wt0 = max(r0, 2 * wm0), wt1 = min(r1, 2 * wm1);
   int c = 0;
   {
@@ -135,7 +189,9 @@ __device__ __forceinline__ void dedup_warp_range(const uint8_t* __restrict__ pla
     if ((lane & 1) == 0 && tot && q < 12) atomic_add_i64(hp, (int64_t)tot);
   };
   auto rec = [&](uint32_t w0, uint32_t w1, DedupRec& r) {
-    if constexpr (FAST) {
+    if constexpr (MODE == 2) {
+      dedup_rec_onehot(w0, w1, base, slot16, slotpe, s_ol, src, r);
+    } else if constexpr (MODE == 1) {
       dedup_rec_fast(w0, w1, base, slot8, r);
     } else {
       uint32_t hh[2] = {0, 0}, dd[2] = {0, 0}, uq = 0;
@@ -236,6 +292,7 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
                                                     int64_t* __restrict__ uniq_sums, int64_t* __restrict__ dedup_sums) {
   extern __shared__ __align__(128) uint8_t sm[];  // 256 rows x 256 B
   __shared__ uint32_t s_src;                      // 4 source-server bytes of this layer
+  __shared__ OnehotLayer s_ol;                    // one-hot mode: cost bit-planes and source masks
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm);
   const int lane = threadIdx.x & 31;
   const uint32_t base = smem_addr(sm);
@@ -261,8 +318,40 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
     for (int e = threadIdx.x; e < 256; e += blockDim.x)
       wide |= (__ldg(tables + (int64_t)l * 256 + e) & 0xe0e0e0e0u) | (__ldg(srv_tables + (int64_t)l * 256 + e) & 0x80808080u);
     const bool fast = __syncthreads_or(wide != 0 || (threadIdx.x == 0 && (s_src & 0x80808080u))) == 0 && K == 8;
+    uint32_t wide32 = 0;  // any server id >= 32 (source included) or cost > 15 -> no one-hot masks
+    for (int e = threadIdx.x; e < 256; e += blockDim.x)
+      wide32 |= (__ldg(srv_tables + (int64_t)l * 256 + e) & 0xe0e0e0e0u) | (__ldg(tables + (int64_t)l * 256 + e) & 0xf0f0f0f0u);
+    const bool onehot = MP_DEDUP_ONEHOT && fast &&
+                        __syncthreads_or(wide32 != 0 || (threadIdx.x == 0 && (s_src & 0xe0e0e0e0u))) == 0;
     const uint32_t src = s_src;
-    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+    if (onehot) {
+      if (threadIdx.x < 16) reinterpret_cast<uint32_t*>(s_ol.plane)[threadIdx.x] = 0u;
+      if (threadIdx.x == 0) {
+        s_ol.src = src;
+        s_ol.nb = 0;
+      }
+      __syncthreads();
+      uint32_t maxp = 0;
+      for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+        const uint32_t pw = __ldg(tables + (int64_t)l * 256 + e), sw = __ldg(srv_tables + (int64_t)l * 256 + e);
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t p = (pw >> (8 * q)) & 0xffu, sv = (sw >> (8 * q)) & 31u;
+          maxp = max(maxp, p);
+          for (int b = 0; b < 4; ++b)
+            if ((p >> b) & 1u) atomicOr(&s_ol.plane[q][b], 1u << sv);
+        }
+      }
+      atomicMax(&s_ol.nb, 32 - __clz((int)maxp));
+      for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+        const int e = i >> 5, j = i & 31;
+        const uint32_t pw = __ldg(tables + (int64_t)l * 256 + e), sw = __ldg(srv_tables + (int64_t)l * 256 + e);
+        smw[e * 64 + 32 + j] = pw;  // pe word at 128 + lane * 4
+        if (j < 8) {                // one-hot masks at (lane & 7) * 16
+#pragma unroll
+          for (int q = 0; q < 4; ++q) smw[e * 64 + 4 * j + q] = 1u << ((sw >> (8 * q)) & 31u);
+        }
+      }
+    } else for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
       const int e = i >> 5, j = i & 31;
       const uint32_t pw = __ldg(tables + (int64_t)l * 256 + e), sw = __ldg(srv_tables + (int64_t)l * 256 + e);
       if (fast) {  // {pe, server | source flag} at lane slot j*8
@@ -284,10 +373,12 @@ __global__ void __launch_bounds__(kDedupThreads, 2) dedup_kernel(const uint8_t* 
       const int64_t perw = (m1 - m0 + nwarps - 1) / nwarps;
       const int64_t wm0 = min(m1, m0 + perw * warp), wm1 = min(m1, wm0 + perw);
       if (wm0 < wm1) {
-        if (fast) dedup_warp_range<true>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
-                                         hop_sums, uniq_sums, dedup_sums);
-        else dedup_warp_range<false>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
-                                     hop_sums, uniq_sums, dedup_sums);
+        if (onehot) dedup_warp_range<2>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
+                                        hop_sums, uniq_sums, dedup_sums, &s_ol);
+        else if (fast) dedup_warp_range<1>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
+                                           hop_sums, uniq_sums, dedup_sums, &s_ol);
+        else dedup_warp_range<0>(plane, wm0, wm1, r0, r1, bounds, C, base, slot, slot8, src, lane,
+                                 hop_sums, uniq_sums, dedup_sums, &s_ol);
       }
       g += r1 - r0;
       continue;
