@@ -121,8 +121,10 @@ int mp_contract_counts(const int64_t* counts, int C, const uint8_t* pe, int P, i
  *   swizzled K-major tiles), stream-K over every (128-row pe tile, 128-byte k-block) unit with runs
  *   of <= 32768 K per accumulation so every int32 partial is exact, the digits recombined in the
  *   epilogue and added with coalesced int64 atomics.  ldpe, ldd: multiples of 16; pe, digits:
- *   16-byte aligned.  ctas = 0: one CTA per SM; else that many CTAs (per 512-row digit tile).  Together with mp_hist_chunks_u8 this is the
- *   factorized evaluator for any number of placements.                                            */
+ *   16-byte aligned.  ctas = 0: automatic (single CTAs, one epilogue each); ctas > 0: that many
+ *   single CTAs per 512-row digit tile; ctas < 0: -ctas CTA pairs per digit tile
+ *   (tcgen05.mma.cta_group::2 on 256-row tiles, each CTA loading half of the digit tile).  Together with
+ *   mp_hist_chunks_u8 this is the factorized evaluator for any number of placements.              */
 int mp_count_digits_u8(const int64_t* counts, int C, int64_t LE, int ndig, int64_t ldd, uint8_t* out, int64_t* err,
                        void* stream);
 int mp_contract_tc_u8(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig, int64_t LE,

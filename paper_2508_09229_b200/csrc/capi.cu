@@ -144,7 +144,7 @@ int mp_count_digits_u8(const int64_t* counts, int C, int64_t LE, int ndig, int64
 
 int mp_contract_tc_u8(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig, int64_t LE,
                       int64_t ldd, int64_t* out, int ctas, void* stream) {
-  if (!pe || !digits || !out || P <= 0 || C <= 0 || LE <= 0 || ctas < 0) return MP_ERR_ARG;
+  if (!pe || !digits || !out || P <= 0 || C <= 0 || LE <= 0 || ctas < -65536) return MP_ERR_ARG;
   if (ndig != 1 && ndig != 2 && ndig != 4) return MP_ERR_ARG;
   if (ldpe < LE || ldd < LE || (ldpe & 15) || (ldd & 15) || !aligned16(pe) || !aligned16(digits)) return MP_ERR_ARG;
   if ((int64_t)C * ndig > (1 << 24)) return MP_ERR_UNSUPPORTED;

@@ -144,7 +144,7 @@ inline int device_sm_count() {
 
 // cudaFuncSetAttribute(max dynamic shared memory) once per (device, kernel, size); *per_sm = resident
 // CTAs per SM at (threads, smem), from cudaOccupancyMaxActiveBlocksPerMultiprocessor (cached).
-inline cudaError_t prepare_kernel(const void* kern, int threads, int smem, int* per_sm) {
+inline cudaError_t prepare_kernel(const void* kern, int threads, int smem, int* per_sm, bool occupancy = true) {
   static std::mutex mu;
   static std::map<std::tuple<int, const void*, int, int>, int> cache;
   int dev = 0;
@@ -160,8 +160,8 @@ inline cudaError_t prepare_kernel(const void* kern, int threads, int smem, int* 
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  int n = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+  int n = 1;  // cluster kernels (CTA pairs) skip the occupancy query: one CTA per SM by construction
+  if (occupancy) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> g(mu);
   cache[key] = n;

@@ -253,6 +253,211 @@ __global__ void __launch_bounds__(kTcThreads2, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
 }
 
+// ---- CTA-pair variant (tcgen05 cta_group::2) ------------------------------------------------
+// Two CTAs of a cluster on one TPC form an M = 256 tile: CTA r loads pe rows m0 + 128r (A) and HALF of
+// the N tile's digit rows (B rows n0 + H*r .. + H, H = NT/2) into its own shared memory, both with
+// `cp.async.bulk.tensor.cta_group::2` signalling the leader's full barrier; the leader's single
+// thread issues `tcgen05.mma.cta_group::2.kind::i8`, which reads A and B from both CTAs and writes
+// D rows 128r.. into CTA r's TMEM; commits multicast to both CTAs' barriers.  Per k-block an SM
+// receives 128 + H rows instead of 128 + 2H (config 4: 35.5 KB instead of 55 KB).  Measured
+// (tools/probe_contract.py, config 4): bit-exact, but 0.058 ms with 64 pairs against 0.039 ms for
+// 128 single CTAs -- operand bytes were not the single-CTA kernel's limit (ncu: TMA/L2 reads at 6 % of
+// peak; the pair waits for the slower CTA's loads and the leader's thread issues M = 256 MMAs for
+// both) -- so AUTO keeps single CTAs and the pair kernel runs on request (ctas < 0).  TMEM column j holds digit row map(j): the first MMA
+// covers B rows [0, h1) of each half (columns [0, h1) from CTA 0, [h1, 2h1) from CTA 1), a second
+// one the remaining H - h1 rows of each half.
+struct Tc2Args {
+  int P, C, ndig, n_cols;
+  int NT, H, h1;            // digit rows per N tile, per CTA half (NT / 2), per half in the first MMA
+  int kblocks, m_tiles;     // k-blocks of 128 B; 256-row pe tiles
+  int64_t units;            // m_tiles * kblocks, split evenly over the pairs
+  int max_seg, stages;
+  uint32_t tmem_cols;
+  int64_t* out;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t idesc_i8_m256(int n) {
+  return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+// digit row (relative to the N tile) held by TMEM column j
+__device__ __forceinline__ int pair_col_row(int j, int H, int h1) {
+  if (j < 2 * h1) return (j >= h1 ? H : 0) + (j % h1);
+  const int jj = j - 2 * h1, h2 = H - h1;
+  return (jj >= h2 ? H : 0) + h1 + (jj % h2);
+}
+
+struct Seg2 {
+  int64_t u;
+  __device__ bool next(const Tc2Args& a, int64_t u1, int64_t* s0, int64_t* s1) {
+    if (u >= u1) return false;
+    const int64_t tile_end = (u / a.kblocks + 1) * a.kblocks;
+    *s0 = u;
+    *s1 = min(min(u1, tile_end), u + a.max_seg);
+    u = *s1;
+    return true;
+  }
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads2, 1)
+    contract_tc2_kernel(const __grid_constant__ CUtensorMap tm_pe, const __grid_constant__ CUtensorMap tm_dig,
+                        Tc2Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2 * kMaxStages + 2];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int S = a.stages;
+  const uint32_t a_bytes = 128 * kBK, b_bytes = (uint32_t)a.H * kBK, stage_bytes = a_bytes + b_bytes;
+  const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[kMaxStages]);
+  const uint32_t tmem_full = smem_addr(&bars[2 * kMaxStages]), tmem_empty = smem_addr(&bars[2 * kMaxStages + 1]);
+  const int n0 = blockIdx.y * a.NT;
+  const int pair = (int)(blockIdx.x >> 1), npairs = (int)(gridDim.x >> 1);
+  const int64_t u0 = pair * a.units / npairs, u1 = (pair + 1) * a.units / npairs;
+
+  if (warp == 4 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 2 * kEpiWarps);  // the epilogue warps of both CTAs
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_pe)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dig)) : "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
+                 "r"(a.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 4) {  // ---- TMA producer (each CTA loads its own A rows and B half) ----
+    if (lane == 0) {
+      const uint32_t full_lead = mapa_shared(full0, 0);
+      int i = 0;
+      for (int64_t u = u0; u < u1; ++u, ++i) {
+        const int s = i % S;
+        if (i >= S) mbar_wait(empty0 + 8 * s, ((i / S) - 1) & 1);
+        const int m0 = (int)(u / a.kblocks) * 256 + (int)rank * 128, kb = (int)(u % a.kblocks);
+        const uint32_t dst = base + (uint32_t)s * stage_bytes;
+        if (rank == 0) mbar_expect_tx(full0 + 8 * s, 2 * stage_bytes);  // both CTAs' bytes
+        tma_load_2d_pair(dst, &tm_pe, kb * kBK, m0, full_lead + 8 * s);
+        tma_load_2d_pair(dst + a_bytes, &tm_dig, kb * kBK, n0 + (int)rank * a.H, full_lead + 8 * s);
+      }
+    }
+  } else if (warp == 5) {  // ---- MMA issuer: one thread of the leader CTA ----
+    if (rank == 0 && lane == 0) {
+      Seg2 sg{u0};
+      int64_t s0, s1;
+      int i = 0, seg = 0;
+      const int h2 = a.H - a.h1;
+      while (sg.next(a, u1, &s0, &s1)) {
+        if (seg > 0) mbar_wait(tmem_empty, (seg - 1) & 1);  // both epilogues have drained TMEM
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int64_t u = s0; u < s1; ++u, ++i) {
+          const int s = i % S;
+          mbar_wait(full0 + 8 * s, (i / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = base + (uint32_t)s * stage_bytes, sb = sa + a_bytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 32; ++k) {
+            const uint32_t acc = (u > s0 || k > 0) ? 1u : 0u;
+            mma_i8_pair(tmem, sw128_desc(sa + 32 * k), sw128_desc(sb + 32 * k), idesc_i8_m256(2 * a.h1), acc);
+            if (h2 > 0)
+              mma_i8_pair(tmem + 2 * a.h1, sw128_desc(sa + 32 * k), sw128_desc(sb + (uint32_t)a.h1 * kBK + 32 * k),
+                          idesc_i8_m256(2 * h2), acc);
+          }
+          mma_commit_pair(empty0 + 8 * s);  // frees slot s in both CTAs
+        }
+        mma_commit_pair(tmem_full);
+        ++seg;
+      }
+    }
+  } else {  // ---- epilogue warps 0-3 of each CTA: own TMEM lanes = pe rows m0 + 128 * rank + ... ----
+    uint8_t* tile = smem_raw + (base - smem_addr(smem_raw)) + (uint32_t)S * stage_bytes + warp * kEpiTileBytes;
+    int64_t* t64 = reinterpret_cast<int64_t*>(tile);
+    const int nd = a.ndig, V = 16 / nd;
+    const uint32_t empty_lead = mapa_shared(tmem_empty, 0);
+    Seg2 sg{u0};
+    int64_t s0, s1;
+    int seg = 0;
+    while (sg.next(a, u1, &s0, &s1)) {
+      mbar_wait(tmem_full, seg & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row0 = (int)(s0 / a.kblocks) * 256 + (int)rank * 128 + warp * 32;
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+      for (int c0 = 0; c0 < 2 * a.H; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(trow + c0, v);
+        if (c0 + 16 >= 2 * a.H) {  // last TMEM read of this segment: tell the leader
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(empty_lead) : "memory");
+        }
+        if (nd == 1) stage_values<1>(v, t64 + lane * 17);
+        else if (nd == 2) stage_values<2>(v, t64 + lane * 17);
+        else stage_values<4>(v, t64 + lane * 17);
+        __syncwarp();
+        for (int r = 0; r < V; ++r) {
+          const int idx = r * 32 + lane;
+          const int rr = idx / V, j = idx % V;
+          const int row = row0 + rr;
+          const int drow = n0 + pair_col_row(c0 + j * nd, a.H, a.h1);  // first digit row of this value
+          const int ch = drow / nd;
+          const int64_t val = t64[rr * 17 + j];
+          if (val && row < a.P && ch < a.C && drow < a.n_cols) atomic_add_i64(a.out + (int64_t)row * a.C + ch, val);
+        }
+        __syncwarp();
+      }
+      ++seg;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // neither CTA frees TMEM while the pair's MMAs may still target it
+  if (warp == 5)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+}
+
 // out[(c*ndig + a)*ldd + i] = byte a of counts[c*LE + i]; columns [LE, ldd) are zero.  One thread per
 // 8 consecutive columns of one chunk row (blockIdx.y = chunk): eight int64 loads, ndig u64 stores.
 __global__ void count_digits_u8_kernel(const int64_t* __restrict__ counts, int C, int64_t LE, int ndig, int64_t ldd,
@@ -315,11 +520,50 @@ cudaError_t launch_count_digits_u8(const int64_t* counts, int C, int64_t LE, int
   return cudaGetLastError();
 }
 
-// ctas: 0 = one CTA per SM (stream-K over every (pe tile, k-block) unit), else that many CTAs per N tile
+static cudaError_t launch_contract_tc2(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig,
+                                       int64_t LE, int64_t ldd, int64_t* out, int pairs, int sms, cudaStream_t s) {
+  Tc2Args a;
+  a.P = P;
+  a.C = C;
+  a.ndig = ndig;
+  a.n_cols = C * ndig;
+  const int n_tiles = (a.n_cols + 511) / 512;
+  const int per = (a.n_cols + n_tiles - 1) / n_tiles;
+  a.NT = (per + 31) / 32 * 32;  // H = NT / 2 a multiple of 16 (swizzle atoms, digit groups)
+  a.H = a.NT / 2;
+  a.h1 = std::min(128, a.H);
+  a.tmem_cols = a.NT <= 32 ? 32 : a.NT <= 64 ? 64 : a.NT <= 128 ? 128 : a.NT <= 256 ? 256 : 512;
+  a.kblocks = (int)((LE + kBK - 1) / kBK);
+  a.m_tiles = (P + 255) / 256;
+  a.units = (int64_t)a.m_tiles * a.kblocks;
+  a.max_seg = kMaxKPerSplit / kBK;
+  const int per_n = std::max(1, sms / 2 / n_tiles);  // pairs per N tile
+  int64_t g = pairs > 0 ? pairs : (a.m_tiles <= per_n ? (int64_t)a.m_tiles * (per_n / a.m_tiles) : per_n);
+  g = std::min(g, a.units);
+  const int stage_bytes = 128 * kBK + a.H * kBK;
+  const int epi_bytes = kEpiWarps * kEpiTileBytes;
+  a.stages = std::min(kMaxStages, (kSmemLimit - 2048 - epi_bytes) / stage_bytes);
+  if (a.stages < 2) return cudaErrorInvalidValue;
+  a.out = out;
+  CUtensorMap tm_pe, tm_dig;
+  if (!make_map(&tm_pe, pe, (uint64_t)LE, (uint64_t)P, (uint64_t)ldpe, 128)) return cudaErrorInvalidValue;
+  if (!make_map(&tm_dig, digits, (uint64_t)LE, (uint64_t)a.n_cols, (uint64_t)ldd, (uint32_t)a.H))
+    return cudaErrorInvalidValue;
+  const int smem = a.stages * stage_bytes + epi_bytes + 1024;
+  int per_sm = 0;
+  cudaError_t e = prepare_kernel((const void*)contract_tc2_kernel, kTcThreads2, smem, &per_sm, false);
+  if (e != cudaSuccess) return e;
+  contract_tc2_kernel<<<dim3((unsigned)(2 * g), (unsigned)n_tiles), kTcThreads2, smem, s>>>(tm_pe, tm_dig, a);
+  return cudaGetLastError();
+}
+
+// ctas: 0 = auto (single CTAs, tile-aligned split), > 0 = that many single CTAs per N tile
+// (stream-K), < 0 = -ctas CTA pairs per N tile (cta_group::2; measured slower, see above)
 cudaError_t launch_contract_tc(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* digits, int C, int ndig,
                                int64_t LE, int64_t ldd, int64_t* out, int ctas, cudaStream_t s) {
   if (P <= 0 || C <= 0 || LE <= 0) return cudaSuccess;
   const int sms = device_sm_count();
+  if (ctas < 0) return launch_contract_tc2(pe, P, ldpe, digits, C, ndig, LE, ldd, out, -ctas, sms, s);
   TcArgs a;
   a.P = P;
   a.C = C;

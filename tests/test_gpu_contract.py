@@ -41,7 +41,9 @@ def test_contract_tc_matches_exact_references(P, LE, C, cmax):
     got = ev.contract_tc(cnt, pe, max_count=cmax)
     assert torch.equal(got, want)
     d = ev.CountDigits(cnt, cmax)
-    for ctas in (1, 3, 77, 300):  # stream-K splits landing anywhere inside the pe tiles
+    # single CTAs: stream-K splits landing anywhere inside the pe tiles; negative: CTA pairs
+    # (tcgen05 cta_group::2, 256-row tiles), including pairs that straddle tiles
+    for ctas in (1, 3, 77, 300, -1, -3, -37):
         out = torch.zeros((P, C), dtype=torch.int64, device="cuda")
         d.contract(pe, out, ctas=ctas)
         assert torch.equal(out, want), ctas

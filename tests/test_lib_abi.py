@@ -82,7 +82,7 @@ def test_argument_validation_matrix():
         (L.mp_count_digits_u8(P, 4, 10, 3, 16, P, P, None), ARG),           # ndig not 1/2/4
         (L.mp_contract_tc_u8(P, 8, 24, P, 4, 2, 20, 32, P, 0, None), ARG),  # ldpe not a multiple of 16
         (L.mp_contract_tc_u8(P, 8, 32, P, 4, 3, 20, 32, P, 0, None), ARG),  # ndig not 1/2/4
-        (L.mp_contract_tc_u8(P, 8, 32, P, 4, 2, 20, 32, P, -1, None), ARG), # negative split
+        (L.mp_contract_tc_u8(P, 8, 32, P, 4, 2, 20, 32, P, -70000, None), ARG),  # absurd pair count
         (L.mp_pe_gather_u8(P, 1, Lr, 8, None, P, None, 4, E, P, Lr * E, None, None), ARG),  # err required
         (L.mp_pe_gather_u8(P, 1, Lr, 8, None, P, None, 4, E, P, Lr * E - 1, P, None), ARG),  # ldpe < L*E
         (L.mp_perturb_pe_u8(P, Lr, E, 4, 2, 0, 0, P, Lr * E + 8, P, None), ARG),  # ldpe not 16-aligned

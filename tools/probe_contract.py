@@ -40,7 +40,7 @@ _lib.call("mp_contract_counts", _lib.ptr(cnt), C, _lib.ptr(pe), P, LE, _lib.ptr(
 res["CountDigits_python_call_ms"] = timeit(lambda: ev.CountDigits(cnt, 6666))
 res["count_digits_u8_kernel_ms"] = timeit(lambda: _lib.call("mp_count_digits_u8", _lib.ptr(cnt), C, LE, 2, d.ldd,
                                                             _lib.ptr(d.buf), _lib.ptr(d.err), _lib.stream_handle()))
-for sp in (0, 64, 128, 148, 296):
+for sp in (0, 64, 128, 148, 296, -32, -64, -74):
     out.zero_()
     d.contract(pe, out, ctas=sp)
     ok = torch.equal(out, ref)
