@@ -14,7 +14,8 @@ hop sums by count-contract (histogram of every (layer, chunk) piece contracted w
 tables at the piece's flush; exact by linearity); --algo gather times the per-byte
 table gather instead (bit-identical results, tests/test_gpu_algos.py).  For N GPUs each rank
 owns a contiguous 10M-token shard of one N*10M-token trace (weak scaling) and the packed int64
-[counts | hop sums] buffer is combined with one NCCL all_reduce inside the timed step.
+[counts | hop sums] buffer is summed inside the timed step by the library's NVLink/NVSwitch peer-memory kernel
+(symmetric memory, multimem.ld_reduce; `--collective nccl` uses one NCCL all_reduce instead).
 
 value  = token-layers scored x placements per second, whole job: N*10M*58*4 / step time.
 e2e    = the same metric through the public API (moeplace.eval.evaluate_with_stats) on the SPEC's
@@ -81,7 +82,9 @@ def workload(wl: int, n_gpus: int, tok: int, n_total: int, P: int) -> dict:
     return {"workload": desc, "tokens_per_gpu": tok, "tokens_total": n_total, "placements": P,
             "l2": (f"inputs larger than L2: {by / 1e9:.2f} GB trace per GPU vs 126 MB L2, no flush needed" if by > 126e6
                    else f"trace {by / 1e6:.0f} MB < 126 MB L2 (reused across the step's passes)"),
-            "parallelism": (f"token shards x{n_gpus} + 1 NCCL all_reduce of int64 counts|sums" if n_gpus > 1
+            "parallelism": (f"token shards x{n_gpus} + 1 sum of the int64 counts|sums vector over NVLink/NVSwitch "
+                            "peer memory (library kernel, multimem.ld_reduce; NCCL all_reduce with --collective nccl)"
+                            if n_gpus > 1
                             else "single GPU")}
 
 
@@ -344,6 +347,9 @@ def main():
     ap.add_argument("--sustained-s", type=float, default=0.6, help="seconds of back-to-back steps for the sustained figure")
     ap.add_argument("--write-fixtures", default=None, help="directory: save the placements the CPU legs use")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--collective", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: sum the packed result with the library's NVLink/NVSwitch peer-memory kernel "
+                         "(default) or with torch.distributed.all_reduce (NCCL)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -373,6 +379,7 @@ def main():
     import moeplace.solver as sv
     import moeplace.topology as topo
     from paper_2508_09229_b200 import _lib
+    from paper_2508_09229_b200.shard import PeerSum
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -482,13 +489,23 @@ def main():
             groups.append((W, tables, max_p, len(grp)))
     n_sums = sum(4 * W for W, _, _, _ in groups)
     with_hist = wl in (2, 5)
-    buf = torch.zeros((L * E if with_hist else 0) + n_sums * C, dtype=torch.int64, device=dev)
-    counts = buf[:L * E] if with_hist else None
-    sums_all = buf[L * E:] if with_hist else buf
-    views, off = [], 0
-    for W, _, _, _ in groups:
-        views.append(sums_all[off:off + 4 * W * C])
-        off += 4 * W * C
+    # N > 1: the packed [counts | sums] vector lives in symmetric memory and is summed over NVLink /
+    # NVSwitch by the library's own kernel (shard.PeerSum, multimem.ld_reduce); --collective nccl
+    # uses torch.distributed.all_reduce instead
+    n_buf = (L * E if with_hist else 0) + n_sums * C
+    peer = PeerSum.create(n_buf) if world > 1 and args.collective == "peer" else None
+    buf = torch.zeros(n_buf, dtype=torch.int64, device=dev)
+
+    def carve(b):
+        """[counts | sums] views of one packed buffer: (counts or None, [sums view per group])."""
+        sums_all = b[L * E:] if with_hist else b
+        vs, off = [], 0
+        for W, _, _, _ in groups:
+            vs.append(sums_all[off:off + 4 * W * C])
+            off += 4 * W * C
+        return (b[:L * E] if with_hist else None), vs
+
+    counts, views = carve(buf)  # the step's result (after the cross-GPU sum when N > 1)
 
     algo = {"auto": 0, "gather": 1, "count": 2, "token": 3, "seg": 4, "factorized": 0}[args.algo]
     # config 4 (4096 candidates): the product path is evaluate_many(method="auto") -> factorized (one per-chunk
@@ -512,20 +529,25 @@ def main():
             dist.all_reduce(out_f4)
 
     def step(hi=None):
+        nonlocal counts, views
         hi = hi or t1
-        buf.zero_()
+        b = peer.input() if peer is not None else buf  # peer: this epoch's half of the symmetric pair
+        b.zero_()
+        cnt_b, views_b = carve(b)
         if with_hist and fused:
             W, tables, max_p, _ = groups[0]
             _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, t0, hi, L, K, E, _lib.ptr(bounds), C,
-                      _lib.ptr(tables), W, max_p, _lib.ptr(counts), _lib.ptr(views[0]), _lib.ptr(err), algo, sh)
+                      _lib.ptr(tables), W, max_p, _lib.ptr(cnt_b), _lib.ptr(views_b[0]), _lib.ptr(err), algo, sh)
         else:
             if with_hist:
-                _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, hi, L, K, E, _lib.ptr(counts), _lib.ptr(err), sh)
-            for (W, tables, max_p, _), v in zip(groups, views):
+                _lib.call("mp_hist_u8", _lib.ptr(planes), stride, t0, hi, L, K, E, _lib.ptr(cnt_b), _lib.ptr(err), sh)
+            for (W, tables, max_p, _), v in zip(groups, views_b):
                 _lib.call("mp_score_ex_u8", _lib.ptr(planes), stride, t0, hi, L, K, _lib.ptr(bounds), C,
                           _lib.ptr(tables), W, max_p, _lib.ptr(v), algo, sh)
-        if world > 1:
-            dist.all_reduce(buf)
+        if peer is not None:
+            counts, views = carve(peer.allreduce())
+        elif world > 1:
+            dist.all_reduce(b)
 
     def main_kernel():
         """The step's dominant kernel alone (no zeroing, no collective): the roofline numerator."""
@@ -618,6 +640,8 @@ def main():
         torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
     _lib.check_err(err, "bench: device data error in the timed steps")
+    if peer is not None:
+        peer.check()
     t_step = torch.tensor([ev_a.elapsed_time(ev_b) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)

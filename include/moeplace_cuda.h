@@ -198,6 +198,20 @@ int mp_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begi
 int mp_hist_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begin, int64_t tok_end,
                         int L, int K, int E, const int64_t* chunk_bounds, int C, const uint32_t* tables, int W,
                         int max_p, int64_t* counts, int64_t* hop_sums, int64_t* err, int algo, void* stream);
+/* ---- cross-GPU sum of the packed result vector ---------------------------------
+ * mp_allreduce_peers_i64: out[i] = sum over the world of every rank's copy of a symmetric int64
+ * buffer (torch.distributed._symmetric_memory), through NVLink/NVSwitch peer memory instead of a
+ * separate NCCL collective.  peer_bufs / peer_pads: DEVICE arrays of the world's buffer and
+ * signal-pad addresses (the buffer to sum, e.g. one half of a double-buffered allocation); mc: its
+ * multicast address (NVLS: one multimem.ld_reduce per element, summed in the switch) or NULL (P2P
+ * loads); out: this rank's private result.  Every rank calls it with the same n and an epoch larger
+ * than any earlier call's; a rank must not rewrite the summed buffer before the NEXT call has
+ * returned (double-buffer the inputs by epoch parity).  Signal-pad words [1024, 2048) are used;
+ * n <= 2^21 / world (else MP_ERR_UNSUPPORTED).  A peer that does not arrive within ~2 s of clock
+ * sets err = {MP_DATA_UNREACHABLE, rank, slice} instead of hanging.                          */
+int mp_allreduce_peers_i64(int64_t* out, int64_t n, const int64_t* mc, const uint64_t* peer_bufs,
+                           const uint64_t* peer_pads, int rank, int world, uint32_t epoch, int64_t* err, void* stream);
+
 /* The algorithm MP_ALGO_AUTO resolves to for a call over `tokens` tokens in C chunks (hist != 0: the
  * fused histogram + score pass).  Host-only, no device work. */
 int mp_choose_algo(int hist, int W, int64_t tokens, int C, int L, int K, int max_p);

@@ -18,7 +18,7 @@ LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libmoeplace_cuda.so"
 ROOT = PKG.parent
 
-CU_SOURCES = ["stream.cu", "seg.cu", "gen.cu", "topo.cu", "dedup.cu", "parse.cu", "tokens.cu", "ingest.cu", "contract.cu", "search.cu", "capi.cu"]
+CU_SOURCES = ["stream.cu", "seg.cu", "gen.cu", "topo.cu", "dedup.cu", "parse.cu", "tokens.cu", "ingest.cu", "contract.cu", "search.cu", "collective.cu", "capi.cu"]
 CXX_SOURCES = ["solver.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

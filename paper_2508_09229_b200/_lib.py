@@ -45,6 +45,7 @@ SIGNATURES = {
     "mp_hist_score_ex_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _i32,
                                    _p]),
     "mp_choose_algo": (_i32, [_i32, _i32, _i64, _i32, _i32, _i32, _i32]),
+    "mp_allreduce_peers_i64": (_i32, [_p, _i64, _p, _p, _p, _i32, _i32, C.c_uint32, _p, _p]),
     "mp_score_dedup_u8": (_i32, [_p, _i64, _i64, _i64, _i32, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "mp_pack_server_tables": (_i32, [_p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p, _p, _p]),
     "mp_apsp_bfs": (_i32, [_p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),

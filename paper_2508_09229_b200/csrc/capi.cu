@@ -7,6 +7,10 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
                           int L, int K, int E, const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                           int64_t* hop_sums, int64_t* err, cudaStream_t s, int algo);
 int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K, int max_p);
+int allreduce_supported(int64_t n, int world);
+cudaError_t launch_allreduce_i64(int64_t* out, int64_t n, const int64_t* mc, const int64_t* const* peers,
+                                 uint32_t* const* pads, int rank, int world, uint32_t epoch, int64_t* err,
+                                 cudaStream_t s);
 cudaError_t launch_gen(uint64_t seed, int64_t t0, int64_t t1, int L, int K, int E, const uint32_t* cdf,
                        const uint8_t* perm, uint8_t* planes, int64_t stride, cudaStream_t s);
 cudaError_t launch_validate(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
@@ -212,6 +216,16 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
                      int64_t* hop_sums, int64_t* err, void* stream) {
   return mp_hist_score_ex_u8(planes, plane_stride, tok_begin, tok_end, L, K, E, chunk_bounds, C, tables, 1, max_p,
                              counts, hop_sums, err, MP_ALGO_AUTO, stream);
+}
+
+int mp_allreduce_peers_i64(int64_t* out, int64_t n, const int64_t* mc, const uint64_t* peer_bufs,
+                           const uint64_t* peer_pads, int rank, int world, uint32_t epoch, int64_t* err, void* stream) {
+  if (!out || n < 0 || !peer_bufs || !peer_pads || !err || world < 1 || world > 64 || rank < 0 || rank >= world)
+    return MP_ERR_ARG;
+  if (!mp::allreduce_supported(n, world)) return MP_ERR_UNSUPPORTED;  // signal-pad words / vector length
+  return status(mp::launch_allreduce_i64(out, n, mc, reinterpret_cast<const int64_t* const*>(peer_bufs),
+                                         reinterpret_cast<uint32_t* const*>(peer_pads), rank, world, epoch, err,
+                                         S(stream)));
 }
 
 int mp_choose_algo(int hist, int W, int64_t tokens, int C, int L, int K, int max_p) {
