@@ -37,6 +37,7 @@ class PeerSum:
     ``torch.distributed.all_reduce``."""
 
     _cache: dict = {}
+    _epochs: dict = {}  # per group: every call on the group takes the next epoch, whatever its PeerSum
 
     def __init__(self, n: int, group):
         import torch
@@ -54,7 +55,8 @@ class PeerSum:
         self.pads = dev_ptrs(self.hdl.signal_pad_ptrs)
         self.out = torch.zeros(n, dtype=torch.int64, device="cuda")
         self.err = _lib.new_err()
-        self.epoch = 0
+        self.group_name = group.group_name
+        self.epoch = 0  # calls made on this buffer (selects the input half)
 
     @classmethod
     def create(cls, n: int, group=None):
@@ -94,8 +96,10 @@ class PeerSum:
         from . import _lib
         self.epoch += 1
         h = self.epoch & 1
+        ge = PeerSum._epochs.get(self.group_name, 0) + 1  # unique per group: signal pads may be shared
+        PeerSum._epochs[self.group_name] = ge
         _lib.call("mp_allreduce_peers_i64", _lib.ptr(self.out), self.n, self.mcs[h] or None, _lib.ptr(self.peers[h]),
-                  _lib.ptr(self.pads), self.rank, self.world, self.epoch & 0xFFFFFFFF, _lib.ptr(self.err),
+                  _lib.ptr(self.pads), self.rank, self.world, ge & 0xFFFFFFFF, _lib.ptr(self.err),
                   _lib.stream_handle())
         return self.out
 
