@@ -53,7 +53,9 @@ __device__ __forceinline__ bool pad_barrier(uint32_t* const* pads, int rank, int
     st_release_sys(pads[threadIdx.x] + kArPadBase + slot0 + rank, epoch);
     const uint32_t* mine = pads[rank] + kArPadBase + slot0 + threadIdx.x;
     const long long t0 = clock64();
-    while (ld_acquire_sys(mine) != epoch) {
+    // at least this epoch: a fast peer may already have moved on to the next call and stored a larger
+    // one (it can only do so after its own part of this call is complete)
+    while ((int)(ld_acquire_sys(mine) - epoch) < 0) {
       if (clock64() - t0 > (1ll << 32)) {
         ok = false;
         break;
