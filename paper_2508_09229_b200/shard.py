@@ -12,6 +12,7 @@ bits as a single-GPU run; the report floats are then derived once, identically e
 """
 from __future__ import annotations
 
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -49,6 +50,8 @@ class PeerSum:
         self.hdl = symm.rendezvous(self.sym, group.group_name)
         self.rank, self.world = self.hdl.rank, self.hdl.world_size
         mc = int(getattr(self.hdl, "multicast_ptr", 0) or 0)
+        if os.environ.get("MOEPLACE_PEER_NO_MULTICAST"):  # exercise the P2P-load path on an NVLS box
+            mc = 0
         dev_ptrs = lambda xs: torch.tensor(xs, dtype=torch.int64, device="cuda")  # noqa: E731 (< 2^63)
         self.peers = [dev_ptrs([p + h * n * 8 for p in self.hdl.buffer_ptrs]) for h in (0, 1)]
         self.mcs = [mc + h * n * 8 if mc else 0 for h in (0, 1)]

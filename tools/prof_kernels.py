@@ -72,6 +72,10 @@ for _ in range(a.reps):
             else:
                 _lib.call("mp_score_ex_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t_), W, mp_,
                           _lib.ptr(s), 4, sh)
+        elif w == "hist_chunks":
+            cc = torch.zeros((C, L * E), dtype=torch.int64, device="cuda")
+            _lib.call("mp_hist_chunks_u8", _lib.ptr(P), st, 0, a.tokens, L, K, E, _lib.ptr(b), C, _lib.ptr(cc),
+                      _lib.ptr(err), sh)
         elif w == "dedup":
             _lib.call("mp_score_dedup_u8", _lib.ptr(P), st, 0, a.tokens, L, K, _lib.ptr(b), C, _lib.ptr(t1),
                       _lib.ptr(srv1), _lib.ptr(src1), _lib.ptr(s), _lib.ptr(s2), _lib.ptr(s3), sh)
