@@ -206,3 +206,40 @@ def test_dedup_warp_ranges_stress(L, E, N, C, seed, topo_case):
         assert rep.spec.chunk_hop_sums == h.tolist()
         assert rep.chunk_uniq_sums == u.tolist()
         assert rep.chunk_dedup_sums == d.tolist()
+
+
+@settings(max_examples=int(__import__("os").environ.get("MP_STRESS_EXAMPLES", "8")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(1, 6), st.sampled_from([16, 256]), st.integers(20_000, 200_000), st.integers(2, 4_000),
+       st.integers(0, 2 ** 31), st.sampled_from([1, 2, 4]), st.floats(0.0, 0.45), st.floats(0.55, 1.0))
+def test_segmented_gather_views_stress(L, E, N, C, seed, W, lo, hi):
+    """The segmented gather (round-2 kernel: compile-time interior windows, edge windows only at a
+    warp range's odd first token and its end) and the unique-destination kernel on chunk-range VIEWS
+    starting and ending at arbitrary (often odd) tokens, over many CTAs: bit-exact against the
+    per-byte gather, the oracle histogram and the dedup oracle."""
+    from helpers import oracle_cost, setup_topology
+    from oracle import evaluate as oe
+    m = mt.ModelSpec(L, E, 8)
+    tr = mt.generate_trace(m, 1.2, N, C, seed)
+    c0, c1 = int(lo * C), max(int(lo * C) + 1, int(hi * C))
+    sub = tr.view(c0, c1)
+    rng = np.random.default_rng(seed % 983)
+    cost, p = _cost(rng, L, 19, 31)
+    pls = [mpl.Placement(rng.integers(0, 19, (L, E)).astype(np.int32)) for _ in range(4 * W)]
+    want = ev.score_sums(sub, pls, cost, algo="gather")
+    assert np.array_equal(ev.score_sums(sub, pls, cost, algo="seg"), want)
+    f, reps = ev.evaluate_with_stats(sub, pls, cost, algo="seg")
+    sel = sub.tokens()
+    assert np.array_equal(f.counts, np.stack([np.bincount(sel[:, l, :].ravel(), minlength=E) for l in range(L)]))
+    assert [r.chunk_hop_sums for r in reps] == want.tolist()
+    # unique destinations on the same view (FatTree: fast layers)
+    g, dist, order, attn, cst = setup_topology("FatTree", 4, 2, 4, m)
+    _, pc = oracle_cost(g, attn)
+    dp = [mpl.Placement(rng.integers(0, g.n_devices, (L, E)).astype(np.int32)) for _ in range(4)]
+    dreps = ev.evaluate_dedup(sub, dp, cst)
+    b = sub.chunk_bounds - sub.chunk_bounds[0]
+    for pl, rep in zip(dp, dreps):
+        h, u, d = oe.dedup_sums(sel, oe.pe_table(pc, pl.assign), g.device_server[pl.assign],
+                                g.device_server[attn.dispatch], b)
+        assert rep.spec.chunk_hop_sums == h.tolist()
+        assert rep.chunk_uniq_sums == u.tolist() and rep.chunk_dedup_sums == d.tolist()
