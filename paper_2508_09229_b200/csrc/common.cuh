@@ -142,29 +142,35 @@ inline int device_sm_count() {
   return n;
 }
 
-// cudaFuncSetAttribute(max dynamic shared memory) once per (device, kernel, size); *per_sm = resident
-// CTAs per SM at (threads, smem), from cudaOccupancyMaxActiveBlocksPerMultiprocessor (cached).
+// The kernel's max-dynamic-shared-memory attribute is raised (never lowered: it is per-function state,
+// and a smaller later value would break a cached larger launch) once per (device, kernel, larger
+// size); *per_sm = resident CTAs per SM at (threads, smem), from
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor (cached per (device, kernel, threads, smem)).
 inline cudaError_t prepare_kernel(const void* kern, int threads, int smem, int* per_sm, bool occupancy = true) {
   static std::mutex mu;
-  static std::map<std::tuple<int, const void*, int, int>, int> cache;
+  static std::map<std::tuple<int, const void*, int, int>, int> occ;
+  static std::map<std::tuple<int, const void*>, int> attr;  // largest size set so far
   int dev = 0;
   cudaGetDevice(&dev);
   const auto key = std::make_tuple(dev, kern, threads, smem);
-  {
-    std::lock_guard<std::mutex> g(mu);
-    const auto it = cache.find(key);
-    if (it != cache.end()) {
-      *per_sm = it->second;
-      return cudaSuccess;
-    }
-  }
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  int n = 1;  // cluster kernels (CTA pairs) skip the occupancy query: one CTA per SM by construction
-  if (occupancy) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
-  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> g(mu);
-  cache[key] = n;
+  int& cur = attr[std::make_tuple(dev, kern)];
+  if (smem > cur) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cur = smem;
+  }
+  const auto it = occ.find(key);
+  if (it != occ.end()) {
+    *per_sm = it->second;
+    return cudaSuccess;
+  }
+  int n = 1;  // cluster kernels (CTA pairs) skip the occupancy query: one CTA per SM by construction
+  if (occupancy) {
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+  }
+  occ[key] = n;
   *per_sm = n;
   return cudaSuccess;
 }

@@ -588,8 +588,9 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
 #pragma unroll
       for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
     }
-    int c = chunk_of(bounds, C, x0 / K);
-    int64_t cend = __ldg(bounds + c + 1) * K;
+    // bounds == nullptr: the whole range is one chunk (mp_hist_u8: counts is [L][E])
+    int c = bounds ? chunk_of(bounds, C, x0 / K) : 0;
+    int64_t cend = bounds ? __ldg(bounds + c + 1) * K : INT64_MAX;
     for (int64_t x = x0; x < x1;) {
       while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
       const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
@@ -736,7 +737,9 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
                           int64_t* hop_sums, int64_t* err, cudaStream_t s, int algo) {
 #define MP_ARGS planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s
   const int widen = max_p <= 15 ? 16 : max_p <= 63 ? 4 : 1;
-  if (W == 0) return launch_t<true, 0, 16>(MP_ARGS);
+  // plain histogram: the pipelined-flush kernel with the whole range as one chunk (pieces end only at
+  // layer ends): 0.836 -> 0.754 ms for 10M R1 tokens against the two-set streaming kernel
+  if (W == 0) return launch_hist_chunks(planes, stride, t0, t1, L, K, E, nullptr, 1, counts, err, s);
   const int chosen = choose_algo(hist, W, algo, t1 - t0, C, L, K, max_p);
   if (chosen == MP_ALGO_SEG)
     return launch_seg(hist, W, planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
