@@ -438,11 +438,17 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
 #ifndef MP_PIPE_SPLIT
 #define MP_PIPE_SPLIT 1
 #endif
-constexpr int kPipeSets = 3;
+// Replica sets per worker: 3 rotate with one piece of slack between warps; 2 need a wait per piece
+// (piece k reuses piece k-2's set) but fit below 128 KB of shared memory, where shared atomics are
+// fast -- sets placed above ~96 KB of the allocation count ~40 % extra ATOMS wavefronts and run
+// ~30 % slower (tools/microbench11.cu, profiles/r2_smem_atoms.txt).  The launcher takes 2 sets for
+// pieces of >= kTwoSetPiece bytes on average (R1 10M / 150 chunks, 533 KB pieces: fused step
+// 0.845 -> 0.805 ms) and 3 for shorter ones (1500 chunks: 1.215 vs 1.335 ms with 2 sets).
+constexpr int kPipeSetsMax = 3;
 constexpr int kPipeHalves = MP_PIPE_SPLIT ? 2 : 1;
 constexpr int kPipeRow = 128 * kPipeHalves;                 // bytes per expert row of one set
 constexpr int kPipeSetBytes = 256 * kPipeRow;
-constexpr int kPipeSmem = kPipeSets * kPipeSetBytes;
+constexpr int kPipeSmemMax = kPipeSetsMax * kPipeSetBytes;
 constexpr int kPipeThreads = kThreads * kPipeHalves;
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
@@ -508,7 +514,7 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
 
 // WC == 0: per-chunk histogram, counts is int64 [C][L][E].  WC > 0: count-contract with WC-word
 // tables; counts (nullable) is int64 [L][E] and hop_sums int64 [4*WC][C].
-template <int WC, int UNROLL>
+template <int WC, int UNROLL, int kPipeSets>
 __global__ void __launch_bounds__(kPipeThreads, 2 / kPipeHalves)
 pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
             const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
@@ -522,14 +528,16 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
   const uint32_t base0 = smem_addr(sm);
   const uint32_t bar0 = smem_addr(&bar[half][0]);
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm) + half * 32;
-  for (int i = threadIdx.x; i < kPipeSmem / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  for (int i = threadIdx.x; i < kPipeSets * kPipeSetBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
   if (tid == 0)
     for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, kThreads);
   __syncthreads();
 
   // flush roles: two threads per bin (16 replicas each, rotated: a warp's 32 loads hit 32 banks)
   const int fe = (int)(tid >> 1), fh = (int)(tid & 1);
-  uint32_t snap[kPipeSets] = {0u, 0u, 0u};
+  uint32_t snap[kPipeSets];
+#pragma unroll
+  for (int b = 0; b < kPipeSets; ++b) snap[b] = 0u;
   // piece k-1 awaiting its flush
   int pk = -1, pl = 0, pc = 0;
   uint32_t ptw[WC > 0 ? WC : 1];
@@ -595,6 +603,9 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
       while (cend <= x && c + 1 < C) cend = __ldg(bounds + (++c) + 1) * K;  // skips empty chunks
       const int64_t xe = min(min(x1, cend), x + (WC > 0 ? kMaxContractPiece : kMaxPiece));
       const int set = k % kPipeSets;
+      if constexpr (kPipeSets == 2) {  // piece k reuses piece k-2's set: every thread must have flushed it
+        if (k >= 2) mbar_wait(bar0 + 8 * ((k - 1) % 2), (uint32_t)(((k - 1) / 2) & 1));
+      }
       pipe_count<UNROLL>(plane, x, xe, base0 + (uint32_t)(set * kPipeSetBytes + half * 128 + (lane << 2)), tid);
       if (pk >= 0) flush_prev();
       mbar_arrive(bar0 + 8 * set);  // counted piece k, flushed piece k-1
@@ -612,23 +623,41 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
   if (pk >= 0) flush_prev();
 }
 
-template <int WC>
-static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
-                               const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
-                               int64_t* hop_sums, int64_t* err, cudaStream_t s) {
-  auto kern = pipe_kernel<WC, MP_COUNT_UNROLL>;
+constexpr int64_t kTwoSetPiece = 128 * 1024;  // crossover measured between 133 KB (C = 600) and 89 KB
+
+template <int WC, int SETS>
+static cudaError_t launch_pipe_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                                 const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
+                                 int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+  auto kern = pipe_kernel<WC, MP_COUNT_UNROLL, SETS>;
+  constexpr int smem = SETS * kPipeSetBytes;
   int per_sm = 0;
-  cudaError_t e = prepare_kernel((const void*)kern, kPipeThreads, kPipeSmem, &per_sm);
+  cudaError_t e = prepare_kernel((const void*)kern, kPipeThreads, smem, &per_sm);
   if (e != cudaSuccess) return e;
   const int nsm = device_sm_count();
   if (per_sm < 1) per_sm = 1;
+  if (per_sm > 2 / kPipeHalves) per_sm = 2 / kPipeHalves;  // one 1024-thread CTA (two workers) per SM
   const int64_t total = (t1 - t0) * (int64_t)K * L;
   int64_t grid = (int64_t)nsm * per_sm;
   const int64_t min_bytes_per_cta = 64 * 1024 * kPipeHalves;
   grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
-  kern<<<(unsigned)grid, kPipeThreads, kPipeSmem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
-                                                        hop_sums, err);
+  kern<<<(unsigned)grid, kPipeThreads, smem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums,
+                                                  err);
   return cudaGetLastError();
+}
+
+template <int WC>
+static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
+                               const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
+                               int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+  const int64_t piece = (t1 - t0) * (int64_t)K / (bounds ? C : 1);  // average (layer, chunk) piece
+#ifdef MP_PIPE_FORCE_SETS
+  if (MP_PIPE_FORCE_SETS == 2)
+#else
+  if (piece >= kTwoSetPiece)
+#endif
+    return launch_pipe_t<WC, 2>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s);
+  return launch_pipe_t<WC, 3>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s);
 }
 
 cudaError_t launch_hist_chunks(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
