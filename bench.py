@@ -704,7 +704,7 @@ def main():
         torch.cuda.synchronize()
         run()
         torch.cuda.synchronize()
-        ok = torch.equal(out_f4, sums_all[:P_ * C].view(P_, C))
+        ok = torch.equal(out_f4, buf[(L * E if with_hist else 0):][:P_ * C].view(P_, C))
         pa, pb = _events()
         n_p = max(3, args.steps // 4)
         pa.record(stream)
