@@ -175,18 +175,37 @@ __device__ __forceinline__ void dedup_warp_range(const uint8_t* __restrict__ pla
   const uint32_t T0lo = (uint32_t)T0;                      // 32-bit relative chunk starts
   auto next_start = [&](int cc) { return (int)(__ldg(reinterpret_cast<const uint32_t*>(bounds + cc)) - T0lo); };
   int nbr = next_start(c + 1);
-  // reduce-scatter<16> slot q = lane >> 1: values 0-3 hops, 4-7 unique servers, 8-11 dedup hops
-  const int qs = lane >> 1;
-  int64_t* hp = (qs < 4 ? hop_sums : qs < 8 ? uniq_sums : dedup_sums) + (int64_t)(qs & 3) * C + c;
+  // lane q < 12 adds value q: 0-3 SPEC hops, 4-7 distinct remote servers, 8-11 deduplicated hops
+  // (placement q & 3)
+  const int qs = lane < 12 ? lane : 0, qk = qs >> 2, qp = qs & 3;
+  int64_t* hp = (qk == 0 ? hop_sums : qk == 1 ? uniq_sums : dedup_sums) + (int64_t)qp * C + c;
   uint32_t h16[2] = {0, 0}, u16[2] = {0, 0}, d16[2] = {0, 0};  // running sums of chunk c, u16 lanes
+  int since = 0;  // windows started since the last flush (warp-uniform)
+  // warp sums by redux.sync (no shuffle traffic; was a 16-value reduce-scatter); word k16[qp & 1]
+  // holds placement qp in its (qp >> 1) half.  Fast records (<= 248 per kind) within 3 windows of
+  // the last flush keep the 6 packed words (32 lanes x 4 windows x 2 x 248 < 2^16).
   auto flush = [&]() {
-    uint32_t v[16] = {h16[0] & 0xffffu, h16[1] & 0xffffu, h16[0] >> 16, h16[1] >> 16,
-                      u16[0] & 0xffffu, u16[1] & 0xffffu, u16[0] >> 16, u16[1] >> 16,
-                      d16[0] & 0xffffu, d16[1] & 0xffffu, d16[0] >> 16, d16[1] >> 16, 0u, 0u, 0u, 0u};
+    const uint32_t w[6] = {h16[0], h16[1], u16[0], u16[1], d16[0], d16[1]};
+    const int j = 2 * qk + (qp & 1);
+    uint32_t t = 0;
+    if (FAST && since <= 3) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, w[i]);
+        t = i == j ? v : t;
+      }
+      t = (qp & 2) ? t >> 16 : t & 0xffffu;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const uint32_t lo = __reduce_add_sync(0xffffffffu, w[i] & 0xffffu);
+        const uint32_t hi = __reduce_add_sync(0xffffffffu, w[i] >> 16);
+        t = i == j ? ((qp & 2) ? hi : lo) : t;
+      }
+    }
     h16[0] = h16[1] = u16[0] = u16[1] = d16[0] = d16[1] = 0;
-    int q = 0;
-    const uint32_t tot = warp_reduce_scatter<16>(v, lane, &q);
-    if ((lane & 1) == 0 && tot && q < 12) atomic_add_i64(hp, (int64_t)tot);
+    since = 0;
+    if (lane < 12 && t) atomic_add_i64(hp, (int64_t)t);
   };
   auto rec = [&](uint32_t w0, uint32_t w1, DedupRec& r) {
     if constexpr (MODE == 2) {
@@ -219,6 +238,7 @@ __device__ __forceinline__ void dedup_warp_range(const uint8_t* __restrict__ pla
   };
   const uint4* __restrict__ pv = reinterpret_cast<const uint4*>(plane) + wm0;
   auto window = [&](const uint4& x, int rfirst, bool edge) {
+    ++since;
     const int tA = 2 * (rfirst + lane);
     DedupRec A, B;
     rec(x.x, x.y, A);

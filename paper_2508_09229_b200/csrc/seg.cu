@@ -8,7 +8,7 @@
 // sub-range in windows of 64 tokens (one 16-byte vector = two 8-pick records per lane, four
 // windows in flight) and keeps running per-lane sums of the current chunk.  Chunk boundaries are
 // detected per window from the chunk bounds (warp-uniform): the tokens before the boundary are
-// added, the warp reduce-scatters its running sums and adds them to hop_sums[q][c] (one int64
+// added, the warp sums its running sums (redux.sync) and adds them to hop_sums[q][c] (one int64
 // atomic per placement), and the sums restart for the next chunk.  The streaming kernels instead
 // spread every (layer, chunk) piece over the whole CTA, so short chunks leave most threads idle;
 // here a boundary costs one warp reduction wherever it falls.
@@ -78,21 +78,37 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
       acc16[2 * w + 1] += prmt(a[w], 0u, 0x7371u) + prmt(b[w], 0u, 0x7371u);  // bytes 1, 3
     }
   };
-  int64_t* hp = nullptr;  // &hop_sums[q][c] of this lane's reduce-scatter slot q (set per warp range)
-  auto flush = [&]() {  // warp-uniform: running sums of the current chunk -> hop_sums[.][c]
-    uint32_t v[P];
+  int64_t* hp = nullptr;  // &hop_sums[p][c] of this lane's placement p = lane & (P - 1) (set per warp range)
+  int since = 0;          // windows started since the last flush (warp-uniform)
+  // warp-uniform: running sums of the current chunk -> hop_sums[.][c].  The warp sums come from
+  // redux.sync, one instruction per word with no shuffle traffic through the shared-memory pipe
+  // (a P = 16 reduce-scatter took 16 SHFL per boundary: 140 tokens per chunk, score W = 4 2.74 ->
+  // 2.49 ms, W = 1 1.04 -> 0.95 ms, fused 1.49 -> 1.39 ms); lane p < P then adds placement p.  Within 3 windows of the
+  // last flush (at most 4 windows of sums: the flushed window's rest + 3) the u16 lanes of the warp
+  // sum cannot overflow (32 lanes x 4 x 2 tokens x 248 < 2^16), so the 2W packed words are summed
+  // as they are; otherwise each u16 lane is summed on its own.
+  auto flush = [&]() {
+    const int pl = lane & (P - 1), j = 2 * (pl >> 2) + (pl & 1);  // word of placement pl; bit 1: high half
+    uint32_t t = 0;
+    if (since <= 3) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      v[4 * w + 0] = acc16[2 * w] & 0xffffu;
-      v[4 * w + 2] = acc16[2 * w] >> 16;
-      v[4 * w + 1] = acc16[2 * w + 1] & 0xffffu;
-      v[4 * w + 3] = acc16[2 * w + 1] >> 16;
-      acc16[2 * w] = 0;
-      acc16[2 * w + 1] = 0;
+      for (int i = 0; i < 2 * W; ++i) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, acc16[i]);
+        t = i == j ? v : t;
+        acc16[i] = 0;
+      }
+      t = (pl & 2) ? t >> 16 : t & 0xffffu;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 2 * W; ++i) {
+        const uint32_t lo = __reduce_add_sync(0xffffffffu, acc16[i] & 0xffffu);
+        const uint32_t hi = __reduce_add_sync(0xffffffffu, acc16[i] >> 16);
+        t = i == j ? ((pl & 2) ? hi : lo) : t;
+        acc16[i] = 0;
+      }
     }
-    int q = 0;
-    const uint32_t tot = warp_reduce_scatter<P>(v, lane, &q);
-    if ((lane & (32 / P - 1)) == 0 && tot) atomic_add_i64(hp, (int64_t)tot);
+    since = 0;
+    if (lane < P && t) atomic_add_i64(hp, (int64_t)t);
   };
   // the 8 lookups (+ histogram increments) of one token record: u8-lane sums per table word
   auto record = [&](uint32_t w0, uint32_t w1, bool valid, uint32_t (&sum)[W]) {
@@ -173,8 +189,7 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
         return (int)(__ldg(reinterpret_cast<const uint32_t*>(bounds + cc)) - T0lo);
       };
       int nbr = next_start(c + 1);  // first token of the next chunk
-      // this lane's reduce-scatter slot (warp_reduce_scatter: q = lane >> (5 - log2 P))
-      hp = hop_sums + (int64_t)(lane >> (P == 4 ? 3 : P == 8 ? 2 : 1)) * C + c;
+      hp = hop_sums + (int64_t)(lane & (P - 1)) * C + c;
       const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane) + wm0;
 
       // one 64-token window: pairs [rfirst, rfirst + 32).  EDGE: it may hold tokens outside
@@ -182,6 +197,7 @@ seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64
       // per-lane validity logic at all.
       auto window = [&](const int4& x, int rfirst, auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
+        ++since;
         bool vA = true, vB = true;
         if constexpr (EDGE) {
           const int tA = 2 * (rfirst + lane);

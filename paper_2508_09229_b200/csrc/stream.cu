@@ -739,13 +739,15 @@ int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K,
   // at R1, profiles/r1_chunk_granularity.txt).
   if (K == 8 && max_p <= 31) {
     // SEG below seg_hi tokens per chunk, TOKEN below tok_lo (R1, 10M tokens, forced algorithms,
-    // profiles/r2_chunk_granularity.txt): hist+W=1 count 1.226 / seg 1.307 ms at 6667 tokens per
-    // chunk, 1.377 / 1.314 at 5000; the token walk (2.13 ms) never wins with a histogram; score W=1
-    // seg 0.79 vs gather 0.99 ms at 6667 tokens per chunk and 0.785 vs 0.774 at 66,667, token 1.32 vs
-    // seg 1.37 at 67 and 1.32 vs 1.04 at 140; W=2 count 1.245 / seg 1.232 at 6667; W=4 count
-    // 1.81 / 2.62 vs seg 2.30 / 2.31 at 3333 / 2000; hist+W=2 and hist+W=4 cross at ~2900 / ~1800.
-    const int seg_hi = hist ? (W == 1 ? 5500 : W == 2 ? 3000 : 1800) : W == 1 ? 20000 : W == 2 ? 7000 : 2400;
-    const int tok_lo = hist ? 0 : W == 1 ? 80 : 0;
+    // after the redux.sync flush; profiles/r2_crossovers.txt): hist+W=1 count 1.300 / seg 1.310 ms
+    // at 5000 tokens per chunk, 1.220 / 1.308 at 6667; the token walk (2.13 ms) never wins with a
+    // histogram; score W=1 seg 0.770 / gather 0.774 at 33,333 tokens per chunk, seg 1.20 vs token
+    // 1.32 at 67 and 1.04 vs 1.32 at 100 (seg ~ 0.77 + 28 / tokens-per-chunk ms: even at ~50);
+    // W=2 count 1.185 / seg 1.222 at 6667, 1.302 / 1.227 at 5000; W=4 count 1.929 / 2.433 vs seg
+    // 2.31 at 3333 / 2000; hist+W=2 count 1.836 vs seg 1.794 at 3000; hist+W=4 count ~0.88 + 3240 /
+    // tokens-per-chunk vs seg 3.03: even at ~1500.
+    const int seg_hi = hist ? (W == 1 ? 5000 : W == 2 ? 3000 : 1500) : W == 1 ? 40000 : W == 2 ? 6000 : 2400;
+    const int tok_lo = hist ? 0 : W == 1 ? 50 : 0;
     if (tok_ok && tokens < (int64_t)tok_lo * C) return MP_ALGO_TOKEN;
     if (tokens < (int64_t)seg_hi * C) return MP_ALGO_SEG;
     return (hist || W > 1) ? MP_ALGO_COUNT : MP_ALGO_GATHER;

@@ -127,13 +127,13 @@ def test_integration_stub_matches_the_abi():
 
 def test_auto_algorithm_rule():
     """mp_choose_algo (host-only) is the rule MP_ALGO_AUTO applies: the crossovers measured for R1
-    (profiles/r2_chunk_granularity.txt) -- count-contract / gather for long chunks, the segmented
+    (profiles/r2_crossovers.txt) -- count-contract / gather for long chunks, the segmented
     gather for dialog-length ones, the token walk only for the shortest score-only chunks."""
     N, L, K = 10_000_000, 58, 8
-    tpc = {150: 66_667, 1500: 6667, 2000: 5000, 71_429: 140, 150_000: 67}
+    tpc = {150: 66_667, 1500: 6667, 2000: 5000, 2500: 4000, 71_429: 140, 150_000: 67, 250_000: 40}
     want = {  # (hist, W): algorithm per chunk count
-        (True, 1): {150: "count", 1500: "count", 2000: "seg", 71_429: "seg", 150_000: "seg"},
-        (False, 1): {150: "gather", 1500: "seg", 2000: "seg", 71_429: "seg", 150_000: "token"},
+        (True, 1): {150: "count", 1500: "count", 2000: "count", 2500: "seg", 71_429: "seg", 150_000: "seg"},
+        (False, 1): {150: "gather", 1500: "seg", 2000: "seg", 71_429: "seg", 150_000: "seg", 250_000: "token"},
         (False, 4): {150: "count", 1500: "count", 2000: "count", 71_429: "seg", 150_000: "seg"},
         (True, 4): {150: "count", 1500: "count", 2000: "count", 71_429: "seg", 150_000: "seg"},
     }

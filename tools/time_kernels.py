@@ -23,6 +23,7 @@ ap.add_argument("--out")
 ap.add_argument("--lib", help="load this libmoeplace_cuda.so variant instead of the product build")
 ap.add_argument("--only", default="")
 ap.add_argument("--chunks", type=int, default=150)
+ap.add_argument("--dump", help="save each kernel's hop sums / counts (zeroed before it runs) to this .npz")
 a = ap.parse_args()
 if a.lib:
     from pathlib import Path
@@ -96,13 +97,21 @@ def run_ext(w):
 _pk = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
 PEAK = float(json.load(open(_pk)).get("hbm_gbs", 6458.4)) if os.path.exists(_pk) else 6458.4
 res = {}
+dumps = {}
 bytes_ = a.tokens * L * K
 for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4", "fused", "token_hops", "hist_chunks", "dedup")):
     base = w
     for suf in ("_gather", "_count", "_token", "_seg"):
         base = base[:-len(suf)] if base.endswith(suf) else base
     fn = run if base in ("hist", "score1", "score2", "score4", "fused", "fused2", "fused4") else run_ext
-    for _ in range(3):
+    s.zero_()
+    cnt.zero_()
+    fn(w)
+    torch.cuda.synchronize()
+    if a.dump:
+        dumps[w + "_sums"] = s.cpu().numpy().copy()
+        dumps[w + "_counts"] = cnt.cpu().numpy().copy()
+    for _ in range(2):
         fn(w)
     ts = []
     for _ in range(a.reps):
@@ -115,6 +124,8 @@ for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4"
     ms = float(np.mean(ts))
     res[w] = {"ms": ms, "min_ms": float(min(ts)), "GBps": bytes_ / ms / 1e6, "frac_hbm": bytes_ / ms / 1e6 / PEAK}
     print(f"{w:8s} {ms:7.3f} ms (min {min(ts):.3f})  {bytes_ / ms / 1e6:8.1f} GB/s  {100 * bytes_ / ms / 1e6 / PEAK:5.1f}%")
+if a.dump:
+    np.savez(a.dump, **dumps)
 if a.only:
     if a.out:
         json.dump(res, open(a.out, "w"), indent=1)
