@@ -4,7 +4,7 @@
 //
 // A CTA walks its byte range plane segment by plane segment like the streaming kernels and stages
 // the layer's W-word table replicated per lane slot (conflict-free PRMT-addressed lookups).  The
-// segment's tokens are then split into 16 contiguous warp sub-ranges; a warp streams its
+// segment's tokens are then split into 32 contiguous warp sub-ranges; a warp streams its
 // sub-range in windows of 64 tokens (one 16-byte vector = two 8-pick records per lane, four
 // windows in flight) and keeps running per-lane sums of the current chunk.  Chunk boundaries are
 // detected per window from the chunk bounds (warp-uniform): the tokens before the boundary are
@@ -22,7 +22,15 @@
 
 namespace mp {
 
-constexpr int kSegWarps = kThreads / 32;  // 16
+// One 1024-thread CTA per SM: its tables + histogram (64 / 96 KB) stay below the upper part of the
+// shared-memory carve-out, where atomics run ~30 % slower (profiles/r2_smem_atoms.txt); two 512-thread
+// CTAs put the second one's there.  140 tokens per chunk: fused 1.387 -> 1.322 ms, hist + W = 2
+// 1.929 -> 1.816, hist + W = 4 3.267 -> 3.171, score W = 1 0.950 -> 0.928 (profiles/r2_seg_cta1024.txt).
+#ifndef MP_SEG_THREADS
+#define MP_SEG_THREADS 1024
+#endif
+constexpr int kSegThreads = MP_SEG_THREADS;
+constexpr int kSegWarps = kSegThreads / 32;
 // windows in flight per warp for W = 1 (R1 10M tokens, 4 placements, 1500 / 15k / 150k chunks):
 // 2: 1.035 / 1.112 / 1.895 ms, 4: 0.985 / 1.052 / 1.841 ms, 8: 1.014 / 1.087 / 1.853 ms (spills)
 #ifndef MP_SEG_U1
@@ -45,7 +53,7 @@ __device__ __forceinline__ void seg_lookup(uint32_t a, uint32_t (&t)[W]) {
 }
 
 template <int W, bool HIST>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kSegThreads, 1024 / kSegThreads)
 seg_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int E,
            const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
            int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
@@ -283,13 +291,13 @@ static cudaError_t launch_seg_t(const uint8_t* planes, int64_t stride, int64_t t
   auto kern = seg_kernel<W, HIST>;
   const int smem = 256 * 256 + ((HIST && W > 1) ? 256 * 128 : 0) + 128;
   int per_sm = 0;
-  cudaError_t e = prepare_kernel((const void*)kern, kThreads, smem, &per_sm);
+  cudaError_t e = prepare_kernel((const void*)kern, kSegThreads, smem, &per_sm);
   if (e != cudaSuccess) return e;
   const int nsm = device_sm_count();
   const int64_t total = (t1 - t0) * 8 * (int64_t)L;
   int64_t grid = (int64_t)nsm * max(1, per_sm);
   grid = max((int64_t)1, min(grid, (total + 65535) / 65536));
-  kern<<<(unsigned)grid, kThreads, smem, s>>>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err);
+  kern<<<(unsigned)grid, kSegThreads, smem, s>>>(planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err);
   return cudaGetLastError();
 }
 
