@@ -65,7 +65,10 @@ def _check(tr, sel, bounds, t0, pls, p, W, hist_ws=(1,)):
 
 @pytest.mark.parametrize("W", [1, 2, 4])
 @pytest.mark.parametrize("shape", [R1, B16, (3, 5, 2), (5, 200, 7)])
-def test_algorithms_agree_with_oracle(shape, W):
+@pytest.mark.parametrize("cmax", [13, 32])
+def test_algorithms_agree_with_oracle(shape, W, cmax):
+    """Costs < 13 take the segmented gather's nibble tables (W = 2 / 4, max_p <= 15); costs up to 31
+    its u8 tables."""
     L, E, K = shape
     m = mt.ModelSpec(L, E, K)
     N, C = 5003, 17
@@ -73,7 +76,7 @@ def test_algorithms_agree_with_oracle(shape, W):
     sel, bounds = og.generate(L, E, K, 1.2, N, C, 3)
     rng = np.random.default_rng(W)
     S = 24
-    p = rng.integers(0, 13, (L, S)).astype(np.uint8)
+    p = rng.integers(0, cmax, (L, S)).astype(np.uint8)
     pls = [mpl.Placement(random_assign(rng, L, E, S)) for _ in range(4 * W - (1 if W > 1 else 0))]
     _check(tr, sel, bounds, 0, pls, p, W)
     # a chunk sub-range view (token range starts mid-trace; plane byte offsets unaligned)
