@@ -516,6 +516,29 @@ def test_token_hops_all_matches_oracle(shape, kind, maxp):
     assert ev.hop_distribution(tr, pls[0], cost).sum() == N
 
 
+def test_token_hops_all_multi_tile_ranges():
+    """Per-CTA token ranges of several 4096-token tiles (the TMA ring walks tile x layer steps across
+    tile ends), an odd token count and a view starting on an odd token (slices 8 bytes into a
+    16-byte line) == the oracle."""
+    import torch
+    L, E, K = 3, 256, 8
+    m = mt.ModelSpec(L, E, K)
+    N = 1_300_001
+    tr = mt.generate_trace(m, 1.2, N, 7, 11)
+    sel, bounds = og.generate(L, E, K, 1.2, N, 7, 11)
+    rng = np.random.default_rng(8)
+    p = rng.integers(0, 32, (L, 16)).astype(np.uint8)
+    cost = mpl.CostMatrix(torch.as_tensor(p, device="cuda"))
+    pls = [mpl.Placement(random_assign(rng, L, E, 16)) for _ in range(2)]
+    got = ev.token_hops_all(tr, pls, cost)
+    for i, pl in enumerate(pls):
+        assert np.array_equal(got[i], oe.per_token_hops(sel, oe.pe_table(p, pl.assign)))
+    odd = next(c for c in range(1, 7) if bounds[c] % 2 == 1) if any(b % 2 for b in bounds[1:7]) else 1
+    v = tr.view(odd, 7)
+    gv = ev.token_hops_all(v, pls[:1], cost)[0]
+    assert np.array_equal(gv, got[0][bounds[odd]:bounds[7]])
+
+
 @pytest.mark.parametrize("shape", [R1, B16, (3, 5, 2)])
 def test_factorized_evaluator_matches_gather(shape):
     """per-chunk histograms + exact contraction == per-token gather, bit for bit, for
