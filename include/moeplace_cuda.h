@@ -174,15 +174,15 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
  *     down sharply for short chunks.  Requires L*K*max_p <= 65535 (else MP_ERR_UNSUPPORTED);
  *     with a histogram it is mp_hist_u8 + the token pass;
  *   MP_ALGO_AUTO:   the faster one for the shape, by average tokens per chunk (measured
- *     crossovers, mp_choose_algo): when SEG applies (K = 8, max_p <= 31) SEG below 5500 / 3000 /
- *     1800 (with a histogram, W = 1 / 2 / 4) and 20000 / 7000 / 2400 (score-only) tokens per
- *     chunk, TOKEN below 80 (score-only W = 1); otherwise TOKEN below MP_TOKEN_CHUNK_TOKENS (W = 1 with
+ *     crossovers, mp_choose_algo): when SEG applies (K = 8, max_p <= 31) SEG below 5000 / 3000 /
+ *     1500 (with a histogram, W = 1 / 2 / 4) and 40000 / 6000 / 2400 (score-only) tokens per
+ *     chunk, TOKEN below 50 (score-only W = 1); otherwise TOKEN below MP_TOKEN_CHUNK_TOKENS (W = 1 with
  *     a histogram; half of it for W = 2, 700 for W = 4; score-only 4096 / 1600 / 800) when the
  *     limit above holds; else GATHER for score-only W = 1 and COUNT otherwise.  This is what
  *     mp_score_u8 / mp_hist_score_u8 use.
  *   MP_ALGO_SEG:    segmented gather -- a layer-major stream in which each warp owns a contiguous
  *     token range and reduces its running sums at every chunk boundary it crosses (a warp
- *     reduction per boundary, no per-piece CTA work), so it is C-independent like TOKEN while
+ *     redux.sync per boundary, no per-piece CTA work), so it is C-independent like TOKEN while
  *     reading each layer's table once per CTA segment.  K = 8 and max_p <= 31 only (else
  *     MP_ERR_UNSUPPORTED); the histogram is fused for every W.
  * mp_hist_score_ex_u8 takes W = 1, 2 or 4 (GATHER supports W = 1 only -> MP_ERR_UNSUPPORTED).   */
