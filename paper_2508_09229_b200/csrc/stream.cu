@@ -445,11 +445,22 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
 // pieces of >= kTwoSetPiece bytes on average (R1 10M / 150 chunks, 533 KB pieces: fused step
 // 0.845 -> 0.805 ms) and 3 for shorter ones (1500 chunks: 1.215 vs 1.335 ms with 2 sets).
 constexpr int kPipeSetsMax = 3;
-constexpr int kPipeHalves = MP_PIPE_SPLIT ? 2 : 1;
-constexpr int kPipeRow = 128 * kPipeHalves;                 // bytes per expert row of one set
-constexpr int kPipeSetBytes = 256 * kPipeRow;
-constexpr int kPipeSmemMax = kPipeSetsMax * kPipeSetBytes;
-constexpr int kPipeThreads = kThreads * kPipeHalves;
+constexpr int kPipeHalves = MP_PIPE_SPLIT ? 2 : 1;  // workers per CTA (count-contract, per-chunk histogram)
+// A CTA of HALVES workers of WT threads; one set = 256 expert rows of HALVES x 128 bytes (worker h's
+// 32 lane replicas at bytes h*128 .. h*128+127 of each row).
+template <int WT, int HALVES>
+struct PipeShape {
+  static constexpr int kWT = WT, kHalves = HALVES, kThreads = WT * HALVES;
+  static constexpr int kRow = 128 * HALVES;
+  static constexpr int kSetBytes = 256 * kRow;
+};
+using PipeCC = PipeShape<kThreads, kPipeHalves>;  // count-contract / per-chunk histogram: 2 x 512 threads
+// The plain histogram (one chunk: pieces end only at layer ends, a handful of flushes) runs ONE
+// 1024-thread worker whose three 32 KB sets all sit below 96 KB of shared memory: 0.769 -> 0.726 ms
+// for 10M R1 tokens (98.9 % of HBM); with short pieces the single worker is slower (one piece at a
+// time for the whole SM: 1500 chunks 1.20 -> 1.57 ms), so the chunked instances keep two workers
+// (profiles/r2_pipe_workers.txt).
+using PipeHist = PipeShape<1024, 1>;
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -464,15 +475,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
       : "memory");
 }
 
-// ATOMS increments for bytes [xa, xb) of one plane; sb = shared address of this lane's replica of bin 0 in the piece's set (bin e at sb + e * kPipeRow)
-template <int UNROLL>
+// ATOMS increments for bytes [xa, xb) of one plane by the T threads of a worker; sb = shared address
+// of this lane's replica of bin 0 in the piece's set (bin e at sb + e * ROW)
+template <int UNROLL, uint32_t T, uint32_t ROW>
 __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, int64_t xa, int64_t xb, uint32_t sb,
                                            uint32_t tid) {
-  constexpr uint32_t T = kThreads;  // threads of one (half-)CTA
   const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
   const int64_t tb = max(ha, xb & ~(int64_t)15);
-  for (int64_t x = xa + tid; x < ha; x += T) atoms_inc(sb + (uint32_t)plane[x] * (uint32_t)kPipeRow);
-  for (int64_t x = tb + tid; x < xb; x += T) atoms_inc(sb + (uint32_t)plane[x] * (uint32_t)kPipeRow);
+  for (int64_t x = xa + tid; x < ha; x += T) atoms_inc(sb + (uint32_t)plane[x] * ROW);
+  for (int64_t x = tb + tid; x < xb; x += T) atoms_inc(sb + (uint32_t)plane[x] * ROW);
   const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
   const uint32_t nv = (uint32_t)((tb - ha) >> 4);
   auto vec = [&](const int4& x) {
@@ -480,7 +491,7 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) atoms_inc(prmt(wd[q], 0u, 0x4440u | (uint32_t)b) * (uint32_t)kPipeRow + sb);
+      for (int b = 0; b < 4; ++b) atoms_inc(prmt(wd[q], 0u, 0x4440u | (uint32_t)b) * ROW + sb);
   };
   uint32_t v = tid;
   for (; v + (UNROLL - 1) * T < nv; v += UNROLL * T) {
@@ -514,23 +525,25 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
 
 // WC == 0: per-chunk histogram, counts is int64 [C][L][E].  WC > 0: count-contract with WC-word
 // tables; counts (nullable) is int64 [L][E] and hop_sums int64 [4*WC][C].
-template <int WC, int UNROLL, int kPipeSets>
-__global__ void __launch_bounds__(kPipeThreads, 2 / kPipeHalves)
+template <int WC, int UNROLL, int kPipeSets, class Shape>
+__global__ void __launch_bounds__(Shape::kThreads, 1024 / Shape::kThreads)
 pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
             const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
             int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
+  constexpr int kPipeWT = Shape::kWT, kPipeHalves = Shape::kHalves;
+  constexpr int kPipeRow = Shape::kRow, kPipeSetBytes = Shape::kSetBytes;
   extern __shared__ __align__(128) uint8_t sm[];  // kPipeSets x 256 rows x kPipeRow B
   __shared__ __align__(8) uint64_t bar[kPipeHalves][kPipeSets];
   constexpr int PC = 4 * (WC > 0 ? WC : 1);
   const int lane = threadIdx.x & 31;
-  const int half = kPipeHalves > 1 ? (int)(threadIdx.x >> 9) : 0;  // independent 512-thread halves
-  const uint32_t tid = threadIdx.x & (kThreads - 1);
+  const int half = kPipeHalves > 1 ? (int)(threadIdx.x / kPipeWT) : 0;  // independent workers
+  const uint32_t tid = threadIdx.x & (kPipeWT - 1);
   const uint32_t base0 = smem_addr(sm);
   const uint32_t bar0 = smem_addr(&bar[half][0]);
   uint32_t* smw = reinterpret_cast<uint32_t*>(sm) + half * 32;
   for (int i = threadIdx.x; i < kPipeSets * kPipeSetBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
   if (tid == 0)
-    for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, kThreads);
+    for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, kPipeWT);
   __syncthreads();
 
   // flush roles: two threads per bin (16 replicas each, rotated: a warp's 32 loads hit 32 banks)
@@ -606,7 +619,7 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
       if constexpr (kPipeSets == 2) {  // piece k reuses piece k-2's set: every thread must have flushed it
         if (k >= 2) mbar_wait(bar0 + 8 * ((k - 1) % 2), (uint32_t)(((k - 1) / 2) & 1));
       }
-      pipe_count<UNROLL>(plane, x, xe, base0 + (uint32_t)(set * kPipeSetBytes + half * 128 + (lane << 2)), tid);
+      pipe_count<UNROLL, (uint32_t)kPipeWT, (uint32_t)kPipeRow>(plane, x, xe, base0 + (uint32_t)(set * kPipeSetBytes + half * 128 + (lane << 2)), tid);
       if (pk >= 0) flush_prev();
       mbar_arrive(bar0 + 8 * set);  // counted piece k, flushed piece k-1
       pk = k++;
@@ -625,24 +638,24 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
 
 constexpr int64_t kTwoSetPiece = 128 * 1024;  // crossover measured between 133 KB (C = 600) and 89 KB
 
-template <int WC, int SETS>
+template <int WC, int SETS, class Shape = PipeCC>
 static cudaError_t launch_pipe_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                                  const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                                  int64_t* hop_sums, int64_t* err, cudaStream_t s) {
-  auto kern = pipe_kernel<WC, MP_COUNT_UNROLL, SETS>;
-  constexpr int smem = SETS * kPipeSetBytes;
+  auto kern = pipe_kernel<WC, MP_COUNT_UNROLL, SETS, Shape>;
+  constexpr int smem = SETS * Shape::kSetBytes;
   int per_sm = 0;
-  cudaError_t e = prepare_kernel((const void*)kern, kPipeThreads, smem, &per_sm);
+  cudaError_t e = prepare_kernel((const void*)kern, Shape::kThreads, smem, &per_sm);
   if (e != cudaSuccess) return e;
   const int nsm = device_sm_count();
   if (per_sm < 1) per_sm = 1;
-  if (per_sm > 2 / kPipeHalves) per_sm = 2 / kPipeHalves;  // one 1024-thread CTA (two workers) per SM
+  if (per_sm > 1024 / Shape::kThreads) per_sm = 1024 / Shape::kThreads;  // 1024 threads per SM
   const int64_t total = (t1 - t0) * (int64_t)K * L;
   int64_t grid = (int64_t)nsm * per_sm;
-  const int64_t min_bytes_per_cta = 64 * 1024 * kPipeHalves;
+  const int64_t min_bytes_per_cta = 64 * 1024 * Shape::kHalves;
   grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
-  kern<<<(unsigned)grid, kPipeThreads, smem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums,
-                                                  err);
+  kern<<<(unsigned)grid, Shape::kThreads, smem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
+                                                     hop_sums, err);
   return cudaGetLastError();
 }
 
@@ -769,8 +782,14 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
 #define MP_ARGS planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s
   const int widen = max_p <= 15 ? 16 : max_p <= 63 ? 4 : 1;
   // plain histogram: the pipelined-flush kernel with the whole range as one chunk (pieces end only at
-  // layer ends): 0.836 -> 0.754 ms for 10M R1 tokens against the two-set streaming kernel
+  // layer ends): 0.836 -> 0.754 ms for 10M R1 tokens against the two-set streaming kernel, 0.726 ms
+  // with one 1024-thread worker per SM
+#if MP_PIPE_FLUSH
+  if (W == 0)  // one 1024-thread worker, three 32 KB sets (PipeHist)
+    return launch_pipe_t<0, 3, PipeHist>(planes, stride, t0, t1, L, K, E, nullptr, 1, nullptr, counts, nullptr, err, s);
+#else
   if (W == 0) return launch_hist_chunks(planes, stride, t0, t1, L, K, E, nullptr, 1, counts, err, s);
+#endif
   const int chosen = choose_algo(hist, W, algo, t1 - t0, C, L, K, max_p);
   if (chosen == MP_ALGO_SEG)
     return launch_seg(hist, W, planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
