@@ -482,10 +482,11 @@ def main():
         tables, max_p = ev._group_tables(placements, costs, model, 1)
         groups.append((1, tables, max_p, P_))
     else:
-        for g0 in range(0, P_, 16):
-            grp = placements[g0:g0 + 16]
+        lanes = ev.pass_lanes(trace, costs)  # 32 per count-contract pass (config 3: P = 24 in one pass)
+        for g0 in range(0, P_, lanes):
+            grp = placements[g0:g0 + lanes]
             W = ev._lanes_for(len(grp))
-            tables, max_p = ev._group_tables(grp, costs[g0:g0 + 16], model, W)
+            tables, max_p = ev._group_tables(grp, costs[g0:g0 + lanes], model, W)
             groups.append((W, tables, max_p, len(grp)))
     n_sums = sum(4 * W for W, _, _, _ in groups)
     with_hist = wl in (2, 5)
@@ -715,7 +716,7 @@ def main():
         p_ms = pa.elapsed_time(pb) / n_p
         passes = {"ms_per_step": p_ms, "launches_per_step": len(groups), "algorithm": "count-contract",
                   "value": n_total * L * P_ / (p_ms / 1e3), "bit_identical_to_step": ok,
-                  "note": "evaluate_many(method='count'): 256 mp_score_u8 W=4 passes over the resident trace"}
+                  "note": f"evaluate_many(method='count'): {len(groups)} mp_score_u8 W={groups[0][0]} passes over the resident trace"}
 
     # ---------------- e2e through the public API, host buffers ----------------
     e2e = None

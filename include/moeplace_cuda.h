@@ -132,7 +132,8 @@ int mp_contract_tc_u8(const uint8_t* pe, int P, int64_t ldpe, const uint8_t* dig
 
 /* ---- placement tables: Placement -> per-expert round-trip hops ---------
  * tables[((l*256 + e)*W + w)] is a u32 whose byte j is pe_q[l][e] = cost[topo_of[q]][l][assign[q][l][e]]
- * for placement q = 4*w + j (q < P; unused lanes and e >= E are 0).  W = 1, 2 or 4 (P <= 4W).
+ * for placement q = 4*w + j (q < P; unused lanes and e >= E are 0).  W = 1, 2, 4 or 8 (P <= 4W;
+ * W = 8 -- 32 placements per pass -- runs the count-contract algorithm only).
  *   cost: device uint8[T][L][S]; assign: device int32[P][L][E]; topo_of: device int32[P]      */
 int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int32_t* topo_of, int P,
                    int L, int E, int S, uint32_t* tables, int W, int64_t* err, void* stream);
@@ -185,7 +186,8 @@ int mp_hist_score_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_be
  *     redux.sync per boundary, no per-piece CTA work), so it is C-independent like TOKEN while
  *     reading each layer's table once per CTA segment.  K = 8 and max_p <= 31 only (else
  *     MP_ERR_UNSUPPORTED); the histogram is fused for every W.
- * mp_hist_score_ex_u8 takes W = 1, 2 or 4 (GATHER supports W = 1 only -> MP_ERR_UNSUPPORTED).   */
+ * mp_hist_score_ex_u8 takes W = 1, 2, 4 or 8 (GATHER supports W = 1 only, and W = 8 COUNT / AUTO
+ * only -> MP_ERR_UNSUPPORTED).                                                                     */
 #define MP_ALGO_AUTO 0
 #define MP_ALGO_GATHER 1
 #define MP_ALGO_COUNT 2

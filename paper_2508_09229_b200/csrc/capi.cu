@@ -159,7 +159,7 @@ int mp_pack_tables(const uint8_t* cost, int T, const int32_t* assign, const int3
                    int S_, uint32_t* tables, int W, int64_t* err, void* stream) {
   if (E > mp::kMaxE) return MP_ERR_UNSUPPORTED;
   if (!cost || !assign || !topo_of || !tables || !err || T <= 0 || P <= 0 || L <= 0 || E <= 0 || S_ <= 0) return MP_ERR_ARG;
-  if (!(W == 1 || W == 2 || W == 4) || P > 4 * W) return MP_ERR_ARG;
+  if (!(W == 1 || W == 2 || W == 4 || W == 8) || P > 4 * W) return MP_ERR_ARG;
   return status(mp::launch_pack(cost, T, assign, topo_of, P, L, E, S_, tables, W, err, S(stream)));
 }
 
@@ -168,9 +168,10 @@ int mp_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok_begi
                    int algo, void* stream) {
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
-  if (!chunk_bounds || C <= 0 || !tables || !hop_sums || !(W == 1 || W == 2 || W == 4)) return MP_ERR_ARG;
+  if (!chunk_bounds || C <= 0 || !tables || !hop_sums || !(W == 1 || W == 2 || W == 4 || W == 8)) return MP_ERR_ARG;
   if (max_p < 0 || algo < MP_ALGO_AUTO || algo > MP_ALGO_SEG) return MP_ERR_ARG;
   if (max_p > 255 || (algo == MP_ALGO_TOKEN && (int64_t)L * K * max_p > 65535)) return MP_ERR_UNSUPPORTED;
+  if (W == 8 && algo != MP_ALGO_AUTO && algo != MP_ALGO_COUNT) return MP_ERR_UNSUPPORTED;  // 32 lanes: count-contract only
   if (algo == MP_ALGO_SEG && (K != 8 || max_p > 31)) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;
   return status(mp::launch_stream(false, W, max_p, planes, plane_stride, tok_begin, tok_end, L, K, 256, chunk_bounds,
@@ -202,8 +203,9 @@ int mp_hist_score_ex_u8(const uint8_t* planes, int64_t plane_stride, int64_t tok
   int r = check_trace(planes, plane_stride, tok_begin, tok_end, L, K);
   if (r) return r;
   if (E <= 0 || !counts || !err || !chunk_bounds || C <= 0 || !tables || !hop_sums || max_p < 0) return MP_ERR_ARG;
-  if (!(W == 1 || W == 2 || W == 4) || algo < MP_ALGO_AUTO || algo > MP_ALGO_SEG) return MP_ERR_ARG;
+  if (!(W == 1 || W == 2 || W == 4 || W == 8) || algo < MP_ALGO_AUTO || algo > MP_ALGO_SEG) return MP_ERR_ARG;
   if (max_p > 255 || (algo == MP_ALGO_GATHER && W != 1)) return MP_ERR_UNSUPPORTED;
+  if (W == 8 && algo != MP_ALGO_AUTO && algo != MP_ALGO_COUNT) return MP_ERR_UNSUPPORTED;  // 32 lanes: count-contract only
   if (algo == MP_ALGO_SEG && (K != 8 || max_p > 31)) return MP_ERR_UNSUPPORTED;
   if (algo == MP_ALGO_TOKEN && (int64_t)L * K * max_p > 65535) return MP_ERR_UNSUPPORTED;
   if (tok_end == tok_begin) return MP_OK;

@@ -553,7 +553,6 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
   for (int b = 0; b < kPipeSets; ++b) snap[b] = 0u;
   // piece k-1 awaiting its flush
   int pk = -1, pl = 0, pc = 0;
-  uint32_t ptw[WC > 0 ? WC : 1];
   auto flush_prev = [&]() {
     const int set = pk % kPipeSets;
     mbar_wait(bar0 + 8 * set, (uint32_t)((pk / kPipeSets) & 1));  // every thread finished counting piece pk
@@ -584,11 +583,16 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
         else report_err(err, MP_DATA_EXPERT_RANGE, pl, fe, n);
       }
       if (__any_sync(0xffffffffu, n != 0)) {
+        // the piece's table words are read here (L1-resident) rather than held in registers across
+        // the count loop: WC = 8 would otherwise pin 16 more registers at the 64-register budget
+        const uint32_t* tp = tables + ((int64_t)pl * 256 + (fe < 256 ? fe : 0)) * WC;
         uint32_t v[PC];
 #pragma unroll
-        for (int w = 0; w < WC; ++w)
+        for (int w = 0; w < WC; ++w) {
+          const uint32_t tw = n ? __ldg(tp + w) : 0u;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) v[4 * w + j] = n * ((ptw[w] >> (8 * j)) & 0xffu);
+          for (int j = 0; j < 4; ++j) v[4 * w + j] = n * ((tw >> (8 * j)) & 0xffu);
+        }
         int q = 0;
         const uint32_t tot = warp_reduce_scatter<PC>(v, lane, &q);
         if ((lane & (32 / PC - 1)) == 0 && tot) atomic_add_i64(hop_sums + (int64_t)q * C + pc, (int64_t)tot);
@@ -604,11 +608,6 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
     const int64_t seg = min(f.g1 - g, f.nb - off_in);
     const int64_t x0 = f.b0 + off_in, x1 = x0 + seg;
     const uint8_t* plane = planes + (int64_t)l * stride;
-    uint32_t tw[WC > 0 ? WC : 1];
-    if constexpr (WC > 0) {
-#pragma unroll
-      for (int w = 0; w < WC; ++w) tw[w] = fe < 256 ? __ldg(tables + ((int64_t)l * 256 + fe) * WC + w) : 0u;
-    }
     // bounds == nullptr: the whole range is one chunk (mp_hist_u8: counts is [L][E])
     int c = bounds ? chunk_of(bounds, C, x0 / K) : 0;
     int64_t cend = bounds ? __ldg(bounds + c + 1) * K : INT64_MAX;
@@ -625,10 +624,6 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
       pk = k++;
       pl = l;
       pc = c;
-      if constexpr (WC > 0) {
-#pragma unroll
-        for (int w = 0; w < WC; ++w) ptw[w] = tw[w];
-      }
       x = xe;
     }
     g += seg;
@@ -745,6 +740,7 @@ int token_threshold(bool hist, int W) {
 
 int choose_algo(bool hist, int W, int algo, int64_t tokens, int C, int L, int K, int max_p) {
   if (algo != MP_ALGO_AUTO) return algo;
+  if (W == 8) return MP_ALGO_COUNT;  // 32 placements per pass: the count-contract kernel only
   const bool tok_ok = (int64_t)L * K * max_p <= 65535;
   // Segmented gather (K = 8, max_p <= 31; with a histogram W = 1): C-independent and cheaper than
   // the token walk for W >= 2 and for the fused pass, so it takes the short-chunk range from
@@ -807,6 +803,7 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
     if (W == 1) return launch_pipe<1>(MP_ARGS);
     if (W == 2) return launch_pipe<2>(MP_ARGS);
     if (W == 4) return launch_pipe<4>(MP_ARGS);
+    if (W == 8) return launch_pipe<8>(MP_ARGS);
 #else
     if (W == 1) return launch_t<true, 0, 16, true, 1>(MP_ARGS);
     if (W == 2) return launch_t<true, 0, 16, true, 2>(MP_ARGS);

@@ -21,7 +21,8 @@ from .errors import ConfigError, MoeplaceError
 from .model_trace import ActivationTrace, FrequencyTable, ModelSpec, chunk_counts, frequencies_from_counts, sweep
 from .placement import CostMatrix, Placement
 
-MAX_LANES = 16  # placements scored per pass (W = 4 words of four u8 lanes)
+MAX_LANES = 16  # placements scored per pass by every algorithm (W = 4 words of four u8 lanes)
+MAX_LANES_COUNT = 32  # per count-contract pass (W = 8): its per-placement work is per piece, not per byte
 FACTORIZED_MAX_BYTES = 4 << 30  # evaluate_many(auto): largest per-chunk count array worth materialising
 
 
@@ -218,7 +219,24 @@ def _group_tables(placements: Sequence[Placement], costs: Sequence[CostMatrix], 
 
 
 def _lanes_for(n: int) -> int:
-    return 1 if n <= 4 else 2 if n <= 8 else 4
+    return 1 if n <= 4 else 2 if n <= 8 else 4 if n <= 16 else 8
+
+
+def pass_lanes(trace: ActivationTrace, costs, algo: str = "auto", hist: bool = False) -> int:
+    """Placements per scoring pass: 32 when the pass runs the count-contract kernel (``algo`` "count",
+    or "auto" where the library picks it for this shape, i.e. long chunks) -- a 24-placement batch is
+    then one pass, not two -- else 16."""
+    if algo == "count":
+        return MAX_LANES_COUNT
+    if algo != "auto":
+        return MAX_LANES
+    m = trace.model
+    if m is None or trace.n_tokens == 0:
+        return MAX_LANES
+    cs = [costs] if isinstance(costs, CostMatrix) else list(costs)
+    max_p = max((c.max_p for c in _unique_costs(cs)[0]), default=0)
+    auto = _lib.choose_algo(hist, 4, trace.n_tokens, trace.n_chunks, m.L, m.K, max_p)
+    return MAX_LANES_COUNT if auto == "count" else MAX_LANES
 
 
 ALGOS = {"auto": 0, "gather": 1, "count": 2, "token": 3, "seg": 4}  # include/moeplace_cuda.h MP_ALGO_*
@@ -242,10 +260,11 @@ def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, a
     C = trace.n_chunks
     dev = _lib.require_cuda()
     groups = []
-    for g0 in range(0, len(placements), MAX_LANES):
-        grp = placements[g0:g0 + MAX_LANES]
+    lanes = pass_lanes(trace, costs, algo)
+    for g0 in range(0, len(placements), lanes):
+        grp = placements[g0:g0 + lanes]
         W = _lanes_for(len(grp))
-        tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], m, W)
+        tables, max_p = _group_tables(grp, costs[g0:g0 + lanes], m, W)
         groups.append((g0, len(grp), W, tables, max_p, t.zeros((4 * W, C), dtype=t.int64, device=dev)))
 
     def launch(planes, stride, t0, t1, bounds):
@@ -407,7 +426,8 @@ def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs
         # token-tiled for short chunks -- is the better way)
         m = trace.model
         fact_bytes = trace.n_chunks * (m.L * m.E if m else 0) * 8
-        method = "factorized" if len(placements) > MAX_LANES and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
+        lanes = pass_lanes(trace, _as_costs(costs, len(placements)))
+        method = "factorized" if len(placements) > lanes and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
     if method in ("gather", "count", "token", "pass"):
         sums = score_sums(trace, placements, costs, algo="auto" if method == "pass" else method)
     elif method == "factorized":
@@ -462,7 +482,7 @@ def evaluate_batch(trace: ActivationTrace, assign, costs, method: str = "auto") 
     a = a.to(dev, non_blocking=a.is_pinned())
     if method == "auto":
         fact_bytes = trace.n_chunks * m.L * m.E * 8
-        method = "factorized" if P > MAX_LANES and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
+        method = "factorized" if P > pass_lanes(trace, costs) and fact_bytes <= FACTORIZED_MAX_BYTES else "pass"
     if method == "factorized":
         pe = _pe_from_device_assign(a, costs, m)  # checks every assignment against its topology
         cnt = chunk_counts(trace)
@@ -497,8 +517,9 @@ def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement],
         raise MoeplaceError("evaluate: empty trace")
     if algo not in ALGOS:
         raise ConfigError(f"unknown score algorithm {algo!r}")
-    if not 1 <= len(placements) <= (4 if algo == "gather" else MAX_LANES):
-        raise ConfigError(f"evaluate_with_stats takes 1..{4 if algo == 'gather' else MAX_LANES} placements")
+    top = 4 if algo == "gather" else pass_lanes(trace, _as_costs(cost, len(placements)), algo, hist=True)
+    if not 1 <= len(placements) <= top:
+        raise ConfigError(f"evaluate_with_stats takes 1..{top} placements here")
     dev = _lib.require_cuda()
     W = _lanes_for(len(placements))
     tables, max_p = _group_tables(placements, _as_costs(cost, len(placements)), m, W)

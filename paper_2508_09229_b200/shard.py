@@ -147,12 +147,13 @@ def sharded_evaluate(model, zipf_s: float, n_tokens: int, n_chunks: int, seed: i
     every placement (``costs``: one CostMatrix or one per placement — several topologies can be
     mixed), all-reduce ONE packed int64 buffer, and return the global
     (FrequencyTable, [EvalReport]) — identical on every rank and to a one-GPU run.
-    Placements 0..15 ride the fused statistics pass; further ones are scored 16 per pass."""
+    The first 16 placements (32 where the count-contract kernel runs) ride the fused statistics
+    pass; further ones are scored 16 (32) per pass."""
     import torch
     import torch.distributed as dist
 
     from . import _lib
-    from .eval import MAX_LANES, _as_costs, _group_tables, _lanes_for, report_from_sums
+    from .eval import _as_costs, _group_tables, _lanes_for, pass_lanes, report_from_sums
     from .model_trace import chunk_bounds_even, frequencies_from_counts, generate_trace
 
     if rank is None or world is None:
@@ -174,19 +175,21 @@ def sharded_evaluate(model, zipf_s: float, n_tokens: int, n_chunks: int, seed: i
         bounds = _lib.to_dev(tr.chunk_bounds, torch.int64)
         err = _lib.new_err()
         sh = _lib.stream_handle()
-        head = placements[:MAX_LANES]
+        hl = pass_lanes(tr, costs, hist=True)  # 32 on the count-contract kernel (long chunks), else 16
+        head = placements[:hl]
         W = _lanes_for(len(head))
-        tables, max_p = _group_tables(head, costs[:MAX_LANES], model, W)
+        tables, max_p = _group_tables(head, costs[:hl], model, W)
         sums = torch.zeros((4 * W, n_chunks), dtype=torch.int64, device=dev)
         _lib.call("mp_hist_score_ex_u8", _lib.ptr(planes), stride, 0, b - a, model.L, model.K, model.E,
                   _lib.ptr(bounds), n_chunks, _lib.ptr(tables), W, max_p, _lib.ptr(pk.counts), _lib.ptr(sums),
                   _lib.ptr(err), 0, sh)
         _lib.check_err(err, "sharded_evaluate")
         pk.sums[:len(head)].copy_(sums[:len(head)])
-        for g0 in range(MAX_LANES, P, MAX_LANES):
-            grp = placements[g0:g0 + MAX_LANES]
+        lanes = pass_lanes(tr, costs)
+        for g0 in range(hl, P, lanes):
+            grp = placements[g0:g0 + lanes]
             W = _lanes_for(len(grp))
-            tables, max_p = _group_tables(grp, costs[g0:g0 + MAX_LANES], model, W)
+            tables, max_p = _group_tables(grp, costs[g0:g0 + lanes], model, W)
             gs = torch.zeros((4 * W, n_chunks), dtype=torch.int64, device=dev)
             _lib.call("mp_score_u8", _lib.ptr(planes), stride, 0, b - a, model.L, model.K, _lib.ptr(bounds), n_chunks,
                       _lib.ptr(tables), W, max_p, _lib.ptr(gs), sh)

@@ -85,6 +85,43 @@ def test_algorithms_agree_with_oracle(shape, W, cmax):
     _check(sub, sel[a:b], bounds[3:12], a, pls, p, W)
 
 
+@pytest.mark.parametrize("shape", [R1, B16, (5, 200, 7)])
+@pytest.mark.parametrize("nplace", [17, 24, 32])
+def test_count_contract_32_lanes(shape, nplace):
+    """W = 8 (up to 32 placements in one count-contract pass) == the oracle, with and without the
+    histogram, on whole traces and on a view; the other algorithms refuse W = 8 explicitly."""
+    L, E, K = shape
+    m = mt.ModelSpec(L, E, K)
+    N, C = 6007, 11
+    tr = mt.generate_trace(m, 1.2, N, C, 5)
+    sel, bounds = og.generate(L, E, K, 1.2, N, C, 5)
+    rng = np.random.default_rng(nplace)
+    p = rng.integers(0, 40, (L, 24)).astype(np.uint8)
+    pls = [mpl.Placement(random_assign(rng, L, E, 24)) for _ in range(nplace)]
+    tables, max_p = _tables(pls, p, m, 8)
+    want = np.zeros((32, C), np.int64)
+    for i, pl in enumerate(pls):
+        want[i] = oracle_sums(sel, p, pl.assign, bounds, 0)
+    for algo in (AUTO, COUNT):
+        s, _, _ = _run(tr, tables, 8, max_p, algo, hist=False)
+        assert np.array_equal(s, want), algo
+        s, c, e = _run(tr, tables, 8, max_p, algo, hist=True)
+        assert np.array_equal(s, want) and np.array_equal(c, ost.counts(sel, m.E)) and e[0] == 0, algo
+    sub = tr.view(2, 9)
+    a, b = int(bounds[2]), int(bounds[9])
+    s, _, _ = _run(sub, tables, 8, max_p, AUTO, hist=False)
+    for i, pl in enumerate(pls):
+        assert np.array_equal(s[i], oracle_sums(sel[a:b], p, pl.assign, bounds[2:10], a)), i
+    from paper_2508_09229_b200 import _lib
+    import torch
+    P_ = _lib.ptr(tr.planes)
+    for algo in (GATHER, TOKEN, SEG):
+        assert _lib.load().mp_score_ex_u8(P_, tr.planes.shape[1], 0, N, L, K, _lib.ptr(_lib.to_dev(tr.chunk_bounds,
+                                          torch.int64)), C, _lib.ptr(tables), 8, max_p,
+                                          _lib.ptr(torch.zeros((32, C), dtype=torch.int64, device="cuda")), algo,
+                                          None) == 3
+
+
 def test_algorithms_agree_on_empty_chunks_and_large_costs():
     L, E, K = B16
     m = mt.ModelSpec(L, E, K)

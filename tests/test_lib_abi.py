@@ -143,3 +143,6 @@ def test_auto_algorithm_rule():
     # SEG needs K = 8 and costs <= 31; otherwise the token walk / streaming algorithms apply
     assert _lib.choose_algo(False, 1, N, 71_429, L, K, 40) in ("token", "gather")
     assert _lib.choose_algo(True, 1, N, 150, L, 6, 8) == "count"
+    # 32 placements per pass (W = 8): the count-contract kernel at every shape
+    assert _lib.choose_algo(False, 8, N, 71_429, L, K, 8) == "count"
+    assert _lib.choose_algo(True, 8, N, 150, L, K, 8) == "count"

@@ -36,14 +36,14 @@ order = topo.locality_order(g, d)
 attn = mt.default_attention_placement(m, order)
 cost = mpl.cost_matrix(d, attn)
 c = mpl.Constraints(64, 1)
-pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c)] * 8
+pls = [mpl.place_round_robin(m, attn, order, c), mpl.place_greedy(m, attn, cost, c)] * 16
 tr = mt.generate_trace(m, a.s, a.tokens, a.chunks, 0)
 P, st = tr.planes, tr.planes.shape[1]
 C = tr.n_chunks
 b = _lib.to_dev(tr.chunk_bounds, torch.int64)
-tabs = {W: ev._group_tables(pls[:4 * W], [cost] * 4 * W, m, W) for W in (1, 2, 4)}
+tabs = {W: ev._group_tables(pls[:4 * W], [cost] * 4 * W, m, W) for W in (1, 2, 4, 8)}
 cnt = torch.zeros(L * E, dtype=torch.int64, device="cuda")
-s = torch.zeros(16 * C, dtype=torch.int64, device="cuda")
+s = torch.zeros(32 * C, dtype=torch.int64, device="cuda")
 err = _lib.new_err()
 sh = _lib.stream_handle()
 
@@ -103,7 +103,7 @@ for w in (a.only.split(",") if a.only else ("hist", "score1", "score2", "score4"
     base = w
     for suf in ("_gather", "_count", "_token", "_seg"):
         base = base[:-len(suf)] if base.endswith(suf) else base
-    fn = run if base in ("hist", "score1", "score2", "score4", "fused", "fused2", "fused4") else run_ext
+    fn = run if base in ("hist", "score1", "score2", "score4", "score8", "fused", "fused2", "fused4", "fused8") else run_ext
     s.zero_()
     cnt.zero_()
     fn(w)
