@@ -226,10 +226,17 @@ def test_public_api_algorithms_and_wide_stats_pass():
             f, reps = ev.evaluate_with_stats(tr, pls[:n], costs[:n], algo=algo)
             assert np.array_equal(f.counts, ost.counts(sel, E))
             assert [r.chunk_hop_sums for r in reps] == want[:n].tolist(), (n, algo)
+    # count-contract passes take 32 placements (W = 8); AUTO on these short chunks takes 16
+    f, reps = ev.evaluate_with_stats(tr, pls[:20], costs[:20], algo="count")
+    assert np.array_equal(f.counts, ost.counts(sel, E))
+    assert [r.chunk_hop_sums for r in reps] == want[:20].tolist()
+    assert ev.pass_lanes(tr, costs, "count") == 32 and ev.pass_lanes(tr, costs, "auto") == 16
     with pytest.raises(ConfigError):
         ev.evaluate_with_stats(tr, pls[:5], costs[:5], algo="gather")
     with pytest.raises(ConfigError):
         ev.evaluate_with_stats(tr, pls[:17], costs[:17])
+    with pytest.raises(ConfigError):
+        ev.evaluate_with_stats(tr, (pls * 2)[:33], (costs * 2)[:33], algo="count")
 
 
 def test_evaluate_batch_matches_evaluate_many():

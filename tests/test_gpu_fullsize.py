@@ -107,7 +107,7 @@ def test_config2_full_size_counts_and_hop_sums(config2, oracle_r1):
 def test_config3_six_topologies_full_size(config2, oracle_r1):
     """BASELINE config 3: R1 at 10M tokens on FatTree, FatTreeHier, Dragonfly, DragonflySparse,
     DragonflyPlus (16 x 4 x 4) and SlimFly (18 leaves x 4 x 4) -- 24 placements (4 methods each)
-    scored in one batch (factorized) and as W = 4 + W = 2 passes, against the oracle."""
+    scored as one 32-lane count-contract pass (what AUTO runs) and factorized, against the oracle."""
     tr, freq = config2[0], config2[1]
     bounds = mt.chunk_bounds_even(N2, C2)
     pls, costs, pes = [], [], []
@@ -123,7 +123,8 @@ def test_config3_six_topologies_full_size(config2, oracle_r1):
             costs.append(cost)
             pes.append(oe.pe_table(p, pl.assign))
     _, want = oe.fused_pass(oracle_r1, pes, bounds, E)
-    for method in ("auto", "pass"):
+    assert ev.pass_lanes(tr, costs) == 32
+    for method in ("factorized", "auto"):
         reps = ev.evaluate_many(tr, pls, costs, method=method)
         assert np.array_equal(np.array([r.chunk_hop_sums for r in reps]), want), method
     # ILPLoad is the best of the four methods on every topology (train == test == full trace here)
