@@ -3,7 +3,7 @@
 ``evaluate`` / ``evaluate_many`` score placements on the GPU: the placements' per-expert
 round-trip hop costs pe_q[l, e] = p[l, assign_q[l, e]] are packed into u8 lanes
 (``mp_pack_tables``) and ``mp_score_u8`` streams the trace once per group of up to 16
-placements, gathering pe_q for every (token, layer, pick) and reducing exact int64 hop sums per
+placements (32 where the count-contract kernel runs, see ``pass_lanes``), gathering pe_q for every (token, layer, pick) and reducing exact int64 hop sums per
 chunk.  The host derives the report floats from those integers with numpy (the oracle runs the
 same float code on its own integers, so reports are bit-identical, not merely within 1e-6).
 """
@@ -244,7 +244,7 @@ ALGOS = {"auto": 0, "gather": 1, "count": 2, "token": 3, "seg": 4}  # include/mo
 
 def score_sums(trace: ActivationTrace, placements: Sequence[Placement], costs, algo: str = "auto") -> np.ndarray:
     """Exact per-chunk hop sums, int64 [P, C], computed on the GPU (``mp_score_ex_u8``), up to 16
-    placements per pass.  ``algo``: "gather" (per-byte table lookups), "count" (count-contract:
+    placements per pass (32 per count-contract pass, ``pass_lanes``).  ``algo``: "gather" (per-byte table lookups), "count" (count-contract:
     per-(layer, chunk) histograms contracted with the tables), "token" (token-tiled: per-token sums
     across layers reduced per chunk; cost independent of the chunk count), "seg" (segmented gather:
     warps own contiguous token ranges and reduce at each chunk boundary; C-independent, K = 8 and
@@ -414,7 +414,7 @@ def score_sums_factorized(trace: ActivationTrace, placements: Sequence[Placement
 def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs,
                   method: str = "auto") -> list[EvalReport]:
     """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies),
-    extension A18.  ``method``: "gather" / "count" / "token" — passes of up to 16 placements with
+    extension A18.  ``method``: "gather" / "count" / "token" — passes of up to 16 (count: 32) placements with
     that algorithm; "factorized" — one per-chunk histogram pass + tensor-core contraction for any
     number of placements; "auto" — passes (the library picks the algorithm per pass) when P <= 16
     or the per-chunk counts would exceed FACTORIZED_MAX_BYTES, factorized otherwise.  All give
@@ -507,7 +507,8 @@ def evaluate(trace: ActivationTrace, placement: Placement, cost: CostMatrix) -> 
 
 def evaluate_with_stats(trace: ActivationTrace, placements: Sequence[Placement], cost, algo: str = "auto"):
     """One fused pass (``mp_hist_score_ex_u8``): the trace's FrequencyTable plus the EvalReports of
-    up to 16 placements (``cost``: one CostMatrix or one per placement).  Used for the train
+    up to 16 placements, 32 where the pass runs count-contract (``pass_lanes``; ``cost``: one
+    CostMatrix or one per placement).  Used for the train
     split, where the ILPLoad frequencies and the train-side metric come from the same tokens.
     ``algo`` as in ``score_sums`` ("gather" takes at most 4 placements)."""
     t = _lib.torch()
