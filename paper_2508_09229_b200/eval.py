@@ -416,8 +416,9 @@ def evaluate_many(trace: ActivationTrace, placements: Sequence[Placement], costs
     """Batched ``evaluate`` over placements (and per-placement cost matrices, i.e. topologies),
     extension A18.  ``method``: "gather" / "count" / "token" — passes of up to 16 (count: 32) placements with
     that algorithm; "factorized" — one per-chunk histogram pass + tensor-core contraction for any
-    number of placements; "auto" — passes (the library picks the algorithm per pass) when P <= 16
-    or the per-chunk counts would exceed FACTORIZED_MAX_BYTES, factorized otherwise.  All give
+    number of placements; "auto" — passes (the library picks the algorithm per pass) when P fits one
+    pass (``pass_lanes``: 32 on long chunks, 16 on short ones) or the per-chunk counts would exceed
+    FACTORIZED_MAX_BYTES, factorized otherwise.  All give
     identical integers."""
     placements = list(placements)
     if method == "auto":
