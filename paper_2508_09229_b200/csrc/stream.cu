@@ -482,8 +482,12 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
                                            uint32_t tid) {
   const int64_t ha = min(xb, (xa + 15) & ~(int64_t)15);
   const int64_t tb = max(ha, xb & ~(int64_t)15);
-  for (int64_t x = xa + tid; x < ha; x += T) atoms_inc(sb + (uint32_t)plane[x] * ROW);
-  for (int64_t x = tb + tid; x < xb; x += T) atoms_inc(sb + (uint32_t)plane[x] * ROW);
+  // the < 16 unaligned bytes at each end (one per thread, T >= 16): loaded now, counted after the
+  // vectors -- counting them first put two dependent load round trips ahead of warp 0's vector
+  // loads at every piece, and the pipelined flush then waited for warp 0 every piece
+  // packed into one register (bits 0-8 head, 16-24 tail; 0x100 = none) to stay off the loop's budget
+  const uint32_t ends = (xa + tid < ha ? (uint32_t)__ldg(plane + xa + tid) : 0x100u) |
+                        ((tb + tid < xb ? (uint32_t)__ldg(plane + tb + tid) : 0x100u) << 16);
   const int4* __restrict__ pv = reinterpret_cast<const int4*>(plane + ha);
   const uint32_t nv = (uint32_t)((tb - ha) >> 4);
   auto vec = [&](const int4& x) {
@@ -521,6 +525,8 @@ __device__ __forceinline__ void pipe_count(const uint8_t* __restrict__ plane, in
   }
   for (; v < nv; v += T) vec(ldg_stream(pv + v));
 #endif
+  if (!(ends & 0x100u)) atoms_inc(sb + (ends & 0xffu) * ROW);
+  if (!(ends & 0x1000000u)) atoms_inc(sb + ((ends >> 16) & 0xffu) * ROW);
 }
 
 // WC == 0: per-chunk histogram, counts is int64 [C][L][E].  WC > 0: count-contract with WC-word
@@ -529,7 +535,8 @@ template <int WC, int UNROLL, int kPipeSets, class Shape>
 __global__ void __launch_bounds__(Shape::kThreads, 1024 / Shape::kThreads)
 pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
             const int64_t* __restrict__ bounds, int C, const uint32_t* __restrict__ tables,
-            int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err) {
+            int64_t* __restrict__ counts, int64_t* __restrict__ hop_sums, int64_t* __restrict__ err,
+            unsigned stagger_ns) {
   constexpr int kPipeWT = Shape::kWT, kPipeHalves = Shape::kHalves;
   constexpr int kPipeRow = Shape::kRow, kPipeSetBytes = Shape::kSetBytes;
   extern __shared__ __align__(128) uint8_t sm[];  // kPipeSets x 256 rows x kPipeRow B
@@ -545,6 +552,10 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
   if (tid == 0)
     for (int b = 0; b < kPipeSets; ++b) mbar_init(bar0 + 8 * b, kPipeWT);
   __syncthreads();
+  // one 1024-thread worker: its upper half starts stagger_ns later, so the halves reach the piece
+  // boundaries (where a warp's loads have drained) out of phase and the SM keeps loads in flight
+  // (they may drift apart by up to a piece: the pipelined flush allows it)
+  if (stagger_ns && tid >= (uint32_t)kPipeWT / 2) __nanosleep(stagger_ns);
 
   // flush roles: two threads per bin (16 replicas each, rotated: a warp's 32 loads hit 32 banks)
   const int fe = (int)(tid >> 1), fh = (int)(tid & 1);
@@ -646,11 +657,17 @@ pipe_kernel(const uint8_t* __restrict__ planes, int64_t stride, int64_t t0, int6
 }
 
 constexpr int64_t kTwoSetPiece = 128 * 1024;  // crossover measured between 133 KB (C = 600) and 89 KB
+// Long pieces: ONE 1024-thread worker per SM whose three 32 KB sets sit below 96 KB, its halves
+// staggered by kStaggerNs (R1 10M: C = 150 / 533 KB pieces: fused step 0.809 -> 0.781 ms, C = 50:
+// 0.755 -> 0.692 ms; at C = 300 / 267 KB pieces two 512-thread workers stay faster, 0.878 vs 0.901;
+// profiles/r2_pipe_single_stagger.txt)
+constexpr int64_t kSingleWorkerPiece = 400 * 1024;
+constexpr unsigned kStaggerNs = 4000;
 
 template <int WC, int SETS, class Shape = PipeCC>
 static cudaError_t launch_pipe_t(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                                  const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
-                                 int64_t* hop_sums, int64_t* err, cudaStream_t s) {
+                                 int64_t* hop_sums, int64_t* err, cudaStream_t s, unsigned stagger_ns = 0) {
   auto kern = pipe_kernel<WC, MP_COUNT_UNROLL, SETS, Shape>;
   constexpr int smem = SETS * Shape::kSetBytes;
   int per_sm = 0;
@@ -664,7 +681,7 @@ static cudaError_t launch_pipe_t(const uint8_t* planes, int64_t stride, int64_t 
   const int64_t min_bytes_per_cta = 64 * 1024 * Shape::kHalves;
   grid = max((int64_t)1, min(grid, (total + min_bytes_per_cta - 1) / min_bytes_per_cta));
   kern<<<(unsigned)grid, Shape::kThreads, smem, s>>>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts,
-                                                     hop_sums, err);
+                                                     hop_sums, err, stagger_ns);
   return cudaGetLastError();
 }
 
@@ -673,6 +690,9 @@ static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0
                                const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                                int64_t* hop_sums, int64_t* err, cudaStream_t s) {
   const int64_t piece = (t1 - t0) * (int64_t)K / (bounds ? C : 1);  // average (layer, chunk) piece
+  if (piece >= kSingleWorkerPiece)  // one 1024-thread worker, three 32 KB sets, staggered halves
+    return launch_pipe_t<WC, 3, PipeHist>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s,
+                                          kStaggerNs);
 #ifdef MP_PIPE_FORCE_SETS
   if (MP_PIPE_FORCE_SETS == 2)
 #else
