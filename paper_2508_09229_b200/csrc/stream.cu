@@ -444,7 +444,6 @@ static cudaError_t launch_t(const uint8_t* planes, int64_t stride, int64_t t0, i
 // ~30 % slower (tools/microbench11.cu, profiles/r2_smem_atoms.txt).  The launcher takes 2 sets for
 // pieces of >= kTwoSetPiece bytes on average (R1 10M / 150 chunks, 533 KB pieces: fused step
 // 0.845 -> 0.805 ms) and 3 for shorter ones (1500 chunks: 1.215 vs 1.335 ms with 2 sets).
-constexpr int kPipeSetsMax = 3;
 constexpr int kPipeHalves = MP_PIPE_SPLIT ? 2 : 1;  // workers per CTA (count-contract, per-chunk histogram)
 // A CTA of HALVES workers of WT threads; one set = 256 expert rows of HALVES x 128 bytes (worker h's
 // 32 lane replicas at bytes h*128 .. h*128+127 of each row).
@@ -685,11 +684,93 @@ static cudaError_t launch_pipe_t(const uint8_t* planes, int64_t stride, int64_t 
   return cudaGetLastError();
 }
 
+// {span, non-empty chunks} of a chunk-bounds array, written to host-mapped memory
+__global__ void chunk_stats_kernel(const int64_t* __restrict__ bounds, int C, int64_t* out) {
+  __shared__ int part[32];
+  int n = 0;
+  for (int i = threadIdx.x; i < C; i += blockDim.x) n += __ldg(bounds + i + 1) > __ldg(bounds + i);
+  n = __reduce_add_sync(0xffffffffu, n);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    out[0] = __ldg(bounds + C) - __ldg(bounds);
+    out[1] = t;
+  }
+}
+
+// Average bytes per NON-EMPTY (layer, chunk) piece, which picks the kernel shape (results never
+// depend on it).  (t1 - t0) * K / C is right for a whole trace, but a shard of a larger trace keeps
+// every chunk of the global bounds, clipped (rank r of G sees C / G non-empty chunks), which would
+// make the pieces look G times shorter.  So the first call with a given bounds array launches a
+// one-block kernel on the launch stream that counts the non-empty chunks into host-mapped memory;
+// later calls use that count once its event has completed (a query, never a wait).  Entries are
+// keyed by (device, pointer, C); a reused pointer with other contents can only cost speed.
+static int64_t avg_piece_bytes(const int64_t* bounds, int C, int64_t t0, int64_t t1, int K, cudaStream_t s) {
+  const int64_t est = (t1 - t0) * (int64_t)K / (bounds ? C : 1);
+  if (!bounds || C <= 1) return est;
+  constexpr int kSlots = 256;
+  struct Entry {
+    int slot;
+    cudaEvent_t ev;
+  };
+  static std::mutex mu;
+  static std::map<std::tuple<int, const int64_t*, int>, Entry> cache;
+  static int64_t* pool = nullptr;  // host-mapped, 2 words per slot
+  static int used = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_tuple(dev, bounds, C);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    if (cudaEventQuery(it->second.ev) != cudaSuccess) {
+      cudaGetLastError();  // not ready yet
+      return est;
+    }
+    const volatile int64_t* h = pool + 2 * it->second.slot;
+    const int64_t span = h[0], nonempty = h[1];
+    return (span > 0 && nonempty > 0) ? span * (int64_t)K / nonempty : est;
+  }
+  if (!pool && cudaHostAlloc((void**)&pool, 2 * kSlots * sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable) !=
+                   cudaSuccess) {
+    cudaGetLastError();
+    pool = nullptr;
+    return est;
+  }
+  if (used == kSlots) {  // bounded: start over (the next calls re-count)
+    for (auto& kv : cache) {
+      cudaEventSynchronize(kv.second.ev);
+      cudaEventDestroy(kv.second.ev);
+    }
+    cache.clear();
+    used = 0;
+  }
+  Entry e{used, nullptr};
+  int64_t* d = nullptr;
+  if (cudaHostGetDevicePointer((void**)&d, pool + 2 * e.slot, 0) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e.ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    if (e.ev) cudaEventDestroy(e.ev);
+    return est;
+  }
+  chunk_stats_kernel<<<1, 256, 0, s>>>(bounds, C, d);
+  if (cudaGetLastError() != cudaSuccess || cudaEventRecord(e.ev, s) != cudaSuccess) {
+    cudaGetLastError();
+    cudaEventDestroy(e.ev);
+    return est;
+  }
+  ++used;
+  cache.emplace(key, e);
+  return est;
+}
+
 template <int WC>
 static cudaError_t launch_pipe(const uint8_t* planes, int64_t stride, int64_t t0, int64_t t1, int L, int K, int E,
                                const int64_t* bounds, int C, const uint32_t* tables, int64_t* counts,
                                int64_t* hop_sums, int64_t* err, cudaStream_t s) {
-  const int64_t piece = (t1 - t0) * (int64_t)K / (bounds ? C : 1);  // average (layer, chunk) piece
+  const int64_t piece = avg_piece_bytes(bounds, C, t0, t1, K, s);  // average (layer, chunk) piece
   if (piece >= kSingleWorkerPiece)  // one 1024-thread worker, three 32 KB sets, staggered halves
     return launch_pipe_t<WC, 3, PipeHist>(planes, stride, t0, t1, L, K, E, bounds, C, tables, counts, hop_sums, err, s,
                                           kStaggerNs);
