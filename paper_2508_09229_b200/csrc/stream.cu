@@ -454,11 +454,12 @@ struct PipeShape {
   static constexpr int kSetBytes = 256 * kRow;
 };
 using PipeCC = PipeShape<kThreads, kPipeHalves>;  // count-contract / per-chunk histogram: 2 x 512 threads
-// The plain histogram (one chunk: pieces end only at layer ends, a handful of flushes) runs ONE
-// 1024-thread worker whose three 32 KB sets all sit below 96 KB of shared memory: 0.769 -> 0.726 ms
-// for 10M R1 tokens (98.9 % of HBM); with short pieces the single worker is slower (one piece at a
-// time for the whole SM: 1500 chunks 1.20 -> 1.57 ms), so the chunked instances keep two workers
-// (profiles/r2_pipe_workers.txt).
+// ONE 1024-thread worker whose three 32 KB sets all sit below 96 KB of shared memory: the plain
+// histogram (one chunk: a handful of flushes; 0.769 -> 0.726 ms for 10M R1 tokens, 98.9 % of HBM)
+// and the chunked instances when their pieces average >= kSingleWorkerPiece, there with the two
+// halves staggered (see launch_pipe).  With short pieces the single worker is slower (one piece at
+// a time for the whole SM: 1500 chunks 1.20 -> 1.57 ms), so those keep two 512-thread workers
+// (profiles/r2_pipe_workers.txt, r2_pipe_single_stagger.txt).
 using PipeHist = PipeShape<1024, 1>;
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
