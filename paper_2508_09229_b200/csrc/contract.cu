@@ -468,10 +468,22 @@ __global__ void count_digits_u8_kernel(const int64_t* __restrict__ counts, int C
   for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i0 < ldd;
        i0 += (int64_t)gridDim.x * blockDim.x * 8) {
     uint64_t w[4] = {0, 0, 0, 0};
+    int64_t vv[8];
+    if (i0 + 8 <= LE && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {  // 16-byte loads when the row is aligned
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        const longlong2 p = __ldg(reinterpret_cast<const longlong2*>(row + i0 + k));
+        vv[k] = p.x;
+        vv[k + 1] = p.y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) vv[k] = i0 + k < LE ? __ldg(row + i0 + k) : 0;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int64_t i = i0 + k;
-      int64_t v = i < LE ? __ldg(row + i) : 0;
+      int64_t v = vv[k];
       if (v < 0 || (sh < 64 && (v >> sh) != 0)) {
         report_err(err, MP_DATA_EXPERT_RANGE, c, i);
         v = 0;
