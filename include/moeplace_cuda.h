@@ -12,7 +12,10 @@
  *     caller owns every buffer (inputs, outputs, scratch).  The library never allocates or
  *     frees device memory; its only global state is a mutex-guarded cache of per-device launch
  *     facts (SM count, each kernel's resident CTAs, its shared-memory attribute), filled on a
- *     device's first launch.  Safe to call concurrently on different streams.
+ *     device's first launch, and a 4 KB pinned host-mapped table of {span, non-empty chunks} per
+ *     chunk-bounds array seen by the count-contract launchers (filled by a one-block kernel on the
+ *     caller's stream, read without a wait; it picks a kernel shape, never changes a result).
+ *     Safe to call concurrently on different streams.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
  *     function only ENQUEUES work; nothing synchronises the host.
  *   - Integer outputs are ACCUMULATED (`+=`): the caller zeroes them.  This makes sharded
