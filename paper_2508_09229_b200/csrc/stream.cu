@@ -902,7 +902,14 @@ cudaError_t launch_stream(bool hist, int W, int max_p, const uint8_t* planes, in
 #else
   if (W == 0) return launch_hist_chunks(planes, stride, t0, t1, L, K, E, nullptr, 1, counts, err, s);
 #endif
-  const int chosen = choose_algo(hist, W, algo, t1 - t0, C, L, K, max_p);
+  // AUTO decides by tokens per chunk; a shard of a larger trace carries the global (clipped) chunk
+  // list, so count only its non-empty chunks (avg_piece_bytes: cached, never waits)
+  int C_eff = C;
+  if (algo == MP_ALGO_AUTO && bounds && C > 1 && K > 0) {
+    const int64_t piece = avg_piece_bytes(bounds, C, t0, t1, K, s);
+    if (piece > 0) C_eff = (int)std::max<int64_t>(1, std::min<int64_t>(C, (t1 - t0) * K / piece));
+  }
+  const int chosen = choose_algo(hist, W, algo, t1 - t0, C_eff, L, K, max_p);
   if (chosen == MP_ALGO_SEG)
     return launch_seg(hist, W, planes, stride, t0, t1, L, E, bounds, C, tables, counts, hop_sums, err, s);
   if (chosen == MP_ALGO_TOKEN) {
