@@ -146,3 +146,25 @@ def test_auto_algorithm_rule():
     # 32 placements per pass (W = 8): the count-contract kernel at every shape
     assert _lib.choose_algo(False, 8, N, 71_429, L, K, 8) == "count"
     assert _lib.choose_algo(True, 8, N, 150, L, K, 8) == "count"
+
+
+def test_pass_lanes_rule():
+    """eval.pass_lanes (host-only): 32 placements per pass where the library's AUTO picks the
+    count-contract kernel (long chunks) or count is forced, 16 otherwise."""
+    import types
+
+    import torch
+
+    from paper_2508_09229_b200 import eval as ev
+    from paper_2508_09229_b200.model_trace import ModelSpec
+    from paper_2508_09229_b200.placement import CostMatrix
+    m = ModelSpec(58, 256, 8)
+    cost = CostMatrix(torch.full((58, 32), 6, dtype=torch.uint8))
+    long_chunks = types.SimpleNamespace(model=m, n_tokens=10_000_000, n_chunks=150)
+    dialog = types.SimpleNamespace(model=m, n_tokens=10_000_000, n_chunks=71_429)
+    assert ev.pass_lanes(long_chunks, cost) == 32
+    assert ev.pass_lanes(long_chunks, [cost] * 3, hist=True) == 32
+    assert ev.pass_lanes(dialog, cost) == 16
+    assert ev.pass_lanes(dialog, cost, "count") == 32
+    assert ev.pass_lanes(long_chunks, cost, "gather") == 16
+    assert ev._lanes_for(4) == 1 and ev._lanes_for(16) == 4 and ev._lanes_for(17) == 8 and ev._lanes_for(32) == 8
